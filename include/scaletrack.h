@@ -1,0 +1,216 @@
+/*
+ * scaletrack.h — C ABI of the B200-native SCALE-TRACK hot path
+ * (arXiv 2603.26691, "SCALE-TRACK: Asynchronous Euler-Lagrange particle
+ * tracking on heterogeneous computing architecture").
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * C-n = reading n in DESIGN.md §3 (where the paper is silent or ambiguous).
+ *
+ * What the library computes (one "particle step"):
+ *   for every particle p and every sub-step of length dt:
+ *     1. locate the cell of x_p                              (C-6)
+ *     2. interpolate the fluid velocity u_f at x_p           (C-5)
+ *     3. integrate Newton's law with drag (+ gravity)        (Eq. 9-10, C-1..C-4)
+ *     4. deposit the drag reaction into the start cell       (Eq. 11, C-8..C-10)
+ *     5. apply wall reflection / periodic wrap               (C-11, C-12)
+ *     6. relocate to cell and chunk; rebin the SoA store     (C-14..C-16)
+ *
+ * Conventions shared by every entry point
+ *   - Every call returns st_status; ST_OK == 0.  No C++ exception crosses the ABI.
+ *     On error a message is kept per context (st_last_error).  CUDA errors are
+ *     sticky: after ST_ERR_CUDA the context only accepts st_destroy.
+ *   - Units are SI.  State is IEEE binary32 (C-19).
+ *   - Array arguments are caller-owned.  Pointers may be host (pageable or
+ *     pinned) or device memory of the context's GPU; the kind is detected with
+ *     cudaPointerGetAttributes.  Device inputs are consumed in order on
+ *     cfg.stream; host inputs are copied before the call returns.
+ *   - Vectors are structure-of-arrays: x[3][n] means x[0..n) = x-components,
+ *     x[n..2n) = y, x[2n..3n) = z.  Fields are [3][nz][ny][nx], x fastest.
+ *   - Cell linear index: (cz*ny + cy)*nx + cx (global indices).
+ *     Chunk id: (kz*NCy + ky)*NCx + kx with k_d = c_d / chunk_cells,
+ *     NC_d = ceil(n_d / chunk_cells)                          (C-14)
+ *   - Threading: one context per (process, GPU); calls on one context must
+ *     not be concurrent.
+ *   - Multi-GPU (nranks > 1): one process per GPU; rank r owns the z-slab of
+ *     chunk planes [floor(r*NCz/G), floor((r+1)*NCz/G)) (C-16).  Calls marked
+ *     "collective" must be made by every rank in the same order.
+ */
+#ifndef SCALETRACK_H
+#define SCALETRACK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_ABI_VERSION 1
+
+typedef struct st_ctx st_ctx;   /* opaque; owns the particle store, fields, sources */
+typedef int32_t st_status;
+
+enum {
+  ST_OK = 0,
+  ST_ERR_INVALID_ARG = 1,   /* bad pointer / size / config value ("contract violation") */
+  ST_ERR_STATE = 2,         /* call out of order (e.g. st_advance before any field) */
+  ST_ERR_CAPACITY = 3,      /* store capacity exceeded */
+  ST_ERR_OUT_OF_DOMAIN = 4, /* injected particle outside [lo, hi] (S:60 outside-marker) */
+  ST_ERR_CFL = 5,           /* displacement precondition violated ("never silent") */
+  ST_ERR_CUDA = 6,          /* CUDA runtime error (sticky) */
+  ST_ERR_NCCL = 7,          /* NCCL error */
+  ST_ERR_OOM = 8,           /* device allocation failed */
+  ST_ERR_UNSUPPORTED = 9    /* feature not built / not available on this device */
+};
+
+enum { ST_BC_PERIODIC = 0, ST_BC_REFLECT = 1 };                 /* C-11, C-12 */
+enum { ST_DRAG_STOKES = 0, ST_DRAG_SCHILLER_NAUMANN = 1 };      /* C-2 */
+enum { ST_INT_EXPONENTIAL = 0, ST_INT_SEMI_IMPLICIT = 1 };      /* C-4 */
+enum { ST_ONE_WAY = 0, ST_TWO_WAY = 1 };
+
+/*
+ * Configuration.  Fill with st_config_default() and override.
+ *   dims, origin, cell_size : uniform Cartesian cell-centred mesh.
+ *   chunk_cells             : edge of a cubic chunk in cells (8 -> 8^3-cell chunks, C-14).
+ *   bc[3]                   : ST_BC_* per axis (both faces of an axis share the rule).
+ *   rho_f, nu_f, rho_p      : fluid density, kinematic viscosity, particle density.
+ *   gravity[3]              : body acceleration on particles (C-1; (0,0,0) = paper's
+ *                             "only the drag force").
+ *   drag_law, integrator, coupling : ST_DRAG_*, ST_INT_*, ST_ONE_WAY/ST_TWO_WAY.
+ *   rebin_interval (K >= 1) : the store is stable-sorted by chunk after the last
+ *                             sub-step of every K-th st_advance call (C-15).
+ *   capacity                : maximum particles resident on this rank.
+ *   device                  : CUDA ordinal; stream: cudaStream_t (NULL = library's own).
+ *   rank, nranks            : position in the one-box job (nranks == 1: single GPU).
+ *   nccl_unique_id          : 128-byte ncclUniqueId broadcast by the caller (nranks > 1).
+ */
+typedef struct {
+  int32_t abi_version;
+  int32_t dims[3];
+  double origin[3];
+  double cell_size[3];
+  int32_t chunk_cells;
+  int32_t bc[3];
+  double rho_f, nu_f, rho_p;
+  double gravity[3];
+  int32_t drag_law, integrator, coupling;
+  int32_t rebin_interval;
+  int64_t capacity;
+  int32_t device;
+  void* stream;
+  int32_t rank, nranks;
+  const void* nccl_unique_id;
+} st_config;
+
+/* Geometry of this rank's share of the mesh (filled by st_get_layout). */
+typedef struct {
+  int32_t z0, z1;            /* owned cell planes [z0, z1) (global z index)          */
+  int32_t kz0, kz1;          /* owned chunk planes [kz0, kz1)                         */
+  int32_t n_chunks_global;   /* NCx*NCy*NCz                                           */
+  int32_t nchunk[3];         /* NCx, NCy, NCz                                         */
+  int64_t local_cells;       /* nx*ny*(z1-z0): size of one component of st_get_sources */
+  int32_t halo_cells;        /* z-halo planes kept on each side (0 when nranks == 1)   */
+} st_layout;
+
+/* Counters of the last rebin and running totals (filled by st_get_stats). */
+typedef struct {
+  int64_t n_particles;       /* resident on this rank                                 */
+  int64_t calls;             /* st_advance calls so far                               */
+  int64_t rebins;            /* rebins performed                                      */
+  int64_t last_movers;       /* particles that changed chunk in the last rebin        */
+  int64_t last_sent_total;   /* particles sent to other ranks in the last rebin       */
+  int64_t last_recv_total;   /* particles received in the last rebin                  */
+  int64_t fused_rebins;      /* rebins fused into the advance kernel                  */
+  int64_t kernel_launches;   /* kernels launched by the library so far                */
+} st_stats;
+
+/* Fill *cfg with defaults: 1 GPU, 16^3 unit box, periodic, chunk 8, air/water
+ * properties (rho_f 1.2, nu_f 1.5e-5, rho_p 1000), no gravity, Schiller-Naumann,
+ * exponential integrator, two-way, K = 1, capacity 1e6, device 0, NULL stream. */
+void st_config_default(st_config* cfg);
+
+/* Validate cfg, allocate the store (2 x capacity x 40 B), fields and source
+ * buffers, create streams/events; nranks > 1: ncclCommInitRank (collective).
+ * *out receives the context; on failure *out is NULL and the status says why. */
+st_status st_init(const st_config* cfg, st_ctx** out);
+
+/* Free everything.  NULL is accepted. */
+st_status st_destroy(st_ctx* ctx);
+
+/* Fluid state in ("receive the required states").  u = [3][z1-z0][ny][nx]
+ * fp32 cell-centre velocities of the cells this rank owns.  Asynchronous: the
+ * copy goes into the back buffer on the copy stream (it waits for the last
+ * st_advance still reading that buffer); the next st_advance uses it.  With
+ * nranks > 1 the halo planes are exchanged with the neighbour ranks (collective). */
+st_status st_set_fluid_field(st_ctx* ctx, const float* u);
+
+/* Append n particles in the given order ("particles are created directly
+ * on the GPUs").  x,u: [3][n]; d: [n] diameters (> 0); w: [n] parcel
+ * multiplicity or NULL = 1; id: [n] or NULL = auto ((rank<<40)+counter).
+ * Positions must satisfy lo <= x <= hi per axis, else ST_ERR_OUT_OF_DOMAIN and
+ * nothing is appended.  With nranks > 1 a particle may be injected on any rank;
+ * it migrates to its owner at the next rebin. */
+st_status st_inject(st_ctx* ctx, int64_t n, const float* x, const float* u,
+                    const float* d, const float* w, const uint64_t* id);
+
+/* Advance every particle by nsteps sub-steps of length dt (a fixed number
+ * of sub-steps, interpolated values refreshed once per sub-step), depositing
+ * two-way momentum sources.  Asynchronous (enqueued on the compute stream).
+ * Rebin/migration per C-15/C-16 (collective when nranks > 1). */
+st_status st_advance(st_ctx* ctx, double dt, int32_t nsteps);
+
+/* Momentum source out ("send ... the calculated sources"; Eq. 11).
+ * Closes the current accumulation interval (every st_advance enqueued so far)
+ * and writes S = acc / (V_cell * T_acc), the time-averaged fluid-side rate in
+ * N/m^3 (C-8, C-13), for the cells this rank owns ([3][z1-z0][ny][nx]), after
+ * adding halo deposits received from the neighbour ranks (collective).
+ * *interval_s (may be NULL) receives T_acc.  Blocks until S is written.
+ * st_get_sources == st_request_sources + st_wait_sources. */
+st_status st_get_sources(st_ctx* ctx, float* S, double* interval_s);
+
+/* Split form (asynchronous coupling buffer): request closes
+ * the interval and swaps the accumulation buffer, so st_advance calls made
+ * after it deposit into the other buffer while the readout runs on the copy
+ * stream; wait blocks until the readout is done and copies it into S. */
+st_status st_request_sources(st_ctx* ctx);
+st_status st_wait_sources(st_ctx* ctx, float* S, double* interval_s);
+
+/* Number of particles resident on this rank (after any pending rebin). */
+st_status st_get_count(st_ctx* ctx, int64_t* n);
+
+/* Copy out the store in store order (blocking).  Any output pointer may be
+ * NULL.  x,u: [3][cap] (component stride = cap); cell: global linear cell of
+ * x (C-6); chunk: chunk id.  *n_out receives the count; ST_ERR_CAPACITY if
+ * cap is too small (nothing copied). */
+st_status st_get_particles(st_ctx* ctx, int64_t cap, int64_t* n_out,
+                           float* x, float* u, float* d, float* w, uint64_t* id,
+                           int32_t* cell, int32_t* chunk);
+
+/* Locate n positions x[3][n] (host or device) with the kernel the store uses:
+ * cell and chunk per C-6 / C-14.  Used to check the integer contract. */
+st_status st_locate(st_ctx* ctx, int64_t n, const float* x, int32_t* cell, int32_t* chunk);
+
+/* Migration counts of the last rebin: row[dst] = particles this rank sent to dst
+ * (row[rank] = particles kept).  row has nranks entries. */
+st_status st_get_migration_counts(st_ctx* ctx, int64_t* row);
+
+st_status st_get_layout(st_ctx* ctx, st_layout* out);
+st_status st_get_stats(st_ctx* ctx, st_stats* out);
+
+/* Block until all work enqueued by this context has finished. */
+st_status st_sync(st_ctx* ctx);
+
+/* Time the most recent st_advance's kernels, in milliseconds, measured with
+ * CUDA events on the stream they were launched on (blocks on those events).
+ * advance_ms: the advance (+ fused rebin) kernel; rebin_ms: standalone rebin. */
+st_status st_last_timings(st_ctx* ctx, float* advance_ms, float* rebin_ms);
+
+/* Message of the last error on ctx ("" if none).  NULL ctx: last init error. */
+const char* st_last_error(const st_ctx* ctx);
+
+/* ABI version the library was built with (== ST_ABI_VERSION). */
+int32_t st_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCALETRACK_H */

@@ -1,0 +1,557 @@
+"""Pins of the CPU oracle against things other than itself.
+
+Each test names the pin (P-n), the passage it follows and what a plausible
+mistake in the oracle would break.  No expected value here comes from the CUDA
+path; closed forms are written from the mathematics, brute force is independent
+code (Python integers / fractions / sorted()).
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import Mesh, Physics, Sim
+
+RHO_F, NU_F, RHO_P = 1.2, 1.5e-5, 1000.0
+
+
+def tau_p(d):
+    return RHO_P * d * d / (18.0 * RHO_F * NU_F)
+
+
+def uniform_field(mesh, v, real=np.float64):
+    nx, ny, nz = mesh.dims
+    F = np.zeros((3, nz, ny, nx), real)
+    for a in range(3):
+        F[a] = v[a]
+    return F
+
+
+# ---------------------------------------------------------------- SPEC examples
+def test_spec_drag_examples(golden):
+    """zero slip -> no drag; Re -> 0 -> Stokes; C_D(1) = 27.6."""
+    g = golden["drag"]
+    f1 = oracle.drag_factor(g["Re"])
+    assert 24.0 / g["Re"] * f1 == pytest.approx(g["C_D"], rel=1e-12)
+    assert oracle.drag_factor(0.0) == 1.0                      # Stokes limit, no 0/0
+    assert oracle.drag_factor(5.0, law=oracle.DRAG_STOKES) == 1.0
+    # C-2: above Re = 1000, C_D = 0.44 -> f = 0.44 Re / 24
+    assert oracle.drag_factor(2000.0) == pytest.approx(0.44 * 2000 / 24, rel=1e-14)
+    # continuity gap at Re = 1000 (reading C-2): 1 + 0.15*1000^0.687 vs 0.44*1000/24
+    assert oracle.drag_factor(1000.0) == pytest.approx(1 + 0.15 * 1000 ** 0.687, rel=1e-14)
+    assert oracle.drag_factor(1000.0) < oracle.drag_factor(1000.0 + 1e-9)
+
+
+def test_spec_locate_examples(golden):
+    """S:61-64 locate_cell: midpoint, upper boundary -> last cell."""
+    g = golden["locate_cell"]
+    m = g["mesh"]
+    mesh = Mesh(dims=tuple(m["dims"]), origin=tuple(m["origin"]), cell_size=tuple(m["cell_size"]), chunk_cells=2)
+    sim = Sim(mesh, precision="f64")
+    for case in g["cases"]:
+        if case["cell"] is None:
+            with pytest.raises(ValueError):
+                sim.inject(np.array(case["x"]).reshape(3, 1), np.zeros((3, 1)), np.array([1e-5]))
+            continue
+        cell, chunk = sim.locate(np.array(case["x"], np.float64).reshape(3, 1))
+        cx, cy, cz = case["cell"]
+        assert cell[0] == (cz * 4 + cy) * 4 + cx
+        assert chunk[0] == ((cz // 2) * 2 + cy // 2) * 2 + cx // 2
+
+
+def test_spec_interpolation_examples(golden):
+    """constants reproduced; linear field: nodal value at a centre, mean midway."""
+    g = golden["interpolate_fields"]
+    mesh = Mesh(dims=(4, 4, 4), cell_size=(1.0, 1.0, 1.0), bc=(oracle.BC_REFLECT,) * 3, chunk_cells=2)
+    sim = Sim(mesh, precision="f64")
+    F = uniform_field(mesh, g["uniform"]["field"])
+    rng = np.random.default_rng(0)
+    x = rng.random((3, 200)) * 4.0
+    out = sim.interpolate(x, F)
+    assert np.max(np.abs(out[0] - 1.0)) < 4e-16 and np.all(out[1] == 0.0)   # to rounding (P-5)
+    F = np.zeros((3, 4, 4, 4))
+    F[0] = (np.arange(4) + 0.5)[None, None, :]
+    for case in g["linear_unit_mesh"]["cases"]:
+        v = sim.interpolate(np.array(case["x"], np.float64).reshape(3, 1), F)
+        assert v[0, 0] == pytest.approx(case["ux"], abs=1e-15)
+
+
+def test_spec_particle_mass(golden):
+    """(pi/6)*1000*(1e-5)^3 = 5.235987756e-13 kg (the mass the source uses, C-18)."""
+    g = golden["particle_mass"]
+    assert oracle.particle_mass(g["d_p"], g["rho_p"]) == pytest.approx(g["m_p"], rel=g["rtol"])
+
+
+def test_spec_chunk_momentum(golden):
+    """one parcel, multiplicity 50, m = 2e-12, u = (1,0,0) -> 1e-10."""
+    g = golden["chunk_momentum"]
+    p = g["multiplicity"] * g["m_p"] * np.array(g["u_p"], float)
+    assert np.allclose(p, g["p"], rtol=1e-12, atol=0)
+
+
+# ---------------------------------------------------------------- P-1 closed form
+@pytest.mark.parametrize("u0", [(0.0, 0.0, 0.0), (0.3, -0.1, 0.2)])
+def test_p1_stokes_relaxation_closed_form(u0):
+    """P-1: uniform flow + Stokes drag + gravity, ETD, periodic: exact
+    u(t) = u_s + (u0-u_s)e^{-t/tau}, x(t) = x0 + u_s t + tau (u0-u_s)(1-e^{-t/tau}),
+    u_s = u_f + g tau (BJ north_star: 1e-9 relative in fp64).  A wrong sign of
+    g, a wrong tau, a dropped position term or E/M swapped all fail."""
+    mesh = Mesh(dims=(16, 16, 16), cell_size=(1 / 16,) * 3, chunk_cells=2)
+    g = (0.0, 0.0, -9.81)
+    sim = Sim(mesh, Physics(gravity=g, drag_law=oracle.DRAG_STOKES), precision="f64")
+    uf = np.array([0.05, -0.02, 0.0])
+    rng = np.random.default_rng(1)
+    n = 200
+    x0 = rng.random((3, n))
+    d = rng.uniform(10e-6, 30e-6, n)
+    u0 = np.tile(np.array(u0)[:, None], (1, n))
+    sim.inject(x0, u0, d)
+    sim.set_fluid_field(uniform_field(mesh, uf))
+    dt, steps = 1e-4, 1000
+    for _ in range(steps):
+        sim.advance(dt, 1)
+    p = sim.particles()
+    order = np.argsort(p["id"])
+    x, u = p["x"][:, order], p["u"][:, order]
+    t = dt * steps
+    tau = tau_p(d)
+    us = uf[:, None] + np.array(g)[:, None] * tau[None, :]
+    e = np.exp(-t / tau)[None, :]
+    u_ex = us + (u0 - us) * e
+    x_ex = x0 + us * t + tau[None, :] * (u0 - us) * (1 - e)
+    scale = np.max(np.abs(us)) + np.max(np.abs(u0))
+    assert np.max(np.abs(u - u_ex)) / scale < 1e-9
+    dx = (x - x_ex + 0.5) % 1.0 - 0.5     # periodic-aware, L = 1
+    assert np.max(np.abs(dx)) < 1e-9
+
+
+def test_p1_multi_substep_equals_calls():
+    """P-1 corollary: st_advance(dt, k) == k calls of st_advance(dt, 1) when no rebin
+    reorders (C-7: the field is frozen, the step is per particle)."""
+    mesh = Mesh(dims=(8, 8, 8), cell_size=(1 / 8,) * 3, chunk_cells=4)
+    rng = np.random.default_rng(3)
+    F = rng.normal(size=(3, 8, 8, 8)) * 0.1
+    x0, d = rng.random((3, 50)), rng.uniform(20e-6, 60e-6, 50)
+    a = Sim(mesh, Physics(gravity=(0, 0, -9.81)), precision="f64", rebin_interval=1000)
+    b = Sim(mesh, Physics(gravity=(0, 0, -9.81)), precision="f64", rebin_interval=1000)
+    for s in (a, b):
+        s.inject(x0, np.zeros((3, 50)), d)
+        s.set_fluid_field(F)
+    a.advance(1e-3, 7)
+    for _ in range(7):
+        b.advance(1e-3, 1)
+    pa, pb = a.particles(), b.particles()
+    assert np.array_equal(pa["x"], pb["x"]) and np.array_equal(pa["u"], pb["u"])
+    Sa, Ta = a.get_sources()
+    Sb, Tb = b.get_sources()
+    assert Ta == pytest.approx(Tb) and np.allclose(Sa, Sb, rtol=1e-12, atol=0)
+
+
+# ---------------------------------------------------------------- P-2 semi-implicit
+def test_p2_semi_implicit_discrete_closed_form():
+    """P-2: u_n = u_s + (u0-u_s)(1+h)^{-n},  x_n = x0 + n dt u_s + tau (u0-u_s)(1-(1+h)^{-n})."""
+    mesh = Mesh(dims=(16, 16, 16), cell_size=(1 / 16,) * 3, chunk_cells=2)
+    g = np.array([0.0, 0.0, -9.81])
+    sim = Sim(mesh, Physics(gravity=tuple(g), drag_law=oracle.DRAG_STOKES,
+                            integrator=oracle.INT_SEMI_IMPLICIT), precision="f64")
+    uf = np.array([0.05, -0.02, 0.01])
+    rng = np.random.default_rng(2)
+    n = 100
+    x0, d = rng.random((3, n)), rng.uniform(10e-6, 30e-6, n)
+    u0 = np.tile(np.array([0.2, 0.1, -0.3])[:, None], (1, n))
+    sim.inject(x0, u0, d)
+    sim.set_fluid_field(uniform_field(mesh, uf))
+    dt, steps = 1e-4, 500
+    for _ in range(steps):
+        sim.advance(dt, 1)
+    p = sim.particles()
+    o = np.argsort(p["id"])
+    tau = tau_p(d)
+    h = dt / tau
+    us = uf[:, None] + g[:, None] * tau[None, :]
+    q = (1 + h) ** (-steps)
+    u_ex = us + (u0 - us) * q
+    x_ex = x0 + steps * dt * us + tau * (u0 - us) * (1 - q)
+    assert np.max(np.abs(p["u"][:, o] - u_ex)) / np.max(np.abs(us)) < 1e-12
+    assert np.max(np.abs((p["x"][:, o] - x_ex + 0.5) % 1 - 0.5)) < 1e-12
+
+
+# ---------------------------------------------------------------- P-3 S-N terminal velocity
+def _sn_terminal_slip(d, g=9.81):
+    """Root of v f(v d/nu)/tau = g with f = 1 + 0.15 Re^0.687 (bisection, independent code)."""
+    tau = tau_p(d)
+    lo, hi = 0.0, g * tau
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        Re = mid * d / NU_F
+        val = mid * (1 + 0.15 * Re ** 0.687) / tau - g
+        lo, hi = (mid, hi) if val < 0 else (lo, mid)
+    return 0.5 * (lo + hi)
+
+
+@pytest.mark.parametrize("integrator", [oracle.INT_EXPONENTIAL, oracle.INT_SEMI_IMPLICIT])
+def test_p3_schiller_naumann_terminal_velocity(integrator):
+    """P-3: both integrators relax to the S-N terminal slip (fixed point); C1 value
+    for d = 20 um is 1.200594738671e-2 m/s (bisection)."""
+    mesh = Mesh(dims=(4, 4, 4), cell_size=(0.25,) * 3, chunk_cells=2)
+    sim = Sim(mesh, Physics(gravity=(0, 0, -9.81), integrator=integrator), precision="f64")
+    d = np.array([20e-6, 10e-6, 60e-6])
+    sim.inject(np.full((3, 3), 0.5), np.zeros((3, 3)), d)
+    sim.set_fluid_field(uniform_field(mesh, (0, 0, 0)))
+    for _ in range(400):
+        sim.advance(2e-3, 1)
+    p = sim.particles()
+    o = np.argsort(p["id"])
+    vz = -p["u"][2, o]
+    for k in range(3):
+        assert vz[k] == pytest.approx(_sn_terminal_slip(d[k]), rel=1e-9)
+    assert _sn_terminal_slip(20e-6) == pytest.approx(1.200594738671e-2, rel=1e-9)
+
+
+# ---------------------------------------------------------------- P-4 conservation
+@pytest.mark.parametrize("gravity", [(0.0, 0.0, 0.0), (0.0, 0.0, -9.81)])
+@pytest.mark.parametrize("integrator", [oracle.INT_EXPONENTIAL, oracle.INT_SEMI_IMPLICIT])
+def test_p4_momentum_exchange(gravity, integrator):
+    """P-4 (C-8, C-9, Eq. 11): sum_p w m (du - g T) + sum_c S_c V T = 0 to 1e-10,
+    periodic box, non-uniform random field, S-N drag.  A wrong source sign, a
+    missing weight or mass factor, gravity leaking into S, or a deposit into the
+    wrong array all fail."""
+    mesh = Mesh(dims=(8, 8, 8), cell_size=(0.125, 0.125, 0.125), chunk_cells=4)
+    rng = np.random.default_rng(4)
+    F = rng.normal(size=(3, 8, 8, 8)) * 0.5
+    n = 500
+    sim = Sim(mesh, Physics(gravity=gravity, integrator=integrator), precision="f64")
+    x0 = rng.random((3, n))
+    u0 = rng.normal(size=(3, n)) * 0.2
+    d = rng.uniform(20e-6, 200e-6, n)
+    w = rng.uniform(1, 100, n)
+    sim.inject(x0, u0, d, w)
+    sim.set_fluid_field(F)
+    dt, ns = 2e-3, 5
+    sim.advance(dt, ns)
+    sim.advance(dt, ns)
+    p = sim.particles()
+    o = np.argsort(p["id"])
+    m = np.pi / 6 * RHO_P * d ** 3
+    T = 2 * ns * dt
+    dP = np.sum(w * m * (p["u"][:, o] - u0 - np.array(gravity)[:, None] * T), axis=1)
+    S, TT = sim.get_sources()
+    assert TT == pytest.approx(T)
+    fluid = S.reshape(3, -1).sum(axis=1) * mesh.cell_volume * TT
+    scale = np.sum(np.abs(w * m * (p["u"][:, o] - u0)))
+    assert np.max(np.abs(dP + fluid)) / scale < 1e-10
+    assert scale > 0
+
+
+# ---------------------------------------------------------------- P-5 interpolation
+def test_p5_interpolation_linear_and_convex():
+    """P-5 (C-5): a linear field is reproduced exactly in the interior
+    (between the first and last cell centres) and any field's samples are convex."""
+    mesh = Mesh(dims=(8, 6, 5), origin=(-1.0, 0.5, 2.0), cell_size=(0.25, 0.5, 0.125),
+                bc=(oracle.BC_REFLECT, oracle.BC_PERIODIC, oracle.BC_REFLECT), chunk_cells=4)
+    sim = Sim(mesh, precision="f64")
+    nx, ny, nz = mesh.dims
+    cx = mesh.origin[0] + (np.arange(nx) + 0.5) * mesh.cell_size[0]
+    cz = mesh.origin[2] + (np.arange(nz) + 0.5) * mesh.cell_size[2]
+    F = np.zeros((3, nz, ny, nx))
+    F[0] = 2.0 * cx[None, None, :] + 1.0
+    F[2] = -3.0 * cz[:, None, None]
+    rng = np.random.default_rng(5)
+    x = np.stack([rng.uniform(cx[0], cx[-1], 300),
+                  rng.uniform(0.5, 0.5 + ny * 0.5, 300),
+                  rng.uniform(cz[0], cz[-1], 300)])
+    v = sim.interpolate(x, F)
+    assert np.max(np.abs(v[0] - (2.0 * x[0] + 1.0))) < 1e-13
+    assert np.max(np.abs(v[2] - (-3.0 * x[2]))) < 1e-13
+    G = rng.normal(size=(3, nz, ny, nx))
+    x = np.stack([rng.uniform(-1.0, 1.0, 2000), rng.uniform(0.5, 3.5, 2000), rng.uniform(2.0, 2.625, 2000)])
+    v = sim.interpolate(x, G)
+    for k in range(3):
+        assert v[k].min() >= G[k].min() - 1e-14 and v[k].max() <= G[k].max() + 1e-14
+
+
+def test_p5_periodic_wrap_stencil():
+    """C-5 periodic ghost: on the face x = lo the sample is the mean of the first and
+    last cell (wrap), in the middle of cell 0 it is exactly cell 0's value."""
+    mesh = Mesh(dims=(4, 1, 1), cell_size=(1.0, 1.0, 1.0), chunk_cells=4)
+    sim = Sim(mesh, precision="f64")
+    F = np.zeros((3, 1, 1, 4))
+    F[0, 0, 0] = [1.0, 2.0, 3.0, 7.0]
+    v = sim.interpolate(np.array([[0.0, 0.5, 4.0], [0.5] * 3, [0.5] * 3]), F)
+    assert v[0].tolist() == [4.0, 1.0, 4.0]
+
+
+# ---------------------------------------------------------------- P-6 two-way box
+@pytest.mark.parametrize("r", [0.5, 2.0])
+def test_p6_two_way_box_discrete_closed_form(r):
+    """P-6 (P:257-262 analytical case): one cell, one parcel at 1 m/s in
+    quiescent fluid; the harness applies u_f += T S / rho_f after every call.
+    Discrete closed form of the slip: w_n = w0 [(1+r) e^{-h} - r]^n,
+    r = w m / (rho_f V); total momentum conserved."""
+    L = 0.01
+    mesh = Mesh(dims=(1, 1, 1), cell_size=(L, L, L), chunk_cells=8)
+    sim = Sim(mesh, Physics(drag_law=oracle.DRAG_STOKES), precision="f64")
+    d = 50e-6
+    m = np.pi / 6 * RHO_P * d ** 3
+    V = L ** 3
+    w = r * RHO_F * V / m
+    tau = tau_p(d)
+    dt = 0.1 * tau
+    sim.inject(np.full((3, 1), 0.5 * L), np.array([[1.0], [0.0], [0.0]]), np.array([d]), np.array([w]))
+    uf = np.zeros(3)
+    P0 = w * m * 1.0
+    for n in range(1, 51):
+        sim.set_fluid_field(uniform_field(mesh, uf))
+        sim.advance(dt, 1)
+        S, T = sim.get_sources()
+        uf = uf + T * S.reshape(3) / RHO_F
+        up = sim.particles()["u"][:, 0]
+        slip = up[0] - uf[0]
+        assert slip == pytest.approx(((1 + r) * math.exp(-0.1) - r) ** n, rel=1e-12, abs=1e-15)
+        total = w * m * up[0] + RHO_F * V * uf[0]
+        assert total == pytest.approx(P0, rel=1e-13)
+
+
+def test_p6_continuous_limit_first_order():
+    """P-6 continuous: w(t) = w0 exp(-(1+r) t / tau); error of the coupled
+    loop at t = tau converges at first order under dt halving (S:506 slope 0.8-1.2)."""
+    L = 0.01
+    mesh = Mesh(dims=(1, 1, 1), cell_size=(L, L, L), chunk_cells=8)
+    d = 50e-6
+    m = np.pi / 6 * RHO_P * d ** 3
+    r = 0.5
+    w = r * RHO_F * L ** 3 / m
+    tau = tau_p(d)
+    errs = []
+    for k in (10, 20, 40, 80):
+        sim = Sim(mesh, Physics(drag_law=oracle.DRAG_STOKES), precision="f64")
+        sim.inject(np.full((3, 1), 0.5 * L), np.array([[1.0], [0.0], [0.0]]), np.array([d]), np.array([w]))
+        uf = np.zeros(3)
+        for _ in range(k):
+            sim.set_fluid_field(uniform_field(mesh, uf))
+            sim.advance(tau / k, 1)
+            S, T = sim.get_sources()
+            uf = uf + T * S.reshape(3) / RHO_F
+        slip = sim.particles()["u"][0, 0] - uf[0]
+        errs.append(abs(slip - math.exp(-(1 + r))))
+    slopes = [math.log2(errs[i] / errs[i + 1]) for i in range(3)]
+    assert all(0.8 <= s <= 1.2 for s in slopes), slopes
+
+
+# ---------------------------------------------------------------- P-7 brute-force locate
+def _f32(v):
+    return float(np.float32(v))
+
+
+@pytest.mark.parametrize("n,k,origin", [(2, 1, 0.0), (4, 2, 0.0), (8, 3, -0.5), (16, 4, 0.0), (16, 3, -1.0)])
+def test_p7_locate_brute_force(n, k, origin):
+    """P-7 (C-6): on dyadic grids (h = 2^-k) the fp32 contract formula equals the
+    exact cell found by scanning every cell box [o + c h, o + (c+1) h) with rational
+    arithmetic, at faces, their fp32 neighbours and random points; the upper face maps
+    to the last cell; chunk = scan of chunk boxes."""
+    h = 2.0 ** -k
+    cc = 2 if n > 2 else 1
+    mesh = Mesh(dims=(n, n, n), origin=(origin,) * 3, cell_size=(h,) * 3, chunk_cells=cc)
+    sim = Sim(mesh, precision="f32")
+    lo, hi = origin, origin + n * h
+    pts = []
+    for c in range(n + 1):
+        f = origin + c * h
+        for v in (f, np.nextafter(np.float32(f), np.float32(-np.inf)), np.nextafter(np.float32(f), np.float32(np.inf))):
+            v = _f32(v)
+            if lo <= v <= hi:
+                pts.append(v)
+    rng = np.random.default_rng(n)
+    pts += [_f32(v) for v in rng.uniform(lo, hi, 300)]
+    # keep points whose subtraction x - o is exact in fp32 (then the product by 2^k is exact)
+    pts = [v for v in pts if Fraction(_f32(v - origin)) == Fraction(v) - Fraction(origin)]
+    xs = np.array(pts, np.float32)
+    m = xs.size
+    X = np.stack([xs, np.roll(xs, 1), np.roll(xs, 2)])
+    cell, chunk = sim.locate(X)
+
+    def brute(v):
+        fv = Fraction(float(v))
+        for c in range(n):
+            if Fraction(origin) + c * Fraction(h) <= fv < Fraction(origin) + (c + 1) * Fraction(h):
+                return c
+        assert fv == Fraction(origin) + n * Fraction(h)
+        return n - 1
+
+    def brute_chunk(c):
+        for q in range(0, n, cc):
+            if q <= c < q + cc:
+                return q // cc
+        raise AssertionError
+
+    nc = (n + cc - 1) // cc
+    for i in range(m):
+        cx, cy, cz = (brute(X[a, i]) for a in range(3))
+        assert cell[i] == (cz * n + cy) * n + cx
+        assert chunk[i] == (brute_chunk(cz) * nc + brute_chunk(cy)) * nc + brute_chunk(cx)
+
+
+# ---------------------------------------------------------------- P-8 walls / wrap
+def test_p8_reflection_conserves_speed():
+    """P-8: a particle moving at u = u_f (no drag, g = 0) across a
+    wall is mirrored (x -> 2 lo - x) with the normal velocity negated; speed unchanged."""
+    mesh = Mesh(dims=(4, 4, 4), cell_size=(1.0, 1.0, 1.0), bc=(oracle.BC_REFLECT,) * 3, chunk_cells=2)
+    sim = Sim(mesh, precision="f64")
+    sim.inject(np.array([[0.05], [2.0], [2.0]]), np.array([[-1.0], [0.0], [0.0]]), np.array([1e-5]))
+    sim.set_fluid_field(uniform_field(mesh, (-1.0, 0.0, 0.0)))
+    sim.advance(0.1, 1)
+    p = sim.particles()
+    assert p["u"][:, 0].tolist() == [1.0, 0.0, 0.0]
+    assert p["x"][0, 0] == pytest.approx(0.05, abs=1e-15)
+    # oblique: speed conserved exactly
+    sim2 = Sim(Mesh(dims=(4, 4, 4), bc=(oracle.BC_REFLECT,) * 3, chunk_cells=2), precision="f64")
+    v = np.array([[0.7], [-1.3], [0.4]])
+    sim2.inject(np.array([[3.9], [0.2], [3.95]]), v, np.array([1e-5]))
+    sim2.set_fluid_field(uniform_field(sim2.mesh, v[:, 0]))
+    sim2.advance(0.2, 1)
+    u = sim2.particles()["u"][:, 0]
+    assert np.linalg.norm(u) == np.linalg.norm(v[:, 0])
+    assert u.tolist() == [-0.7, 1.3, -0.4]
+
+
+def test_p8_periodic_wrap_fixup_fp32():
+    """P-8 / C-12: in fp32, (-1e-8) + 2pi rounds to exactly 2pi; the wrap must give lo
+    (cell 0), never cell n.  A displacement one wrap cannot undo -> ST_ERR_CFL."""
+    L = 2 * math.pi
+    mesh = Mesh(dims=(64, 1, 1), cell_size=(L / 64, 1.0, 1.0), chunk_cells=8)
+    sim = Sim(mesh, precision="f32")
+    assert np.float32(np.float32(-1e-8) + np.float32(L)) == np.float32(L)
+    sim.inject(np.array([[2e-8], [0.5], [0.5]]), np.array([[-1e-6], [0.0], [0.0]]), np.array([1e-5]))
+    sim.set_fluid_field(uniform_field(mesh, (-1e-6, 0.0, 0.0), np.float32))
+    assert sim.advance(0.03, 1) == 0
+    p = sim.particles()
+    assert p["x"][0, 0] == 0.0 and p["cell"][0] == 0
+    sim3 = Sim(mesh, precision="f64")
+    # one wrap is exact for any displacement below hi + L - x; beyond it -> CFL
+    sim3.inject(np.array([[1.0], [0.5], [0.5]]), np.array([[200.0], [0.0], [0.0]]), np.array([1e-5]))
+    sim3.set_fluid_field(uniform_field(mesh, (200.0, 0.0, 0.0)))
+    assert sim3.advance(0.1, 1) == oracle.ERR_CFL
+
+
+# ---------------------------------------------------------------- P-9 rebin
+def test_p9_stable_order_vs_sorted():
+    """P-9 (C-15): counting sort == Python's stable sorted() on random keys with ties."""
+    rng = np.random.default_rng(9)
+    for n, nk in ((0, 3), (1, 1), (1000, 7), (5000, 300)):
+        key = rng.integers(0, nk, n).astype(np.int32)
+        perm, off = oracle.stable_order(key, nk)
+        assert perm.tolist() == sorted(range(n), key=lambda i: key[i])
+        assert off.tolist() == [0] + np.cumsum(np.bincount(key, minlength=nk)).tolist()
+
+
+def test_p9_rebin_and_multirank_migration():
+    """P-9 / C-16: after a rebin the store is sorted by chunk, ids are a permutation,
+    ties keep prior order, and the R-rank migration matrix equals a brute-force count;
+    arrivals are appended in ascending source rank before the stable sort."""
+    mesh = Mesh(dims=(16, 16, 32), cell_size=(1 / 16,) * 3, chunk_cells=4)
+    rng = np.random.default_rng(11)
+    R = 4
+    sim = Sim(mesh, Physics(coupling=oracle.ONE_WAY), nranks=R, precision="f32", rebin_interval=1)
+    for r in range(R):
+        n = 300
+        sim.inject(rng.random((3, n)) * np.array([[1.0], [1.0], [2.0]]), np.zeros((3, n)),
+                   np.full(n, 20e-6), rank=r)
+    before = [sim.particles(r) for r in range(R)]
+    sim.set_fluid_field(rng.normal(size=(3, 32, 16, 16)) * 0.1)
+    sim.advance(1e-3, 1)
+    after = [sim.particles(r) for r in range(R)]
+    all_ids = np.concatenate([b["id"] for b in before])
+    assert sorted(np.concatenate([a["id"] for a in after]).tolist()) == sorted(all_ids.tolist())
+    # brute-force owner from the chunk plane
+    ncz = mesh.nchunk[2]
+    ranges = [((r * ncz) // R, ((r + 1) * ncz) // R) for r in range(R)]
+    M = np.zeros((R, R), int)
+    pos = {}
+    for r in range(R):
+        a = after[r]
+        for i in range(a["id"].size):
+            pos[int(a["id"][i])] = (r, i)
+        assert np.all(np.diff(a["chunk"]) >= 0)
+        kz = a["chunk"] // (mesh.nchunk[0] * mesh.nchunk[1])
+        lo, hi = ranges[r]
+        assert np.all((kz >= lo) & (kz < hi))
+    # where did each particle come from (positions moved, so use the post-advance chunk)
+    src_of = {int(i): r for r in range(R) for i in before[r]["id"]}
+    for r in range(R):
+        for i in after[r]["id"]:
+            M[src_of[int(i)], r] += 1
+    assert np.array_equal(M, sim.M)
+    # ties within a chunk: kept particles (source == r) precede arrivals, arrivals by source rank
+    for r in range(R):
+        a = after[r]
+        for c in np.unique(a["chunk"]):
+            srcs = [src_of[int(i)] for i in a["id"][a["chunk"] == c]]
+            key = [(0 if s == r else 1, s) for s in srcs]
+            assert key == sorted(key)
+
+
+# ---------------------------------------------------------------- P-10 / P-11
+def test_p10_planar_field_keeps_z():
+    """P-10 invariant: a field with u_z = 0 and g = 0 keeps u_z = 0 and z exactly."""
+    mesh = Mesh(dims=(8, 8, 8), cell_size=(2 * math.pi / 8,) * 3, chunk_cells=4)
+    rng = np.random.default_rng(12)
+    F = rng.normal(size=(3, 8, 8, 8))
+    F[2] = 0.0
+    sim = Sim(mesh, precision="f32")
+    x0 = (rng.random((3, 400)) * 2 * math.pi).astype(np.float32)
+    sim.inject(x0, np.zeros((3, 400)), np.full(400, 1e-4))
+    sim.set_fluid_field(F)
+    for _ in range(20):
+        sim.advance(0.01, 1)
+    p = sim.particles()
+    o = np.argsort(p["id"])
+    assert np.all(p["u"][2] == 0.0)
+    assert np.array_equal(p["x"][2, o], x0[2])
+
+
+def test_p11_substep_convergence_first_order():
+    """P-11: in a non-uniform field the frozen-coefficient ETD step converges at
+    first order: self-convergence slopes log2(e(dt)/e(dt/2)) in [0.8, 1.2]."""
+    mesh = Mesh(dims=(16, 16, 16), cell_size=(1 / 16,) * 3, bc=(oracle.BC_PERIODIC,) * 3, chunk_cells=4)
+    cx = (np.arange(16) + 0.5) / 16
+    F = np.zeros((3, 16, 16, 16))
+    F[0] = np.sin(2 * np.pi * cx)[None, :, None] * 0.5
+    F[1] = np.cos(2 * np.pi * cx)[:, None, None] * 0.5
+    F[2] = np.sin(2 * np.pi * cx)[None, None, :] * 0.5
+    rng = np.random.default_rng(13)
+    x0, d = rng.random((3, 50)), np.full(50, 60e-6)
+
+    def run(k):
+        s = Sim(mesh, Physics(gravity=(0, 0, -9.81)), precision="f64", rebin_interval=10 ** 9)
+        s.inject(x0, np.zeros((3, 50)), d)
+        s.set_fluid_field(F)
+        s.advance(0.2 / k, k)
+        return s.particles()["x"]
+
+    ref = run(2048)
+    errs = [np.max(np.abs((run(k) - ref + 0.5) % 1 - 0.5)) for k in (8, 16, 32, 64)]
+    slopes = [math.log2(errs[i] / errs[i + 1]) for i in range(3)]
+    assert all(0.8 <= s <= 1.2 for s in slopes), (errs, slopes)
+
+
+def test_p4_deposit_goes_to_start_cell():
+    """C-10 ("the cell containing the particle"): the sub-step's reaction is
+    deposited into the cell of the sub-step START position, even when the particle
+    crosses a face during the sub-step; the amount is -w m du_drag / (V T)."""
+    mesh = Mesh(dims=(4, 4, 4), cell_size=(1.0, 1.0, 1.0), chunk_cells=2)
+    sim = Sim(mesh, Physics(drag_law=oracle.DRAG_STOKES), precision="f64")
+    d, w = 100e-6, 7.0
+    sim.inject(np.array([[1.95], [2.5], [2.5]]), np.array([[1.0], [0.0], [0.0]]), np.array([d]), np.array([w]))
+    sim.set_fluid_field(uniform_field(mesh, (0.0, 0.0, 0.0)))
+    dt = 0.1
+    sim.advance(dt, 1)
+    p = sim.particles()
+    assert p["x"][0, 0] > 2.0                       # crossed into cell x = 2
+    S, T = sim.get_sources()
+    nz = np.argwhere(S[0] != 0)
+    assert nz.tolist() == [[2, 2, 1]]               # (z, y, x) of the start cell
+    m = np.pi / 6 * RHO_P * d ** 3
+    du = p["u"][0, 0] - 1.0
+    assert S[0, 2, 2, 1] * T == pytest.approx(-w * m * du, rel=1e-12)
