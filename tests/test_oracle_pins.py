@@ -542,7 +542,7 @@ def test_p4_deposit_goes_to_start_cell():
     crosses a face during the sub-step; the amount is -w m du_drag / (V T)."""
     mesh = Mesh(dims=(4, 4, 4), cell_size=(1.0, 1.0, 1.0), chunk_cells=2)
     sim = Sim(mesh, Physics(drag_law=oracle.DRAG_STOKES), precision="f64")
-    d, w = 100e-6, 7.0
+    d, w = 300e-6, 7.0
     sim.inject(np.array([[1.95], [2.5], [2.5]]), np.array([[1.0], [0.0], [0.0]]), np.array([d]), np.array([w]))
     sim.set_fluid_field(uniform_field(mesh, (0.0, 0.0, 0.0)))
     dt = 0.1
