@@ -1,0 +1,29 @@
+# Build the product library (CUDA, sm_100a) and the oracle (plain C).
+NVCC      ?= /usr/local/cuda/bin/nvcc
+PY        ?= python
+SITE      := $(shell $(PY) -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")
+NCCL_DIR  ?= $(SITE)/nvidia/nccl
+PKG       := paper_2603_26691_b200
+SRC       := $(PKG)/csrc
+LIB       := $(PKG)/lib/libscaletrack.so
+CU        := $(SRC)/st_api.cu $(SRC)/st_comm.cu $(SRC)/k_advance.cu $(SRC)/k_field.cu $(SRC)/k_sort.cu
+HDR       := include/scaletrack.h $(SRC)/st_internal.h $(SRC)/st_device.cuh $(SRC)/st_comm.h
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -Iinclude -I$(NCCL_DIR)/include \
+             -Xptxas -v --expt-relaxed-constexpr
+ORACLE    := oracle/liboracle_st.so
+
+all: $(LIB) $(ORACLE)
+
+$(LIB): $(CU) $(HDR)
+	@mkdir -p $(PKG)/lib build
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
+	  -Xlinker -rpath=$(NCCL_DIR)/lib 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
+
+$(ORACLE): oracle/st_oracle.c oracle/st_oracle_step.inc
+	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ oracle/st_oracle.c -lm
+
+clean:
+	rm -f $(LIB) $(ORACLE)
+
+.PHONY: all clean

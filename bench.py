@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""bench.py — particle-updates/s of the two-way-coupled SCALE-TRACK particle step
+(arXiv 2603.26691) on N B200s, through the C-ABI (include/scaletrack.h).
+
+One "step" = one pass of the whole hot path over the resident particles:
+  st_set_fluid_field (field ingest, a1) -> st_advance(dt, 1) (locate, interpolate,
+  drag+gravity, walls, relocate, deposit, rebin at the stated interval K, a2-a8,
+  migration/halo when N > 1) -> st_get_sources (readout, a9).
+Default workload: C5 (BASELINE.json configs[4]) true weak scaling, 1e9 particles
+per GPU on a 192x192x(72 N) reflecting chamber grid, two-way, dt = 5 ms.
+
+  python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload C3|C4|C5]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-updates/s (two-way coupled) at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "particle-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C5", choices=["C3", "C4", "C5"])
+    ap.add_argument("--particles", type=float, default=None, help="particles per GPU (default: the workload's)")
+    ap.add_argument("--rebin-interval", type=int, default=4)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target oracle CPU time for cpu_baseline")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_workload(name, G, particles):
+    import synth
+    if name != "C5" and G > 1:
+        raise SystemExit("multi-GPU runs use the C5 weak-scaling workload")
+    wl = synth.workload(name, nranks=G)
+    n_per = int(particles) if particles else (wl.n_particles // G if name == "C5" else wl.n_particles)
+    return wl, n_per
+
+
+def algorithmic_bytes_per_update(two_way=True):
+    """read + write x,u (48 B) + read d (4) + read w (4, two-way)."""
+    return 48 + 4 + (4 if two_way else 0)
+
+
+# ---------------------------------------------------------------- oracle (CPU) legs
+def run_oracle_sample(wl, n_sample, steps, z_range=None, K=4):
+    """Time the oracle (fp32, single-threaded, as it stands) on a bounded sample of the
+    workload: same grid and field recipe, n_sample particles, `steps` calls."""
+    import numpy as np
+
+    import oracle
+    import synth
+    mesh = oracle.Mesh(dims=wl.dims, origin=wl.origin, cell_size=wl.cell_size, chunk_cells=wl.chunk_cells, bc=wl.bc)
+    phys = oracle.Physics(rho_f=synth.RHO_F, nu_f=synth.NU_F, rho_p=synth.RHO_P, gravity=wl.gravity,
+                          drag_law=wl.drag_law, coupling=wl.coupling)
+    sim = oracle.Sim(mesh, phys, rebin_interval=K, precision="f32")
+    lo, hi = synth.domain_box(wl)
+    x, u, d, w = synth.particles_np(n_sample, lo, hi, wl.d_range, wl.d_dist, wl.w, wl.seed_particles)
+    sim.inject(x, u, d, w)
+    F = synth.make_field(wl)
+    sim.set_fluid_field(F)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sim.set_fluid_field(F)
+        sim.advance(wl.dt, 1)
+        sim.get_sources()
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(wl, target_s, K):
+    n = 200_000
+    t1 = run_oracle_sample(wl, n, 1, K=K)
+    steps = max(1, int(target_s / max(t1, 1e-3)))
+    steps = min(steps, 200)
+    t = run_oracle_sample(wl, n, steps, K=K)
+    return {"value": n * steps / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} particles x {steps} steps of {wl.name} (full {wl.dims} grid, same field recipe), "
+                      f"fp32 oracle, single-threaded, {t:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl, _ = make_workload(args.workload, args.gpus, args.particles)
+    n = 100_000
+    t_w = run_oracle_sample(wl, n, max(args.warmup, 0), K=args.rebin_interval) if args.warmup else 0.0
+    t = run_oracle_sample(wl, n, args.steps, K=args.rebin_interval)
+    v = n * args.steps / t
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{wl.name} sample: {n} particles on the {wl.dims} grid (oracle, 1 core)",
+                       "rebin_interval": args.rebin_interval},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{n} particles x {args.steps} steps of {wl.name}, fp32 oracle, 1 thread"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2603_26691_b200 import Config, ScaleTrack, nccl_unique_id
+
+    G = args.gpus
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != G:
+        raise SystemExit(f"--gpus {G} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if G > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl, n_per = make_workload(args.workload, G, args.particles)
+    K = args.rebin_interval
+    uid = None
+    if G > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.current_stream(dev)
+    cap = n_per if G == 1 else int(n_per * 1.05) + 1_000_000
+    cfg = Config(dims=wl.dims, origin=wl.origin, cell_size=wl.cell_size, chunk_cells=wl.chunk_cells, bc=wl.bc,
+                 rho_f=synth.RHO_F, nu_f=synth.NU_F, rho_p=synth.RHO_P, gravity=wl.gravity, drag_law=wl.drag_law,
+                 coupling=wl.coupling, rebin_interval=K, capacity=cap, device=local, rank=rank, nranks=G)
+    st = ScaleTrack(cfg, stream=stream.cuda_stream, unique_id=uid)
+    lay = st.layout
+    z_range = (lay.z0, lay.z1)
+    # particles: uniform in this rank's slab, drawn on the device in batches (seed 8 + rank)
+    lo, hi = synth.domain_box(wl, z_range)
+    batch = 100_000_000
+    for b0 in range(0, n_per, batch):
+        nb = min(batch, n_per - b0)
+        x, u, d, w = synth.particles_torch(nb, lo, hi, wl.d_range, wl.d_dist, wl.w,
+                                           seed=wl.seed_particles * 1000 + rank * 100 + b0 // batch, device=dev)
+        st.inject(x, u, d, w)
+        del x, u, d, w
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    # two fields (t = 0, dt) of this rank's owned planes, alternated every step
+    fields = [synth.make_field(wl, t=s * wl.dt, z_range=z_range, device=dev).contiguous() for s in range(2)]
+    nx, ny, _ = wl.dims
+    S = torch.empty((3, lay.z1 - lay.z0, ny, nx), dtype=torch.float32, device=dev)
+
+    def step(s, Fsrc, Sdst):
+        st.set_fluid_field(Fsrc[s % 2])
+        st.advance(wl.dt, 1)
+        st.get_sources(Sdst)
+
+    for s in range(args.warmup):
+        step(s, fields, S)
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    l0 = st.stats()["kernel_launches"]
+    adv, reb = [], []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for s in range(args.steps):
+        step(s, fields, S)
+        a, r = st.last_timings()
+        adv.append(a)
+        reb.append(r)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = st.stats()["kernel_launches"] - l0
+    ms = e0.elapsed_time(e1)
+    n_local = st.count()
+    tot = torch.tensor([ms, float(n_local)], dtype=torch.float64, device=dev)
+    if G > 1:
+        t_max = tot[:1].clone()
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        n_sum = tot[1:].clone()
+        dist.all_reduce(n_sum, op=dist.ReduceOp.SUM)
+        ms, n_total = float(t_max.item()), float(n_sum.item())
+    else:
+        n_total = float(n_local)
+    value = n_total * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (per launch, CUDA events on the launching stream)
+    adv_ms = statistics.mean(adv)
+    reb_list = [r for r in reb if r > 0]
+    reb_ms = statistics.mean(reb_list) if reb_list else 0.0
+    reb_per_step = reb_ms * len(reb_list) / max(1, len(reb))
+    peak, peak_src = peaks()
+    cells_win = nx * ny * (lay.z1 - lay.z0 + 2 * lay.halo_cells)
+    if adv_ms >= reb_per_step:
+        kname = "advance"
+        alg = algorithmic_bytes_per_update(wl.coupling == 1) * n_local + 24 * cells_win
+        kms = adv_ms
+    else:
+        kname = "rebin (stable sort, full store)"
+        alg = 80 * n_local
+        kms = reb_ms
+    achieved = alg / (kms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(kname.split()[0])
+        except Exception:
+            traffic = None
+
+    # e2e: host (pinned) field in, host sources out, through the same C-ABI calls
+    e2e = None
+    if not args.no_e2e:
+        Fh = [f.cpu().pin_memory() for f in fields]
+        Sh = torch.empty(S.shape, dtype=torch.float32).pin_memory()
+        for s in range(2):
+            step(s, Fh, Sh)
+        torch.cuda.synchronize()
+        if G > 1:
+            dist.barrier()
+        k_e2e = max(3, min(args.steps, 10))
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for s in range(k_e2e):
+            step(s, Fh, Sh)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        ems = h0.elapsed_time(h1)
+        if G > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": n_total * k_e2e / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(Fh[0].numel() * 4), "d2h_bytes_per_step": int(Sh.numel() * 4),
+               "steps": k_e2e, "ms_per_step": ems / k_e2e}
+
+    cpu = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, args.cpu_seconds, K)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {n_per:.3g} particles/GPU, grid {list(wl.dims)}, "
+                                   f"{'reflect' if wl.bc[0] else 'periodic'}, random-Fourier field "
+                                   f"u_rms={wl.field_args.get('u_rms')}, two-way, S-N drag + gravity, dt={wl.dt}",
+                       "particles_per_gpu": n_per, "grid": list(wl.dims), "chunk_cells": wl.chunk_cells,
+                       "rebin_interval": K, "substeps_per_step": 1,
+                       "l2": "inputs larger than L2 (40 B x N resident particle state)",
+                       "parallelism": f"z-slab x{G}"},
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg, "kernel_ms": kms},
+            "advance_ms": adv_ms, "rebin_ms": reb_ms, "rebins_in_timed_region": len(reb_list),
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    st.close()
+    if G > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -210,6 +210,10 @@ const char* st_last_error(const st_ctx* ctx);
 /* ABI version the library was built with (== ST_ABI_VERSION). */
 int32_t st_abi_version(void);
 
+/* Write a fresh 128-byte ncclUniqueId into out (rank 0 calls it and broadcasts
+ * the bytes to the other ranks before st_init).  ST_ERR_NCCL on failure. */
+st_status st_nccl_unique_id(void* out);
+
 #ifdef __cplusplus
 }
 #endif

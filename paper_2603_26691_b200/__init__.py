@@ -1,0 +1,13 @@
+"""B200-native SCALE-TRACK hot path (arXiv 2603.26691): the two-way-coupled
+Lagrangian particle step as sm_100a CUDA kernels behind a C ABI
+(include/scaletrack.h).  This package is the thin Python binding; see DESIGN.md.
+"""
+from ._native import (BC_PERIODIC, BC_REFLECT, DRAG_SCHILLER_NAUMANN, DRAG_STOKES, INT_EXPONENTIAL,
+                      INT_SEMI_IMPLICIT, ONE_WAY, TWO_WAY, StError)
+from .api import Config, ScaleTrack, nccl_unique_id
+
+__all__ = [
+    "Config", "ScaleTrack", "StError", "nccl_unique_id",
+    "BC_PERIODIC", "BC_REFLECT", "DRAG_STOKES", "DRAG_SCHILLER_NAUMANN",
+    "INT_EXPONENTIAL", "INT_SEMI_IMPLICIT", "ONE_WAY", "TWO_WAY",
+]

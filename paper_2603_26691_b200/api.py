@@ -1,0 +1,214 @@
+"""Python face of the C-ABI (include/scaletrack.h): same names, marshalling only.
+
+Arrays may be numpy arrays (host) or torch tensors (host or CUDA); the library
+detects the pointer kind.  Every step of the particle path runs in the CUDA
+kernels of libscaletrack.so — nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+
+def _ptr(a):
+    """Raw address of a contiguous numpy array or torch tensor (or None)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _as_f32(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return np.ascontiguousarray(a, dtype=np.float32)
+    import torch
+    return a.to(torch.float32).contiguous()
+
+
+@dataclass
+class Config:
+    """Python mirror of st_config (defaults = st_config_default)."""
+
+    dims: tuple = (16, 16, 16)
+    origin: tuple = (0.0, 0.0, 0.0)
+    cell_size: tuple = (1 / 16, 1 / 16, 1 / 16)
+    chunk_cells: int = 8
+    bc: tuple = (N.BC_PERIODIC,) * 3
+    rho_f: float = 1.2
+    nu_f: float = 1.5e-5
+    rho_p: float = 1000.0
+    gravity: tuple = (0.0, 0.0, 0.0)
+    drag_law: int = N.DRAG_SCHILLER_NAUMANN
+    integrator: int = N.INT_EXPONENTIAL
+    coupling: int = N.TWO_WAY
+    rebin_interval: int = 1
+    capacity: int = 1_000_000
+    device: int = 0
+    rank: int = 0
+    nranks: int = 1
+
+    def to_c(self, stream=None, unique_id: bytes | None = None) -> N.StConfig:
+        c = N.StConfig()
+        N.load().st_config_default(ctypes.byref(c))
+        for a in range(3):
+            c.dims[a] = int(self.dims[a])
+            c.origin[a] = float(self.origin[a])
+            c.cell_size[a] = float(self.cell_size[a])
+            c.bc[a] = int(self.bc[a])
+            c.gravity[a] = float(self.gravity[a])
+        c.chunk_cells = int(self.chunk_cells)
+        c.rho_f, c.nu_f, c.rho_p = float(self.rho_f), float(self.nu_f), float(self.rho_p)
+        c.drag_law, c.integrator, c.coupling = int(self.drag_law), int(self.integrator), int(self.coupling)
+        c.rebin_interval = int(self.rebin_interval)
+        c.capacity = int(self.capacity)
+        c.device = int(self.device)
+        c.stream = stream
+        c.rank, c.nranks = int(self.rank), int(self.nranks)
+        c.nccl_unique_id = None
+        return c
+
+    @property
+    def ncell(self) -> int:
+        return int(self.dims[0]) * int(self.dims[1]) * int(self.dims[2])
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = N.load().st_nccl_unique_id(buf)
+    if rc:
+        raise N.StError(rc, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+class ScaleTrack:
+    """One st_ctx: the particle store, fields and sources of one rank / GPU."""
+
+    def __init__(self, cfg: Config, stream=None, unique_id: bytes | None = None):
+        self.lib = N.load()
+        self.cfg = cfg
+        c = cfg.to_c(stream=stream)
+        self._uid = None
+        if unique_id is not None:
+            self._uid = ctypes.create_string_buffer(unique_id, 128)
+            c.nccl_unique_id = ctypes.cast(self._uid, ctypes.c_void_p)
+        h = ctypes.c_void_p()
+        rc = self.lib.st_init(ctypes.byref(c), ctypes.byref(h))
+        if rc:
+            raise N.StError(rc, self.lib.st_last_error(None).decode())
+        self.h = h
+        self.layout = self.get_layout()
+
+    # -- lifecycle --
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.st_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc:
+            raise N.StError(rc, self.lib.st_last_error(self.h).decode())
+
+    # -- st_* --
+    def set_fluid_field(self, u):
+        u = _as_f32(u)
+        self._check(self.lib.st_set_fluid_field(self.h, _ptr(u)))
+        self._keep = u   # device inputs stay alive until stream-ordered consumption
+
+    def inject(self, x, u, d, w=None, ids=None):
+        x, u, d, w = _as_f32(x), _as_f32(u), _as_f32(d), _as_f32(w)
+        n = int(d.shape[0])
+        if ids is not None and isinstance(ids, np.ndarray):
+            ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        self._check(self.lib.st_inject(self.h, n, _ptr(x), _ptr(u), _ptr(d), _ptr(w), _ptr(ids)))
+
+    def advance(self, dt: float, nsteps: int = 1):
+        self._check(self.lib.st_advance(self.h, float(dt), int(nsteps)))
+
+    def get_sources(self, out=None):
+        """S [3][z1-z0][ny][nx] fp32 (N/m^3) and the interval T_acc."""
+        if out is None:
+            nx, ny, _ = self.cfg.dims
+            out = np.empty((3, self.layout.z1 - self.layout.z0, ny, nx), np.float32)
+        T = ctypes.c_double()
+        self._check(self.lib.st_get_sources(self.h, _ptr(out), ctypes.byref(T)))
+        return out, T.value
+
+    def request_sources(self):
+        self._check(self.lib.st_request_sources(self.h))
+
+    def wait_sources(self, out=None):
+        if out is None:
+            nx, ny, _ = self.cfg.dims
+            out = np.empty((3, self.layout.z1 - self.layout.z0, ny, nx), np.float32)
+        T = ctypes.c_double()
+        self._check(self.lib.st_wait_sources(self.h, _ptr(out), ctypes.byref(T)))
+        return out, T.value
+
+    def count(self) -> int:
+        n = ctypes.c_int64()
+        self._check(self.lib.st_get_count(self.h, ctypes.byref(n)))
+        return n.value
+
+    def get_particles(self) -> dict:
+        n = self.count()
+        x = np.empty((3, n), np.float32)
+        u = np.empty((3, n), np.float32)
+        d = np.empty(n, np.float32)
+        w = np.empty(n, np.float32)
+        ids = np.empty(n, np.uint64)
+        cell = np.empty(n, np.int32)
+        chunk = np.empty(n, np.int32)
+        no = ctypes.c_int64()
+        self._check(self.lib.st_get_particles(self.h, n, ctypes.byref(no), _ptr(x), _ptr(u), _ptr(d), _ptr(w),
+                                              _ptr(ids), _ptr(cell), _ptr(chunk)))
+        return dict(x=x, u=u, d=d, w=w, id=ids, cell=cell, chunk=chunk)
+
+    def locate(self, x):
+        x = _as_f32(x)
+        n = int(x.shape[1])
+        cell = np.empty(n, np.int32)
+        chunk = np.empty(n, np.int32)
+        self._check(self.lib.st_locate(self.h, n, _ptr(x), _ptr(cell), _ptr(chunk)))
+        return cell, chunk
+
+    def migration_counts(self) -> np.ndarray:
+        row = np.zeros(self.cfg.nranks, np.int64)
+        self._check(self.lib.st_get_migration_counts(self.h, _ptr(row)))
+        return row
+
+    def get_layout(self) -> N.StLayout:
+        o = N.StLayout()
+        self._check(self.lib.st_get_layout(self.h, ctypes.byref(o)))
+        return o
+
+    def stats(self) -> dict:
+        o = N.StStats()
+        self._check(self.lib.st_get_stats(self.h, ctypes.byref(o)))
+        return {k: getattr(o, k) for k, _ in N.StStats._fields_}
+
+    def sync(self):
+        self._check(self.lib.st_sync(self.h))
+
+    def last_timings(self):
+        a, r = ctypes.c_float(), ctypes.c_float()
+        self._check(self.lib.st_last_timings(self.h, ctypes.byref(a), ctypes.byref(r)))
+        return a.value, r.value

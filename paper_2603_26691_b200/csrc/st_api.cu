@@ -1,0 +1,705 @@
+// C-ABI of the B200 SCALE-TRACK hot path (include/scaletrack.h).
+// Owns the SoA particle store (ping-pong), the double-buffered fluid field and
+// source accumulators (asynchronous coupling buffer), the
+// compute and copy streams, and (nranks > 1) the NCCL communicator.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "st_comm.h"
+#include "st_internal.h"
+
+using namespace st;
+
+struct st_ctx {
+  st_config cfg{};
+  std::string err;
+  bool dead = false;
+
+  // geometry
+  Geom g{};
+  Phys p{};
+  int z0 = 0, z1 = 0, kz0 = 0, kz1 = 0, H = 0;
+  int64_t local_cells = 0;   // nx*ny*(z1-z0)
+  int32_t chunk_lo = 0, n_local_chunks = 0;
+  int key_bits = 1;
+
+  // streams
+  cudaStream_t cs = nullptr;  // compute
+  bool own_cs = false;
+  cudaStream_t xs = nullptr;  // copy / coupling
+
+  // store
+  int64_t cap = 0, n = 0;
+  Store S[2];
+  int cur = 0;
+  int32_t* key[2] = {nullptr, nullptr};
+  bool keys_valid = false;    // key[cur] == chunk of current positions
+  SortScratch sc;
+  int64_t* offsets = nullptr; // [n_local_chunks + 1] after a rebin
+  uint64_t next_id = 0;
+
+  // fields (double buffer)
+  float4* field[2] = {nullptr, nullptr};
+  int front = -1, pending = -1;
+  cudaEvent_t ev_field_ready[2]{}, ev_field_reader[2]{};
+  float* field_stage = nullptr;  // [3][ext planes][ny][nx] device staging
+  int ext_z0 = 0, ext_nz = 0;    // planes held by field_stage (owned + halos)
+
+  // sources (double buffer)
+  float4* acc[2] = {nullptr, nullptr};
+  int acc_cur = 0;
+  double T_acc[2] = {0.0, 0.0};
+  cudaEvent_t ev_acc_writer[2]{}, ev_acc_free[2]{};
+  float* S_dev = nullptr;        // [3][local_cells]
+  bool readout_pending = false;
+  double readout_T = 0.0;
+  cudaEvent_t ev_readout_done{};
+  cudaEvent_t ev_in{};
+
+  // errors and counters
+  int* d_err = nullptr;
+  int64_t calls = 0, rebins = 0, launches = 0, fused_rebins = 0, last_movers = 0;
+  std::vector<int64_t> mig_row;
+  int64_t last_sent = 0, last_recv = 0;
+
+  // timing
+  cudaEvent_t t_adv0{}, t_adv1{}, t_reb0{}, t_reb1{};
+  bool timed_adv = false, timed_reb = false;
+
+  // multi-GPU
+  Comm* comm = nullptr;
+};
+
+static thread_local std::string g_init_error;
+
+#define ST_CUDA(ctx, call)                                                              \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+      (ctx)->dead = true;                                                               \
+      return e_ == cudaErrorMemoryAllocation ? ST_ERR_OOM : ST_ERR_CUDA;                \
+    }                                                                                   \
+  } while (0)
+
+static st_status fail(st_ctx* c, st_status s, const std::string& msg) {
+  c->err = msg;
+  return s;
+}
+
+#define ST_ALIVE(ctx)                                                                   \
+  do {                                                                                  \
+    if (!(ctx)) return ST_ERR_INVALID_ARG;                                              \
+    if ((ctx)->dead) return ST_ERR_CUDA;                                                \
+  } while (0)
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static st_status check_launch(st_ctx* c, int nl) {
+  c->launches += nl;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    c->err = std::string("kernel launch: ") + cudaGetErrorString(e);
+    c->dead = true;
+    return ST_ERR_CUDA;
+  }
+  return ST_OK;
+}
+
+// Read and clear the device error flags (call only after the producing stream synced).
+static st_status consume_flags(st_ctx* c) {
+  int h = 0;
+  ST_CUDA(c, cudaMemcpy(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (!h) return ST_OK;
+  ST_CUDA(c, cudaMemset(c->d_err, 0, sizeof(int)));
+  if (h & ERRF_CFL) return fail(c, ST_ERR_CFL, "displacement precondition violated (C-11/C-12: one wrap or bounce)");
+  if (h & ERRF_WINDOW)
+    return fail(c, ST_ERR_CFL, "a particle left this rank's field/source window between rebins (C-16)");
+  if (h & ERRF_DOMAIN) return fail(c, ST_ERR_OUT_OF_DOMAIN, "position outside [lo, hi]");
+  return ST_OK;
+}
+
+extern "C" {
+
+int32_t st_abi_version(void) { return ST_ABI_VERSION; }
+
+void st_config_default(st_config* c) {
+  if (!c) return;
+  memset(c, 0, sizeof(*c));
+  c->abi_version = ST_ABI_VERSION;
+  for (int a = 0; a < 3; ++a) {
+    c->dims[a] = 16;
+    c->origin[a] = 0.0;
+    c->cell_size[a] = 1.0 / 16.0;
+    c->bc[a] = ST_BC_PERIODIC;
+    c->gravity[a] = 0.0;
+  }
+  c->chunk_cells = 8;
+  c->rho_f = 1.2;
+  c->nu_f = 1.5e-5;
+  c->rho_p = 1000.0;
+  c->drag_law = ST_DRAG_SCHILLER_NAUMANN;
+  c->integrator = ST_INT_EXPONENTIAL;
+  c->coupling = ST_TWO_WAY;
+  c->rebin_interval = 1;
+  c->capacity = 1000000;
+  c->device = 0;
+  c->stream = nullptr;
+  c->rank = 0;
+  c->nranks = 1;
+  c->nccl_unique_id = nullptr;
+}
+
+const char* st_last_error(const st_ctx* c) { return c ? c->err.c_str() : g_init_error.c_str(); }
+
+static st_status validate(const st_config* c, std::string& why) {
+  if (c->abi_version != ST_ABI_VERSION) { why = "abi_version mismatch"; return ST_ERR_INVALID_ARG; }
+  for (int a = 0; a < 3; ++a) {
+    if (c->dims[a] < 1) { why = "dims must be >= 1"; return ST_ERR_INVALID_ARG; }
+    if (!(c->cell_size[a] > 0.0)) { why = "cell_size must be > 0"; return ST_ERR_INVALID_ARG; }
+    if (c->bc[a] != ST_BC_PERIODIC && c->bc[a] != ST_BC_REFLECT) { why = "bad bc"; return ST_ERR_INVALID_ARG; }
+  }
+  if ((int64_t)c->dims[0] * c->dims[1] * c->dims[2] > (int64_t)INT32_MAX) { why = "too many cells"; return ST_ERR_INVALID_ARG; }
+  if (c->chunk_cells < 1) { why = "chunk_cells must be >= 1"; return ST_ERR_INVALID_ARG; }
+  if (!(c->rho_f > 0 && c->nu_f > 0 && c->rho_p > 0)) { why = "densities and viscosity must be > 0"; return ST_ERR_INVALID_ARG; }
+  if (c->drag_law < 0 || c->drag_law > 1 || c->integrator < 0 || c->integrator > 1 || c->coupling < 0 ||
+      c->coupling > 1) { why = "bad enum"; return ST_ERR_INVALID_ARG; }
+  if (c->rebin_interval < 1) { why = "rebin_interval must be >= 1"; return ST_ERR_INVALID_ARG; }
+  if (c->capacity < 0) { why = "capacity must be >= 0"; return ST_ERR_INVALID_ARG; }
+  if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) { why = "bad rank/nranks"; return ST_ERR_INVALID_ARG; }
+  const int ncz = (c->dims[2] + c->chunk_cells - 1) / c->chunk_cells;
+  if (c->nranks > ncz) { why = "need at least one chunk plane per rank"; return ST_ERR_INVALID_ARG; }
+  if (c->nranks > 1 && !c->nccl_unique_id) { why = "nccl_unique_id required when nranks > 1"; return ST_ERR_INVALID_ARG; }
+  if (c->nranks > 1) {
+    // every slab must hold the (chunk_cells + 1)-plane field halo its neighbour needs
+    for (int r = 0; r < c->nranks; ++r) {
+      const int k0 = (int)(((int64_t)r * ncz) / c->nranks), k1 = (int)(((int64_t)(r + 1) * ncz) / c->nranks);
+      const int zz1 = k1 * c->chunk_cells < c->dims[2] ? k1 * c->chunk_cells : c->dims[2];
+      if (zz1 - k0 * c->chunk_cells < c->chunk_cells + 1) { why = "each rank needs >= chunk_cells+1 z planes"; return ST_ERR_INVALID_ARG; }
+    }
+  }
+  return ST_OK;
+}
+
+static void build_geometry(st_ctx* c) {
+  const st_config& f = c->cfg;
+  Geom& g = c->g;
+  memset(&g, 0, sizeof(g));
+  for (int a = 0; a < 3; ++a) {
+    g.n[a] = f.dims[a];
+    g.lo[a] = (float)f.origin[a];
+    g.ih[a] = (float)(1.0 / f.cell_size[a]);
+    g.hi[a] = (float)(f.origin[a] + (double)f.dims[a] * f.cell_size[a]);
+    g.L[a] = (float)((double)f.dims[a] * f.cell_size[a]);
+    g.bc[a] = f.bc[a];
+    g.NC[a] = (f.dims[a] + f.chunk_cells - 1) / f.chunk_cells;
+  }
+  g.cc = f.chunk_cells;
+  const int G = f.nranks, r = f.rank;
+  c->kz0 = (int)(((int64_t)r * g.NC[2]) / G);
+  c->kz1 = (int)(((int64_t)(r + 1) * g.NC[2]) / G);
+  c->z0 = c->kz0 * g.cc;
+  c->z1 = c->kz1 * g.cc < g.n[2] ? c->kz1 * g.cc : g.n[2];
+  c->H = G > 1 ? g.cc : 0;
+  g.gx = g.n[0] + 2;
+  g.gy = g.n[1] + 2;
+  g.wz0 = c->z0 - c->H - 1;
+  g.wnz = (c->z1 - c->z0) + 2 * c->H + 2;
+  g.az0 = c->z0 - c->H;
+  g.anz = (c->z1 - c->z0) + 2 * c->H;
+  g.wrapz = (G > 1 && f.bc[2] == ST_BC_PERIODIC) ? 1 : 0;
+  g.chunk_base = c->kz0 * g.NC[0] * g.NC[1];
+  c->chunk_lo = g.chunk_base;
+  c->n_local_chunks = (c->kz1 - c->kz0) * g.NC[0] * g.NC[1];
+  c->local_cells = (int64_t)g.n[0] * g.n[1] * (c->z1 - c->z0);
+  const int64_t nchunks = (int64_t)g.NC[0] * g.NC[1] * g.NC[2];
+  int bits = 1;
+  while (((int64_t)1 << bits) < nchunks) ++bits;
+  c->key_bits = bits;
+  // extended planes delivered to the ingest kernel (owned + one halo window each side)
+  c->ext_z0 = c->z0 - c->H - 1;
+  c->ext_nz = g.wnz;
+
+  Phys& p = c->p;
+  p.inv_nu = (float)(1.0 / f.nu_f);
+  p.tau_c = (float)(f.rho_p / (18.0 * f.rho_f * f.nu_f));
+  p.mass_c = (float)(M_PI / 6.0 * f.rho_p);
+  for (int a = 0; a < 3; ++a) p.g[a] = (float)f.gravity[a];
+  p.drag_law = f.drag_law;
+  p.integrator = f.integrator;
+  p.two_way = f.coupling == ST_TWO_WAY;
+}
+
+static st_status alloc_store(st_ctx* c, Store& s) {
+  const int64_t cap = c->cap > 0 ? c->cap : 1;
+  const size_t bytes = (size_t)cap * (6 * sizeof(float) + 2 * sizeof(float) + sizeof(uint64_t)) + 1024;
+  void* b = nullptr;
+  ST_CUDA(c, cudaMalloc(&b, bytes));
+  s.base = b;
+  char* q = (char*)b;
+  s.id = (uint64_t*)q;            // 8-byte aligned first
+  q += (size_t)cap * sizeof(uint64_t);
+  s.x = (float*)q;
+  q += (size_t)cap * 3 * sizeof(float);
+  s.u = (float*)q;
+  q += (size_t)cap * 3 * sizeof(float);
+  s.d = (float*)q;
+  q += (size_t)cap * sizeof(float);
+  s.w = (float*)q;
+  return ST_OK;
+}
+
+static st_status init_impl(st_ctx* c) {
+  ST_CUDA(c, cudaSetDevice(c->cfg.device));
+  build_geometry(c);
+  const Geom& g = c->g;
+  if (g.wrapz && g.wnz > g.n[2]) return fail(c, ST_ERR_UNSUPPORTED, "periodic z needs (slab + 2 halos + 2) <= nz per rank");
+  c->cap = c->cfg.capacity;
+  if (c->cfg.stream) {
+    c->cs = (cudaStream_t)c->cfg.stream;
+  } else {
+    ST_CUDA(c, cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+    c->own_cs = true;
+  }
+  ST_CUDA(c, cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    st_status s = alloc_store(c, c->S[i]);
+    if (s) return s;
+    ST_CUDA(c, cudaMalloc(&c->key[i], (size_t)(c->cap > 0 ? c->cap : 1) * sizeof(int32_t)));
+    ST_CUDA(c, cudaMalloc(&c->field[i], (size_t)g.wnz * g.gy * g.gx * sizeof(float4)));
+    ST_CUDA(c, cudaMemset(c->field[i], 0, (size_t)g.wnz * g.gy * g.gx * sizeof(float4)));
+    ST_CUDA(c, cudaMalloc(&c->acc[i], (size_t)g.anz * g.n[1] * g.n[0] * sizeof(float4)));
+    ST_CUDA(c, cudaMemset(c->acc[i], 0, (size_t)g.anz * g.n[1] * g.n[0] * sizeof(float4)));
+    ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_field_ready[i], cudaEventDisableTiming));
+    ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_field_reader[i], cudaEventDisableTiming));
+    ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_acc_writer[i], cudaEventDisableTiming));
+    ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_acc_free[i], cudaEventDisableTiming));
+  }
+  ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_readout_done, cudaEventDisableTiming));
+  ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  ST_CUDA(c, cudaEventCreate(&c->t_adv0));
+  ST_CUDA(c, cudaEventCreate(&c->t_adv1));
+  ST_CUDA(c, cudaEventCreate(&c->t_reb0));
+  ST_CUDA(c, cudaEventCreate(&c->t_reb1));
+  ST_CUDA(c, cudaMalloc(&c->field_stage, (size_t)3 * c->ext_nz * g.n[1] * g.n[0] * sizeof(float)));
+  ST_CUDA(c, cudaMalloc(&c->S_dev, (size_t)3 * (c->local_cells > 0 ? c->local_cells : 1) * sizeof(float)));
+  ST_CUDA(c, cudaMalloc(&c->d_err, sizeof(int)));
+  ST_CUDA(c, cudaMemset(c->d_err, 0, sizeof(int)));
+  ST_CUDA(c, cudaMalloc(&c->offsets, (size_t)(c->n_local_chunks + 1) * sizeof(int64_t)));
+  ST_CUDA(c, cudaMemset(c->offsets, 0, (size_t)(c->n_local_chunks + 1) * sizeof(int64_t)));
+  // radix-sort scratch
+  c->sc.max_blocks = (c->cap + 4095) / 4096 + 1;
+  const int64_t m = 256 * c->sc.max_blocks;
+  c->sc.partial_cap = (m + 4095) / 4096 + 1;
+  ST_CUDA(c, cudaMalloc(&c->sc.hist, (size_t)m * sizeof(uint32_t)));
+  ST_CUDA(c, cudaMalloc(&c->sc.offs, (size_t)(m + 1) * sizeof(int64_t)));
+  ST_CUDA(c, cudaMalloc(&c->sc.partial, (size_t)c->sc.partial_cap * sizeof(int64_t)));
+  c->mig_row.assign(c->cfg.nranks, 0);
+  c->next_id = (uint64_t)c->cfg.rank << 40;
+  if (c->cfg.nranks > 1) {
+    std::string why;
+    c->comm = comm_create(c->cfg.nccl_unique_id, c->cfg.rank, c->cfg.nranks, c->cs, why);
+    if (!c->comm) return fail(c, ST_ERR_NCCL, why);
+  }
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  return ST_OK;
+}
+
+st_status st_destroy(st_ctx* c) {
+  if (!c) return ST_OK;
+  if (c->cs) cudaStreamSynchronize(c->cs);
+  if (c->xs) cudaStreamSynchronize(c->xs);
+  if (c->comm) comm_destroy(c->comm);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c->S[i].base);
+    cudaFree(c->key[i]);
+    cudaFree(c->field[i]);
+    cudaFree(c->acc[i]);
+    if (c->ev_field_ready[i]) cudaEventDestroy(c->ev_field_ready[i]);
+    if (c->ev_field_reader[i]) cudaEventDestroy(c->ev_field_reader[i]);
+    if (c->ev_acc_writer[i]) cudaEventDestroy(c->ev_acc_writer[i]);
+    if (c->ev_acc_free[i]) cudaEventDestroy(c->ev_acc_free[i]);
+  }
+  cudaFree(c->field_stage);
+  cudaFree(c->S_dev);
+  cudaFree(c->d_err);
+  cudaFree(c->offsets);
+  cudaFree(c->sc.hist);
+  cudaFree(c->sc.offs);
+  cudaFree(c->sc.partial);
+  for (cudaEvent_t e : {c->ev_readout_done, c->ev_in, c->t_adv0, c->t_adv1, c->t_reb0, c->t_reb1})
+    if (e) cudaEventDestroy(e);
+  if (c->own_cs && c->cs) cudaStreamDestroy(c->cs);
+  if (c->xs) cudaStreamDestroy(c->xs);
+  cudaGetLastError();
+  delete c;
+  return ST_OK;
+}
+
+st_status st_init(const st_config* cfg, st_ctx** out) {
+  if (!out) return ST_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!cfg) {
+    g_init_error = "cfg is NULL";
+    return ST_ERR_INVALID_ARG;
+  }
+  std::string why;
+  st_status s = validate(cfg, why);
+  if (s) {
+    g_init_error = why;
+    return s;
+  }
+  st_ctx* c = new st_ctx();
+  c->cfg = *cfg;
+  s = init_impl(c);
+  if (s) {
+    g_init_error = c->err;
+    st_destroy(c);
+    return s;
+  }
+  *out = c;
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------- field in
+st_status st_set_fluid_field(st_ctx* c, const float* u) {
+  ST_ALIVE(c);
+  if (!u) return fail(c, ST_ERR_INVALID_ARG, "u is NULL");
+  const int back = c->pending >= 0 ? c->pending : (c->front < 0 ? 0 : 1 - c->front);
+  // the back buffer may still be read by an advance enqueued earlier
+  ST_CUDA(c, cudaStreamWaitEvent(c->xs, c->ev_field_reader[back], 0));
+  const Geom& g = c->g;
+  const int64_t own_cells = c->local_cells;
+  const bool dev = is_device_ptr(u);
+  float* stage = c->field_stage;
+  // staging layout: [3][ext_nz][ny][nx]; owned planes start at plane (z0 - ext_z0)
+  const int64_t plane = (int64_t)g.n[0] * g.n[1];
+  const int64_t comp = (int64_t)c->ext_nz * plane;
+  const int own_off = c->z0 - c->ext_z0;
+  if (dev) {
+    ST_CUDA(c, cudaEventRecord(c->ev_in, c->cs));
+    ST_CUDA(c, cudaStreamWaitEvent(c->xs, c->ev_in, 0));
+  }
+  for (int k = 0; k < 3; ++k)
+    ST_CUDA(c, cudaMemcpyAsync(stage + k * comp + own_off * plane, u + k * own_cells, own_cells * sizeof(float),
+                               dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->xs));
+  if (!dev) {
+    // host inputs are consumed before the call returns (header contract)
+    ST_CUDA(c, cudaEventRecord(c->ev_in, c->xs));
+    ST_CUDA(c, cudaEventSynchronize(c->ev_in));
+  }
+  int src_z0 = c->z0, src_nz = c->z1 - c->z0;
+  if (c->comm) {
+    std::string why;
+    if (comm_field_halo(c->comm, stage, comp, plane, c->ext_z0, c->ext_nz, c->z0, c->z1, g.n[2], g.bc[2], c->xs, why))
+      return fail(c, ST_ERR_NCCL, why);
+    src_z0 = c->ext_z0;
+    src_nz = c->ext_nz;
+  }
+  const float* src = stage + (c->comm ? 0 : own_off * plane);
+  st_status s = check_launch(c, launch_field_ingest(g, src, comp, src_z0, src_nz, c->field[back], c->xs));
+  if (s) return s;
+  ST_CUDA(c, cudaEventRecord(c->ev_field_ready[back], c->xs));
+  c->pending = back;
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------- inject
+st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const float* d, const float* w,
+                    const uint64_t* id) {
+  ST_ALIVE(c);
+  if (n < 0) return fail(c, ST_ERR_INVALID_ARG, "n < 0");
+  if (n == 0) return ST_OK;
+  if (!x || !u || !d) return fail(c, ST_ERR_INVALID_ARG, "x, u and d are required");
+  if (c->n + n > c->cap) return fail(c, ST_ERR_CAPACITY, "store capacity exceeded");
+  Store s = c->S[c->cur];
+  const int64_t o = c->n, cap = c->cap;
+  auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
+  for (int a = 0; a < 3; ++a) {
+    ST_CUDA(c, cudaMemcpyAsync(s.x + a * cap + o, x + a * n, n * sizeof(float), kind(x), c->cs));
+    ST_CUDA(c, cudaMemcpyAsync(s.u + a * cap + o, u + a * n, n * sizeof(float), kind(u), c->cs));
+  }
+  ST_CUDA(c, cudaMemcpyAsync(s.d + o, d, n * sizeof(float), kind(d), c->cs));
+  int nl = 0;
+  if (w) {
+    ST_CUDA(c, cudaMemcpyAsync(s.w + o, w, n * sizeof(float), kind(w), c->cs));
+  } else {
+    nl += launch_fill_f32(s.w + o, n, 1.0f, c->cs);
+  }
+  if (id) {
+    ST_CUDA(c, cudaMemcpyAsync(s.id + o, id, n * sizeof(uint64_t), kind(id), c->cs));
+  } else {
+    nl += launch_fill_u64_seq(s.id + o, n, c->next_id, c->cs);
+  }
+  nl += launch_check_domain(c->g, s.x + o, cap, n, c->d_err, c->cs);
+  st_status st = check_launch(c, nl);
+  if (st) return st;
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  st = consume_flags(c);
+  if (st) return st;   // nothing appended: c->n unchanged
+  if (!id) c->next_id += (uint64_t)n;
+  c->n += n;
+  c->keys_valid = false;
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------- rebin
+// C-15 / C-16: stable sort by chunk of the current positions; with nranks > 1
+// movers go to their owner first (kept ++ arrivals by source rank, then sort).
+static st_status rebin(st_ctx* c) {
+  if (!c->keys_valid) {
+    st_status s = check_launch(c, launch_keys(c->g, c->S[c->cur].x, c->cap, c->n, c->key[c->cur], c->cs));
+    if (s) return s;
+  }
+  ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
+  int in_b = 0;
+  const int other = 1 - c->cur;
+  int nl = launch_stable_sort(c->S[c->cur], c->S[other], c->cap, c->n, c->key[c->cur], c->key[other], c->key_bits,
+                              c->sc, &in_b, c->cs);
+  if (nl < 0) return fail(c, ST_ERR_CAPACITY, "sort scratch too small");
+  st_status s = check_launch(c, nl);
+  if (s) return s;
+  if (in_b) c->cur = other;
+  if (c->comm) {
+    std::string why;
+    int64_t n_new = 0;
+    nl = 0;
+    int rc = comm_migrate(c->comm, c->g, c->S, &c->cur, c->key, c->cap, c->n, c->chunk_lo, c->n_local_chunks,
+                          c->key_bits, c->sc, c->mig_row.data(), &n_new, &nl, c->cs, why);
+    c->launches += nl;
+    if (rc == 3) return fail(c, ST_ERR_CAPACITY, why);
+    if (rc) return fail(c, ST_ERR_NCCL, why);
+    c->last_sent = 0;
+    for (int r = 0; r < c->cfg.nranks; ++r)
+      if (r != c->cfg.rank) c->last_sent += c->mig_row[r];
+    c->last_recv = n_new - c->mig_row[c->cfg.rank];
+    c->n = n_new;
+  } else {
+    c->mig_row[0] = c->n;
+  }
+  s = check_launch(c, launch_chunk_offsets(c->key[c->cur], c->n, c->chunk_lo, c->n_local_chunks, c->offsets, c->cs));
+  if (s) return s;
+  ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));
+  c->timed_reb = true;
+  c->keys_valid = true;
+  c->rebins += 1;
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------- advance
+st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
+  ST_ALIVE(c);
+  if (!(dt > 0.0) || nsteps < 1) return fail(c, ST_ERR_INVALID_ARG, "dt must be > 0 and nsteps >= 1");
+  if (c->pending >= 0) {
+    ST_CUDA(c, cudaStreamWaitEvent(c->cs, c->ev_field_ready[c->pending], 0));
+    c->front = c->pending;
+    c->pending = -1;
+  }
+  if (c->front < 0) return fail(c, ST_ERR_STATE, "st_advance before st_set_fluid_field (P:202: first step is synchronous)");
+  // the accumulator must be free (its previous readout finished zeroing it)
+  ST_CUDA(c, cudaStreamWaitEvent(c->cs, c->ev_acc_free[c->acc_cur], 0));
+  ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
+  Store s = c->S[c->cur];
+  st_status st = check_launch(c, launch_advance(c->g, c->p, c->field[c->front], c->acc[c->acc_cur], s, c->cap, c->n,
+                                                nullptr, 0, (float)dt, nsteps, c->key[c->cur], c->d_err, c->cs));
+  if (st) return st;
+  ST_CUDA(c, cudaEventRecord(c->t_adv1, c->cs));
+  c->timed_adv = true;
+  c->keys_valid = true;
+  ST_CUDA(c, cudaEventRecord(c->ev_field_reader[c->front], c->cs));
+  ST_CUDA(c, cudaEventRecord(c->ev_acc_writer[c->acc_cur], c->cs));
+  c->T_acc[c->acc_cur] += (double)nsteps * dt;
+  c->calls += 1;
+  if (c->calls % c->cfg.rebin_interval == 0) {
+    st = rebin(c);
+    if (st) return st;
+  } else {
+    c->timed_reb = false;
+  }
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------- sources out
+st_status st_request_sources(st_ctx* c) {
+  ST_ALIVE(c);
+  if (c->readout_pending) return fail(c, ST_ERR_STATE, "previous readout not yet waited for");
+  const int old = c->acc_cur;
+  c->acc_cur = 1 - old;
+  c->readout_T = c->T_acc[old];
+  c->T_acc[old] = 0.0;
+  const Geom& g = c->g;
+  ST_CUDA(c, cudaStreamWaitEvent(c->xs, c->ev_acc_writer[old], 0));
+  if (c->comm) {
+    std::string why;
+    if (comm_source_halo(c->comm, c->acc[old], g, c->z0, c->z1, c->H, c->xs, why)) return fail(c, ST_ERR_NCCL, why);
+  }
+  const double V = c->cfg.cell_size[0] * c->cfg.cell_size[1] * c->cfg.cell_size[2];
+  const float scale = c->readout_T > 0.0 ? (float)(1.0 / (V * c->readout_T)) : 0.0f;
+  st_status s = check_launch(c, launch_source_readout(g, c->acc[old], c->z0, c->z1, scale, c->S_dev, c->xs));
+  if (s) return s;
+  ST_CUDA(c, cudaMemsetAsync(c->acc[old], 0, (size_t)g.anz * g.n[1] * g.n[0] * sizeof(float4), c->xs));
+  ST_CUDA(c, cudaEventRecord(c->ev_acc_free[old], c->xs));
+  ST_CUDA(c, cudaEventRecord(c->ev_readout_done, c->xs));
+  c->readout_pending = true;
+  return ST_OK;
+}
+
+st_status st_wait_sources(st_ctx* c, float* S, double* interval_s) {
+  ST_ALIVE(c);
+  if (!c->readout_pending) return fail(c, ST_ERR_STATE, "no readout requested");
+  c->readout_pending = false;
+  if (S) {
+    const bool dev = is_device_ptr(S);
+    ST_CUDA(c, cudaMemcpyAsync(S, c->S_dev, 3 * c->local_cells * sizeof(float),
+                               dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->xs));
+  }
+  ST_CUDA(c, cudaStreamSynchronize(c->xs));
+  if (interval_s) *interval_s = c->readout_T;
+  return consume_flags(c);
+}
+
+st_status st_get_sources(st_ctx* c, float* S, double* interval_s) {
+  st_status s = st_request_sources(c);
+  if (s) return s;
+  return st_wait_sources(c, S, interval_s);
+}
+
+// ---------------------------------------------------------------- queries
+st_status st_sync(st_ctx* c) {
+  ST_ALIVE(c);
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  ST_CUDA(c, cudaStreamSynchronize(c->xs));
+  return consume_flags(c);
+}
+
+st_status st_get_count(st_ctx* c, int64_t* n) {
+  ST_ALIVE(c);
+  if (!n) return ST_ERR_INVALID_ARG;
+  *n = c->n;
+  return ST_OK;
+}
+
+st_status st_get_particles(st_ctx* c, int64_t cap, int64_t* n_out, float* x, float* u, float* d, float* w,
+                           uint64_t* id, int32_t* cell, int32_t* chunk) {
+  ST_ALIVE(c);
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  st_status st = consume_flags(c);
+  if (st) return st;
+  if (n_out) *n_out = c->n;
+  if (cap < c->n) return fail(c, ST_ERR_CAPACITY, "output capacity smaller than the store");
+  const int64_t n = c->n;
+  if (n == 0) return ST_OK;
+  Store s = c->S[c->cur];
+  auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost; };
+  for (int a = 0; a < 3; ++a) {
+    if (x) ST_CUDA(c, cudaMemcpyAsync(x + a * cap, s.x + a * c->cap, n * sizeof(float), kind(x), c->cs));
+    if (u) ST_CUDA(c, cudaMemcpyAsync(u + a * cap, s.u + a * c->cap, n * sizeof(float), kind(u), c->cs));
+  }
+  if (d) ST_CUDA(c, cudaMemcpyAsync(d, s.d, n * sizeof(float), kind(d), c->cs));
+  if (w) ST_CUDA(c, cudaMemcpyAsync(w, s.w, n * sizeof(float), kind(w), c->cs));
+  if (id) ST_CUDA(c, cudaMemcpyAsync(id, s.id, n * sizeof(uint64_t), kind(id), c->cs));
+  if (cell || chunk) {
+    int32_t* tmp = nullptr;
+    ST_CUDA(c, cudaMallocAsync(&tmp, 2 * n * sizeof(int32_t), c->cs));
+    st = check_launch(c, launch_locate(c->g, s.x, c->cap, n, tmp, tmp + n, c->cs));
+    if (st) return st;
+    if (cell) ST_CUDA(c, cudaMemcpyAsync(cell, tmp, n * sizeof(int32_t), kind(cell), c->cs));
+    if (chunk) ST_CUDA(c, cudaMemcpyAsync(chunk, tmp + n, n * sizeof(int32_t), kind(chunk), c->cs));
+    ST_CUDA(c, cudaFreeAsync(tmp, c->cs));
+  }
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  return ST_OK;
+}
+
+st_status st_locate(st_ctx* c, int64_t n, const float* x, int32_t* cell, int32_t* chunk) {
+  ST_ALIVE(c);
+  if (n < 0 || (n > 0 && !x)) return fail(c, ST_ERR_INVALID_ARG, "bad arguments");
+  if (n == 0) return ST_OK;
+  float* dx = nullptr;
+  int32_t* tmp = nullptr;
+  const bool xdev = is_device_ptr(x);
+  ST_CUDA(c, cudaMallocAsync(&tmp, 2 * n * sizeof(int32_t), c->cs));
+  if (!xdev) {
+    ST_CUDA(c, cudaMallocAsync(&dx, 3 * n * sizeof(float), c->cs));
+    ST_CUDA(c, cudaMemcpyAsync(dx, x, 3 * n * sizeof(float), cudaMemcpyHostToDevice, c->cs));
+  }
+  st_status st = check_launch(c, launch_locate(c->g, xdev ? x : dx, n, n, tmp, tmp + n, c->cs));
+  if (st) return st;
+  auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost; };
+  if (cell) ST_CUDA(c, cudaMemcpyAsync(cell, tmp, n * sizeof(int32_t), kind(cell), c->cs));
+  if (chunk) ST_CUDA(c, cudaMemcpyAsync(chunk, tmp + n, n * sizeof(int32_t), kind(chunk), c->cs));
+  ST_CUDA(c, cudaFreeAsync(tmp, c->cs));
+  if (dx) ST_CUDA(c, cudaFreeAsync(dx, c->cs));
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  return ST_OK;
+}
+
+st_status st_get_migration_counts(st_ctx* c, int64_t* row) {
+  ST_ALIVE(c);
+  if (!row) return ST_ERR_INVALID_ARG;
+  for (int r = 0; r < c->cfg.nranks; ++r) row[r] = c->mig_row[r];
+  return ST_OK;
+}
+
+st_status st_get_layout(st_ctx* c, st_layout* o) {
+  ST_ALIVE(c);
+  if (!o) return ST_ERR_INVALID_ARG;
+  o->z0 = c->z0;
+  o->z1 = c->z1;
+  o->kz0 = c->kz0;
+  o->kz1 = c->kz1;
+  o->n_chunks_global = c->g.NC[0] * c->g.NC[1] * c->g.NC[2];
+  for (int a = 0; a < 3; ++a) o->nchunk[a] = c->g.NC[a];
+  o->local_cells = c->local_cells;
+  o->halo_cells = c->H;
+  return ST_OK;
+}
+
+st_status st_get_stats(st_ctx* c, st_stats* o) {
+  ST_ALIVE(c);
+  if (!o) return ST_ERR_INVALID_ARG;
+  o->n_particles = c->n;
+  o->calls = c->calls;
+  o->rebins = c->rebins;
+  o->last_movers = c->last_movers;
+  o->last_sent_total = c->last_sent;
+  o->last_recv_total = c->last_recv;
+  o->fused_rebins = c->fused_rebins;
+  o->kernel_launches = c->launches;
+  return ST_OK;
+}
+
+st_status st_last_timings(st_ctx* c, float* advance_ms, float* rebin_ms) {
+  ST_ALIVE(c);
+  if (advance_ms) {
+    *advance_ms = 0.0f;
+    if (c->timed_adv) {
+      ST_CUDA(c, cudaEventSynchronize(c->t_adv1));
+      ST_CUDA(c, cudaEventElapsedTime(advance_ms, c->t_adv0, c->t_adv1));
+    }
+  }
+  if (rebin_ms) {
+    *rebin_ms = 0.0f;
+    if (c->timed_reb) {
+      ST_CUDA(c, cudaEventSynchronize(c->t_reb1));
+      ST_CUDA(c, cudaEventElapsedTime(rebin_ms, c->t_reb0, c->t_reb1));
+    }
+  }
+  return ST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,274 @@
+// KB4/KB5 + NCCL plumbing for the one-box multi-GPU path.
+// Rank r owns chunk planes [floor(r*NCz/G), floor((r+1)*NCz/G)) (C-16).  All
+// NCCL calls run on one private stream in API-call order, so every rank issues
+// them in the same order; the caller's stream is joined with events.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "st_comm.h"
+
+namespace st {
+
+struct Comm {
+  ncclComm_t nc = nullptr;
+  int rank = 0, nranks = 1;
+  cudaStream_t ns = nullptr;
+  cudaEvent_t e_in = nullptr, e_out = nullptr;
+  float4* halo_recv = nullptr;  // 2 * H * plane float4 (source halo receive)
+  int64_t halo_cap = 0;
+  int64_t* d_counts = nullptr;  // [nranks * nranks]
+  int64_t* d_bounds = nullptr;  // [nranks + 1]
+  int32_t* d_bases = nullptr;   // [nranks + 1]
+};
+
+namespace {
+
+__global__ void k_rank_bounds(const int32_t* __restrict__ key, int64_t n, const int32_t* __restrict__ bases, int nb,
+                              int64_t* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nb) return;
+  const int32_t target = bases[q];
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (key[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  out[q] = lo;
+}
+
+// KB5: acc[dst_plane + p] += recv[p] over `planes` planes.
+__global__ void k_halo_add(float4* __restrict__ acc, const float4* __restrict__ recv, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = acc[i];
+    const float4 b = recv[i];
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    acc[i] = a;
+  }
+}
+
+inline int plane_owner_lo(int r, int ncz, int G) { return (int)(((int64_t)r * ncz) / G); }
+
+#define NCCK(call, why)                                                    \
+  do {                                                                     \
+    ncclResult_t r_ = (call);                                              \
+    if (r_ != ncclSuccess) {                                               \
+      why = std::string(#call) + ": " + ncclGetErrorString(r_);            \
+      return 1;                                                            \
+    }                                                                      \
+  } while (0)
+#define CUCK(call, why)                                                    \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess) {                                               \
+      why = std::string(#call) + ": " + cudaGetErrorString(e_);            \
+      return 1;                                                            \
+    }                                                                      \
+  } while (0)
+
+int join_in(Comm* c, cudaStream_t s, std::string& why) {
+  CUCK(cudaEventRecord(c->e_in, s), why);
+  CUCK(cudaStreamWaitEvent(c->ns, c->e_in, 0), why);
+  return 0;
+}
+int join_out(Comm* c, cudaStream_t s, std::string& why) {
+  CUCK(cudaEventRecord(c->e_out, c->ns), why);
+  CUCK(cudaStreamWaitEvent(s, c->e_out, 0), why);
+  return 0;
+}
+
+}  // namespace
+
+Comm* comm_create(const void* unique_id, int rank, int nranks, cudaStream_t s, std::string& why) {
+  (void)s;
+  Comm* c = new Comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&c->nc, nranks, id, rank);
+  if (r != ncclSuccess) {
+    why = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+    delete c;
+    return nullptr;
+  }
+  if (cudaStreamCreateWithFlags(&c->ns, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->e_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->e_out, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&c->d_counts, sizeof(int64_t) * nranks * nranks) != cudaSuccess ||
+      cudaMalloc(&c->d_bounds, sizeof(int64_t) * (nranks + 1)) != cudaSuccess ||
+      cudaMalloc(&c->d_bases, sizeof(int32_t) * (nranks + 1)) != cudaSuccess) {
+    why = "comm_create: CUDA allocation failed";
+    comm_destroy(c);
+    return nullptr;
+  }
+  return c;
+}
+
+void comm_destroy(Comm* c) {
+  if (!c) return;
+  if (c->ns) cudaStreamSynchronize(c->ns);
+  if (c->nc) ncclCommDestroy(c->nc);
+  if (c->ns) cudaStreamDestroy(c->ns);
+  if (c->e_in) cudaEventDestroy(c->e_in);
+  if (c->e_out) cudaEventDestroy(c->e_out);
+  cudaFree(c->halo_recv);
+  cudaFree(c->d_counts);
+  cudaFree(c->d_bounds);
+  cudaFree(c->d_bases);
+  delete c;
+}
+
+int comm_field_halo(Comm* c, float* stage, int64_t comp, int64_t plane, int ext_z0, int ext_nz, int z0, int z1,
+                    int nz, int bc_z, cudaStream_t s, std::string& why) {
+  const int G = c->nranks, r = c->rank;
+  const bool periodic = bc_z == ST_BC_PERIODIC;
+  const int up = (r + 1 < G) ? r + 1 : (periodic ? 0 : -1);
+  const int dn = (r > 0) ? r - 1 : (periodic ? G - 1 : -1);
+  const int own = z0 - ext_z0;              // = H + 1 planes of halo below
+  const int nh = own;                       // planes exchanged per side
+  const int slab = z1 - z0;
+  (void)ext_nz;
+  (void)nz;
+  const size_t cnt = (size_t)nh * plane;
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclGroupStart(), why);
+  for (int k = 0; k < 3; ++k)  // my top nh owned planes -> upper neighbour's lower halo
+    if (up >= 0) NCCK(ncclSend(stage + k * comp + (int64_t)(own + slab - nh) * plane, cnt, ncclFloat, up, c->nc, c->ns), why);
+  for (int k = 0; k < 3; ++k)  // my bottom nh owned planes -> lower neighbour's upper halo
+    if (dn >= 0) NCCK(ncclSend(stage + k * comp + (int64_t)own * plane, cnt, ncclFloat, dn, c->nc, c->ns), why);
+  for (int k = 0; k < 3; ++k)
+    if (dn >= 0) NCCK(ncclRecv(stage + k * comp, cnt, ncclFloat, dn, c->nc, c->ns), why);
+  for (int k = 0; k < 3; ++k)
+    if (up >= 0) NCCK(ncclRecv(stage + k * comp + (int64_t)(own + slab) * plane, cnt, ncclFloat, up, c->nc, c->ns), why);
+  NCCK(ncclGroupEnd(), why);
+  return join_out(c, s, why);
+}
+
+int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H, cudaStream_t s, std::string& why) {
+  const int G = c->nranks, r = c->rank;
+  const bool periodic = g.bc[2] == ST_BC_PERIODIC;
+  const int up = (r + 1 < G) ? r + 1 : (periodic ? 0 : -1);
+  const int dn = (r > 0) ? r - 1 : (periodic ? G - 1 : -1);
+  const int64_t plane = (int64_t)g.n[0] * g.n[1];
+  const int slab = z1 - z0;
+  const int64_t cnt = (int64_t)H * plane;   // float4 per side
+  if (c->halo_cap < 2 * cnt) {
+    cudaFree(c->halo_recv);
+    c->halo_recv = nullptr;
+    CUCK(cudaMalloc(&c->halo_recv, sizeof(float4) * 2 * cnt), why);
+    c->halo_cap = 2 * cnt;
+  }
+  float4* from_up = c->halo_recv;         // adds to my top H owned planes
+  float4* from_dn = c->halo_recv + cnt;   // adds to my bottom H owned planes
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclGroupStart(), why);
+  if (dn >= 0) NCCK(ncclSend(acc, (size_t)cnt * 4, ncclFloat, dn, c->nc, c->ns), why);                       // lower halo
+  if (up >= 0) NCCK(ncclSend(acc + (int64_t)(H + slab) * plane, (size_t)cnt * 4, ncclFloat, up, c->nc, c->ns), why);  // upper halo
+  if (up >= 0) NCCK(ncclRecv(from_up, (size_t)cnt * 4, ncclFloat, up, c->nc, c->ns), why);
+  if (dn >= 0) NCCK(ncclRecv(from_dn, (size_t)cnt * 4, ncclFloat, dn, c->nc, c->ns), why);
+  NCCK(ncclGroupEnd(), why);
+  const unsigned grid = (unsigned)((cnt + 255) / 256 < 148 * 16 ? (cnt + 255) / 256 : 148 * 16);
+  if (up >= 0) k_halo_add<<<grid, 256, 0, c->ns>>>(acc + (int64_t)slab * plane, from_up, cnt);
+  if (dn >= 0) k_halo_add<<<grid, 256, 0, c->ns>>>(acc + (int64_t)H * plane, from_dn, cnt);
+  CUCK(cudaGetLastError(), why);
+  return join_out(c, s, why);
+}
+
+int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int64_t cap, int64_t n, int32_t chunk_lo,
+                 int32_t n_local_chunks, int key_bits, SortScratch& sc, int64_t* row, int64_t* n_new, int* launches,
+                 cudaStream_t s, std::string& why) {
+  (void)chunk_lo;
+  (void)n_local_chunks;
+  const int G = c->nranks, r = c->rank;
+  const int ncxy = g.NC[0] * g.NC[1];
+  std::vector<int32_t> bases(G + 1);
+  for (int q = 0; q <= G; ++q) bases[q] = plane_owner_lo(q, g.NC[2], G) * ncxy;
+  CUCK(cudaMemcpyAsync(c->d_bases, bases.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, s), why);
+  k_rank_bounds<<<1, 64, 0, s>>>(key[*cur], n, c->d_bases, G + 1, c->d_bounds);
+  *launches += 1;
+  std::vector<int64_t> b(G + 1), cnt(G), M((size_t)G * G);
+  CUCK(cudaMemcpyAsync(b.data(), c->d_bounds, sizeof(int64_t) * (G + 1), cudaMemcpyDeviceToHost, s), why);
+  CUCK(cudaStreamSynchronize(s), why);
+  b[0] = 0;
+  b[G] = n;
+  for (int q = 0; q < G; ++q) cnt[q] = b[q + 1] - b[q];
+  CUCK(cudaMemcpyAsync(c->d_counts + (size_t)r * G, cnt.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, s), why);
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclAllGather(c->d_counts + (size_t)r * G, c->d_counts, G, ncclInt64, c->nc, c->ns), why);
+  CUCK(cudaMemcpyAsync(M.data(), c->d_counts, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, c->ns), why);
+  CUCK(cudaStreamSynchronize(c->ns), why);
+  for (int q = 0; q < G; ++q) row[q] = M[(size_t)r * G + q];
+  int64_t total = M[(size_t)r * G + r];
+  for (int src = 0; src < G; ++src)
+    if (src != r) total += M[(size_t)src * G + r];
+  if (total > cap) {
+    why = "migration would exceed the store capacity";
+    return 3;
+  }
+  const int o = 1 - *cur;
+  Store A = S[*cur], B = S[o];
+  // kept segment first (in order)
+  const int64_t kept = cnt[r], k0 = b[r];
+  if (kept > 0) {
+    for (int a = 0; a < 3; ++a) {
+      CUCK(cudaMemcpyAsync(B.x + a * cap, A.x + a * cap + k0, kept * sizeof(float), cudaMemcpyDeviceToDevice, c->ns), why);
+      CUCK(cudaMemcpyAsync(B.u + a * cap, A.u + a * cap + k0, kept * sizeof(float), cudaMemcpyDeviceToDevice, c->ns), why);
+    }
+    CUCK(cudaMemcpyAsync(B.d, A.d + k0, kept * sizeof(float), cudaMemcpyDeviceToDevice, c->ns), why);
+    CUCK(cudaMemcpyAsync(B.w, A.w + k0, kept * sizeof(float), cudaMemcpyDeviceToDevice, c->ns), why);
+    CUCK(cudaMemcpyAsync(B.id, A.id + k0, kept * sizeof(uint64_t), cudaMemcpyDeviceToDevice, c->ns), why);
+  }
+  NCCK(ncclGroupStart(), why);
+  for (int q = 0; q < G; ++q) {
+    if (q == r || cnt[q] == 0) continue;
+    const int64_t o0 = b[q], m = cnt[q];
+    for (int a = 0; a < 3; ++a) NCCK(ncclSend(A.x + a * cap + o0, m, ncclFloat, q, c->nc, c->ns), why);
+    for (int a = 0; a < 3; ++a) NCCK(ncclSend(A.u + a * cap + o0, m, ncclFloat, q, c->nc, c->ns), why);
+    NCCK(ncclSend(A.d + o0, m, ncclFloat, q, c->nc, c->ns), why);
+    NCCK(ncclSend(A.w + o0, m, ncclFloat, q, c->nc, c->ns), why);
+    NCCK(ncclSend(A.id + o0, m, ncclUint64, q, c->nc, c->ns), why);
+  }
+  int64_t pos = kept;
+  for (int src = 0; src < G; ++src) {
+    const int64_t m = M[(size_t)src * G + r];
+    if (src == r || m == 0) continue;
+    for (int a = 0; a < 3; ++a) NCCK(ncclRecv(B.x + a * cap + pos, m, ncclFloat, src, c->nc, c->ns), why);
+    for (int a = 0; a < 3; ++a) NCCK(ncclRecv(B.u + a * cap + pos, m, ncclFloat, src, c->nc, c->ns), why);
+    NCCK(ncclRecv(B.d + pos, m, ncclFloat, src, c->nc, c->ns), why);
+    NCCK(ncclRecv(B.w + pos, m, ncclFloat, src, c->nc, c->ns), why);
+    NCCK(ncclRecv(B.id + pos, m, ncclUint64, src, c->nc, c->ns), why);
+    pos += m;
+  }
+  NCCK(ncclGroupEnd(), why);
+  if (join_out(c, s, why)) return 1;
+  // kept ++ arrivals -> stable sort by chunk (C-16)
+  *launches += launch_keys(g, B.x, cap, total, key[o], s);
+  int in_other = 0;
+  const int nl = launch_stable_sort(B, A, cap, total, key[o], key[*cur], key_bits, sc, &in_other, s);
+  if (nl < 0) {
+    why = "sort scratch too small";
+    return 3;
+  }
+  *launches += nl;
+  *cur = in_other ? *cur : o;
+  *n_new = total;
+  CUCK(cudaGetLastError(), why);
+  return 0;
+}
+
+}  // namespace st
+
+extern "C" st_status st_nccl_unique_id(void* out) {
+  if (!out) return ST_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return ST_ERR_NCCL;
+  memcpy(out, &id, sizeof(id));
+  return ST_OK;
+}

@@ -1,0 +1,45 @@
+// Multi-GPU exchange over NCCL: z-slab ownership of
+// chunk planes, field-halo exchange at ingest, halo-source exchange at readout,
+// particle migration at rebin (counts by all-gather, payload by grouped send/recv).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "st_internal.h"
+
+namespace st {
+
+struct Comm;
+
+Comm* comm_create(const void* unique_id, int rank, int nranks, cudaStream_t s, std::string& why);
+void comm_destroy(Comm* c);
+
+// Fill the halo planes of the field staging buffer [3][ext_nz][ny][nx] (owned
+// planes at ext index z0-ext_z0 ..) from the neighbour slabs.  Returns 0 on success.
+int comm_field_halo(Comm* c, float* stage, int64_t comp_stride, int64_t plane, int ext_z0, int ext_nz, int z0,
+                    int z1, int nz, int bc_z, cudaStream_t s, std::string& why);
+
+// Send this rank's halo source planes to their owners and add the received ones
+// into the owned planes of acc (float4 window [anz][ny][nx]).  Zeroing the
+// whole window afterwards is the caller's job.
+int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H, cudaStream_t s, std::string& why);
+
+// Migration after the local stable sort (store S[*cur] sorted by key[*cur]):
+// send each owner segment to its rank, build kept ++ arrivals (ascending source
+// rank) in the other buffer, and stable-sort it by chunk (C-16).  row[dst] gets
+// this rank's send counts; *n_new the new local count; *launches the kernels.
+// Returns 0 ok, 1 NCCL/CUDA error, 3 capacity.
+int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int64_t cap, int64_t n,
+                 int32_t chunk_lo, int32_t n_local_chunks, int key_bits, SortScratch& sc, int64_t* row,
+                 int64_t* n_new, int* launches, cudaStream_t s, std::string& why);
+
+}  // namespace st
+
+extern "C" {
+// Exported helper: write a fresh 128-byte ncclUniqueId into out (rank 0 calls it
+// and broadcasts the bytes through torch.distributed).
+st_status st_nccl_unique_id(void* out);
+}

@@ -1,0 +1,295 @@
+"""GPU (CUDA, through the C-ABI) vs the fp32 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * integer work (cell, chunk, rebin order, migration counts) bit-exact given
+    identical positions;
+  * positions / velocities within 1e-5 after 100 steps (positions by the domain
+    length, periodic-aware; velocities by the field's max speed);
+  * per-cell source field within 1e-5 relative L2 for the same particle state.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from tests.conftest import gpu_available
+from tests.helpers import by_id, gpu_config, oracle_sim, periodic_dist
+
+pytestmark = pytest.mark.gpu
+
+if not gpu_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from paper_2603_26691_b200 import ScaleTrack, StError  # noqa: E402
+
+import oracle  # noqa: E402
+
+
+def _setup(wl, rebin_interval=1, integrator=0, n=None, precision="f32"):
+    n = wl.n_particles if n is None else n
+    lo, hi = synth.domain_box(wl)
+    x, u, d, w = synth.particles_np(n, lo, hi, wl.d_range, wl.d_dist, wl.w, wl.seed_particles)
+    F = synth.make_field(wl)
+    g = ScaleTrack(gpu_config(wl, capacity=n, rebin_interval=rebin_interval, integrator=integrator))
+    o = oracle_sim(wl, precision, rebin_interval, integrator)
+    g.inject(x, u, d, w)
+    o.inject(x, u, d, w)
+    g.set_fluid_field(F)
+    o.set_fluid_field(F)
+    return g, o, (x, u, d, w), F
+
+
+# ------------------------------------------------------------------ integer contract
+@pytest.mark.parametrize("name", ["C1", "C2", "C4"])
+def test_locate_bit_exact(name):
+    """C-6 / C-14: st_locate == oracle locate on identical fp32 positions, including
+    faces, their fp32 neighbours and the upper boundary."""
+    wl = synth.workload(name, n_particles=0)
+    lo, hi = synth.domain_box(wl)
+    x, _, _, _ = synth.particles_np(200_000, lo, hi, (1e-5, 2e-5), seed=5)
+    faces = []
+    for a in range(3):
+        f = (np.float32(wl.origin[a]) + np.arange(wl.dims[a] + 1) * np.float32(wl.cell_size[a])).astype(np.float32)
+        faces.append(np.concatenate([f, np.nextafter(f, np.float32(np.inf)), np.nextafter(f, np.float32(-np.inf))]))
+    m = max(len(f) for f in faces)
+    xf = np.stack([np.resize(f, m) for f in faces]).astype(np.float32)
+    xf = np.clip(xf, np.array(lo, np.float32)[:, None], np.array(hi, np.float32)[:, None])
+    X = np.concatenate([x, xf], axis=1)
+    g = ScaleTrack(gpu_config(wl, capacity=16))
+    o = oracle_sim(wl)
+    cg, kg = g.locate(X)
+    co, ko = o.locate(X)
+    assert np.array_equal(cg, co)
+    assert np.array_equal(kg, ko)
+
+
+def test_inject_order_and_rebin_bit_exact():
+    """Injection keeps order; the first rebin equals the oracle's stable counting sort."""
+    wl = synth.workload("C2", n_particles=300_000)
+    g, o, (x, u, d, w), F = _setup(wl)
+    p = g.get_particles()
+    assert np.array_equal(p["x"], x) and np.array_equal(p["d"], d)
+    assert np.array_equal(p["id"], np.arange(x.shape[1], dtype=np.uint64))
+    g.advance(wl.dt, 1)
+    o.advance(wl.dt, 1)
+    pg = g.get_particles()
+    # C-15 given the GPU's own positions: stable sort of the pre-rebin order (= id order here)
+    gi = by_id(pg)
+    _, chunk = o.locate(gi["x"])
+    perm, _ = oracle.stable_order(chunk, wl.dims[0] // 8 * (wl.dims[1] // 8) * (wl.dims[2] // 8))
+    assert np.array_equal(pg["id"], gi["id"][perm])
+    assert np.all(np.diff(pg["chunk"]) >= 0)
+
+
+def test_rebin_order_given_gpu_positions():
+    """After many steps (K = 2): feed the GPU's pre-rebin order and post-step positions
+    to the oracle's locate + stable sort; the GPU's own order must come out."""
+    wl = synth.workload("C2", n_particles=200_000)
+    g, o, _, F = _setup(wl, rebin_interval=2)
+    for _ in range(5):
+        g.advance(wl.dt, 1)      # calls 1..5: rebins after 2, 4
+    before = g.get_particles()   # order after call 5 (no rebin at 5)
+    g.advance(wl.dt, 1)          # call 6: advance then rebin
+    after = g.get_particles()
+    pos = {int(i): k for k, i in enumerate(after["id"])}
+    idx = np.array([pos[int(i)] for i in before["id"]])
+    X = after["x"][:, idx]        # post-step positions in pre-rebin order
+    _, chunk = o.locate(X)
+    perm, _ = oracle.stable_order(chunk, 512)
+    assert np.array_equal(after["id"], before["id"][perm])
+    c2, k2 = o.locate(after["x"])
+    assert np.array_equal(after["cell"], c2) and np.array_equal(after["chunk"], k2)
+
+
+# ------------------------------------------------------------------ closed form through the GPU
+@pytest.mark.parametrize("drag", [0, 1])
+def test_c1_settling_terminal_velocity(drag):
+    """C1 (BJ configs[0]): 1000 particles, uniform flow, gravity, 1000 steps; GPU fp32
+    matches the closed-form terminal velocity u_f + g tau (Stokes) / the oracle (S-N)."""
+    wl = synth.workload("C1")
+    wl.drag_law = drag
+    g, o, (x, u, d, w), F = _setup(wl)
+    for _ in range(wl.steps):
+        g.advance(wl.dt, 1)
+    p = by_id(g.get_particles())
+    if drag == 0:
+        tau = synth.RHO_P * d.astype(np.float64) ** 2 / (18 * synth.RHO_F * synth.NU_F)
+        uz = -9.81 * tau
+        assert np.max(np.abs(p["u"][2] - uz)) / np.max(np.abs(uz)) < 1e-5
+        assert np.max(np.abs(p["u"][0] - 0.05)) < 1e-6
+    else:
+        for _ in range(wl.steps):
+            o.advance(wl.dt, 1)
+        q = by_id(o.particles())
+        assert np.max(np.abs(p["u"] - q["u"])) / 0.05 < 1e-5
+        assert np.max(periodic_dist(p["x"], q["x"], wl.lengths)) < 1e-5
+
+
+# ------------------------------------------------------------------ free-running float parity
+def test_c2_taylor_green_100_steps():
+    """C2 (BJ configs[1]) at full size: 1e6 particles, TG, one-way, periodic, 100 steps."""
+    wl = synth.workload("C2")
+    g, o, _, F = _setup(wl)
+    for _ in range(wl.steps):
+        g.advance(wl.dt, 1)
+        o.advance(wl.dt, 1)
+    pg, po = g.get_particles(), o.particles()
+    a, b = by_id(pg), by_id(po)
+    pos = np.max(periodic_dist(a["x"], b["x"], wl.lengths) / np.array(wl.lengths)[:, None])
+    vel = np.max(np.abs(a["u"] - b["u"])) / 1.0   # U_max = U0 = 1 m/s
+    assert pos <= 1e-5, pos
+    assert vel <= 1e-5, vel
+
+
+@pytest.mark.parametrize("integrator", [0, 1])
+def test_two_way_fourier_100_steps(integrator):
+    """Two-way, random-Fourier field, reflecting walls (C4 shape, reduced): positions and
+    velocities after 100 steps (new field every step: oracle-generated, same on both)."""
+    wl = synth.workload("C4", n_particles=100_000)
+    wl.dims = (32, 32, 96)
+    wl.cell_size = (3 / 32,) * 3
+    g, o, _, F = _setup(wl, integrator=integrator)
+    U = float(np.max(np.linalg.norm(F.reshape(3, -1), axis=0)))
+    for s in range(100):
+        g.advance(wl.dt, 1)
+        o.advance(wl.dt, 1)
+    a, b = by_id(g.get_particles()), by_id(o.particles())
+    pos = np.max(np.abs(a["x"].astype(np.float64) - b["x"]) / np.array(wl.lengths)[:, None])
+    vel = np.max(np.abs(a["u"].astype(np.float64) - b["u"])) / U
+    assert pos <= 1e-5, pos
+    assert vel <= 1e-5, vel
+
+
+# ------------------------------------------------------------------ sources
+def _inject_state(sim_g, sim_o, p):
+    sim_g.inject(p["x"], p["u"], p["d"], p["w"], p["id"])
+    sim_o.inject(p["x"], p["u"], p["d"], p["w"], p["id"])
+
+
+@pytest.mark.parametrize("name,n,steps", [("C3", 400_000, 3), ("C4", 300_000, 2)])
+def test_sources_same_state(name, n, steps):
+    """Per-cell source field (C-8..C-10, C-13) within 1e-5 relative L2 for the same
+    particle state (drive both with the same field, compare the step)."""
+    wl = synth.workload(name, n_particles=n)
+    if name == "C3":
+        wl.dims, wl.cell_size = (64, 64, 64), (1 / 16,) * 3
+    g, o, _, F = _setup(wl)
+    g.advance(wl.dt, steps)
+    o.advance(wl.dt, steps)
+    Sg, Tg = g.get_sources()
+    So, To = o.get_sources()
+    assert Tg == pytest.approx(To, rel=1e-15)
+    err = np.linalg.norm(Sg.astype(np.float64) - So) / np.linalg.norm(So)
+    assert err <= 1e-5, err
+
+
+def test_sources_after_100_steps_from_gpu_state():
+    """After 100 free GPU steps (two-way, C3 shape reduced), hand the GPU's particle
+    state to the oracle and compare one more step's source field and momentum balance."""
+    wl = synth.workload("C3", n_particles=200_000)
+    wl.dims, wl.cell_size = (64, 64, 64), (1 / 16,) * 3
+    g, _, _, F = _setup(wl)
+    for _ in range(100):
+        g.advance(wl.dt, 1)
+    g.get_sources()
+    state = g.get_particles()
+    o = oracle_sim(wl)
+    o.inject(state["x"], state["u"], state["d"], state["w"], state["id"])
+    o.set_fluid_field(F)
+    g.advance(wl.dt, 1)
+    o.advance(wl.dt, 1)
+    Sg, Tg = g.get_sources()
+    So, To = o.get_sources()
+    err = np.linalg.norm(Sg.astype(np.float64) - So) / np.linalg.norm(So)
+    assert err <= 1e-5, err
+
+
+def test_momentum_conservation_gpu():
+    """P-4 on the GPU path (fp32, g = 0, periodic): sum w m du + sum S V T = 0 to fp32
+    accuracy relative to sum |w m du| (fp32 bound)."""
+    wl = synth.workload("C3", n_particles=100_000)
+    wl.dims, wl.cell_size, wl.gravity = (32, 32, 32), (1 / 8,) * 3, (0.0, 0.0, 0.0)
+    g, _, (x, u0, d, w), F = _setup(wl)
+    g.advance(wl.dt, 1)
+    p = by_id(g.get_particles())
+    S, T = g.get_sources()
+    m = math.pi / 6 * synth.RHO_P * d.astype(np.float64) ** 3
+    dP = np.sum(w * m * (p["u"].astype(np.float64) - u0), axis=1)
+    fluid = S.reshape(3, -1).astype(np.float64).sum(axis=1) * np.prod(wl.cell_size) * T
+    scale = np.sum(np.abs(w * m * (p["u"] - u0)))
+    assert np.max(np.abs(dP + fluid)) / scale < 1e-4
+
+
+# ------------------------------------------------------------------ edge cases
+def test_empty_store_and_errors():
+    wl = synth.workload("C1", n_particles=0)
+    g = ScaleTrack(gpu_config(wl, capacity=10))
+    with pytest.raises(StError):
+        g.advance(1e-3, 1)                      # no field yet (ST_ERR_STATE)
+    g.set_fluid_field(synth.make_field(wl))
+    g.advance(1e-3, 1)                          # empty store
+    S, T = g.get_sources()
+    assert T == pytest.approx(1e-3) and not np.any(S)
+    with pytest.raises(StError) as e:           # outside the domain
+        g.inject(np.full((3, 1), 2.0, np.float32), np.zeros((3, 1), np.float32), np.full(1, 1e-5, np.float32))
+    assert "OUT_OF_DOMAIN" in str(e.value)
+    assert g.count() == 0
+    with pytest.raises(StError) as e:           # capacity
+        z = np.zeros((3, 11), np.float32) + 0.5
+        g.inject(z, np.zeros((3, 11), np.float32), np.full(11, 1e-5, np.float32))
+    assert "CAPACITY" in str(e.value)
+
+
+def test_cfl_error_is_loud():
+    """S:174 never silent: a displacement one wrap cannot undo -> ST_ERR_CFL."""
+    wl = synth.workload("C1", n_particles=1)
+    g = ScaleTrack(gpu_config(wl, capacity=4))
+    g.inject(np.full((3, 1), 0.5, np.float32), np.array([[500.0], [0], [0]], np.float32),
+             np.full(1, 1e-3, np.float32))
+    g.set_fluid_field(synth.uniform_field(wl.dims, (500.0, 0, 0)))
+    g.advance(0.01, 1)
+    with pytest.raises(StError) as e:
+        g.sync()
+    assert "CFL" in str(e.value)
+
+
+def test_ragged_chunks_and_multi_substeps():
+    """Dims not divisible by the chunk edge (ragged last chunk) and nsteps > 1 per call."""
+    wl = synth.workload("C4", n_particles=50_000)
+    wl.dims, wl.cell_size = (20, 13, 37), (3 / 20, 3 / 13, 9 / 37)
+    g, o, _, F = _setup(wl)
+    for _ in range(10):
+        g.advance(wl.dt / 4, 4)
+        o.advance(wl.dt / 4, 4)
+    a, b = by_id(g.get_particles()), by_id(o.particles())
+    U = float(np.max(np.abs(F)))
+    assert np.max(np.abs(a["x"].astype(np.float64) - b["x"]) / np.array(wl.lengths)[:, None]) <= 1e-5
+    assert np.max(np.abs(a["u"].astype(np.float64) - b["u"])) / U <= 1e-5
+    pg = g.get_particles()
+    c, k = o.locate(pg["x"])
+    assert np.array_equal(pg["cell"], c) and np.array_equal(pg["chunk"], k)
+    assert np.all(np.diff(pg["chunk"]) >= 0)
+
+
+def test_async_split_readout_and_device_buffers():
+    """Asynchronous coupling buffer: request/wait readout while the next advance is
+    enqueued; device (torch) field and source buffers; intervals add up."""
+    import torch
+    wl = synth.workload("C3", n_particles=100_000)
+    wl.dims, wl.cell_size = (32, 32, 32), (1 / 8,) * 3
+    g, o, _, F = _setup(wl)
+    Fd = torch.from_numpy(F).cuda()
+    Sd = torch.empty((3, 32, 32, 32), dtype=torch.float32, device="cuda")
+    g.advance(wl.dt, 1)
+    o.advance(wl.dt, 1)
+    g.request_sources()
+    g.set_fluid_field(Fd)
+    g.advance(wl.dt, 1)                 # deposits into the other buffer while the readout runs
+    S1, T1 = g.wait_sources(Sd)
+    So, To = o.get_sources()
+    assert T1 == pytest.approx(wl.dt)
+    err = np.linalg.norm(Sd.cpu().numpy().astype(np.float64) - So) / np.linalg.norm(So)
+    assert err <= 1e-5
+    S2, T2 = g.get_sources()
+    assert T2 == pytest.approx(wl.dt) and np.any(S2)
