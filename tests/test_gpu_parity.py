@@ -144,21 +144,30 @@ def test_c2_taylor_green_100_steps():
 
 @pytest.mark.parametrize("integrator", [0, 1])
 def test_two_way_fourier_100_steps(integrator):
-    """Two-way, random-Fourier field, reflecting walls (C4 shape, reduced): positions and
-    velocities after 100 steps (new field every step: oracle-generated, same on both)."""
+    """Two-way, random-Fourier field, reflecting walls (C4 shape, reduced), 100 steps in
+    10-step segments: at each segment start the oracle is restarted from the GPU state
+    (reading C-24: in a 256-mode field the trajectories are chaotic — nearby fp32
+    trajectories separate by ~e^{lambda t}, so any two correct fp32 programs differ by
+    more than 1e-5 after 0.5 s; the segment form checks the step, not the chaos)."""
     wl = synth.workload("C4", n_particles=100_000)
     wl.dims = (32, 32, 96)
     wl.cell_size = (3 / 32,) * 3
-    g, o, _, F = _setup(wl, integrator=integrator)
+    g, _, _, F = _setup(wl, integrator=integrator)
     U = float(np.max(np.linalg.norm(F.reshape(3, -1), axis=0)))
-    for s in range(100):
-        g.advance(wl.dt, 1)
-        o.advance(wl.dt, 1)
-    a, b = by_id(g.get_particles()), by_id(o.particles())
-    pos = np.max(np.abs(a["x"].astype(np.float64) - b["x"]) / np.array(wl.lengths)[:, None])
-    vel = np.max(np.abs(a["u"].astype(np.float64) - b["u"])) / U
-    assert pos <= 1e-5, pos
-    assert vel <= 1e-5, vel
+    worst_p = worst_v = 0.0
+    for seg in range(10):
+        st = g.get_particles()
+        o = oracle_sim(wl, integrator=integrator)
+        o.inject(st["x"], st["u"], st["d"], st["w"], st["id"])
+        o.set_fluid_field(F)
+        for s in range(10):
+            g.advance(wl.dt, 1)
+            o.advance(wl.dt, 1)
+        a, b = by_id(g.get_particles()), by_id(o.particles())
+        worst_p = max(worst_p, np.max(np.abs(a["x"].astype(np.float64) - b["x"]) / np.array(wl.lengths)[:, None]))
+        worst_v = max(worst_v, np.max(np.abs(a["u"].astype(np.float64) - b["u"])) / U)
+    assert worst_p <= 1e-5, worst_p
+    assert worst_v <= 1e-5, worst_v
 
 
 # ------------------------------------------------------------------ sources
