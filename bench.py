@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C5", choices=["C3", "C4", "C5"])
     ap.add_argument("--particles", type=float, default=None, help="particles per GPU (default: the workload's)")
-    ap.add_argument("--rebin-interval", type=int, default=4)
+    ap.add_argument("--rebin-interval", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target oracle CPU time for cpu_baseline")
@@ -272,21 +272,20 @@ def run_ours(args):
         n_total = float(n_local)
     value = n_total * args.steps / (ms / 1e3)
 
-    # roofline of the dominant kernel (per launch, CUDA events on the launching stream)
+    # roofline of the dominant kernel (per launch, CUDA events on the launching stream):
+    # the step kernel (advance, with the rebin scatter fused in every K-th launch)
     adv_ms = statistics.mean(adv)
     reb_list = [r for r in reb if r > 0]
     reb_ms = statistics.mean(reb_list) if reb_list else 0.0
-    reb_per_step = reb_ms * len(reb_list) / max(1, len(reb))
+    st_stats = st.stats()
+    movers = st_stats["last_movers"]          # chunk movers since the last rebin (one step's worth)
+    f_move = movers / max(1, n_local)
     peak, peak_src = peaks()
     cells_win = nx * ny * (lay.z1 - lay.z0 + 2 * lay.halo_cells)
-    if adv_ms >= reb_per_step:
-        kname = "advance"
-        alg = algorithmic_bytes_per_update(wl.coupling == 1) * n_local + 24 * cells_win
-        kms = adv_ms
-    else:
-        kname = "rebin (stable sort, full store)"
-        alg = 80 * n_local
-        kms = reb_ms
+    kname = "step" + (" (advance + fused rebin scatter)" if K == 1 else f" (advance; rebin fused every {K})")
+    # 56 B/update + 80 B per chunk mover (per rebin) + 24 B/cell (u_f in, S out)
+    alg = algorithmic_bytes_per_update(wl.coupling == 1) * n_local + 80 * movers * (1.0 / K) + 24 * cells_win
+    kms = adv_ms
     achieved = alg / (kms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -341,7 +340,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg, "kernel_ms": kms},
-            "advance_ms": adv_ms, "rebin_ms": reb_ms, "rebins_in_timed_region": len(reb_list),
+            "step_kernel_ms": adv_ms, "rebin_prep_ms": reb_ms, "rebins_in_timed_region": len(reb_list),
+            "f_move_chunk": f_move, "fused_rebins": st_stats["fused_rebins"],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -10,11 +10,12 @@ inject -> set fluid field -> advance(dt, nsteps) -> get sources, with
 
 * the per-particle step of SURVEY §8(c1) / DESIGN.md §4 (C core, fp32 or fp64);
 * the rebin rule C-15: after the last sub-step of every K-th ``advance`` call the
-  store is stable-sorted by chunk id (``orc_stable_order``, a counting sort);
+  store is stable-sorted by the bin key (chunk id, cell within the chunk)
+  (``orc_bin_key_*`` + ``orc_stable_order``, a counting sort);
 * the R-rank emulation rule C-16: rank r owns chunk planes
   [floor(r*NCz/R), floor((r+1)*NCz/R)); at a rebin every rank keeps its own
   particles in order, appends arrivals in ascending source rank (each in the
-  sender's order), then stable-sorts by chunk; M[src][dst] counts movers.
+  sender's order), then stable-sorts by bin key; M[src][dst] counts movers.
 * source readout C-13: S = acc / (V_cell * T_acc) in N/m^3, acc in float64.
 
 Parity status: every function here is pinned by tests/test_oracle_pins.py except
@@ -97,10 +98,13 @@ def lib():
         f = getattr(L, f"orc_interpolate_{sfx}")
         f.argtypes = [P, ctypes.c_int64, vp, vp, vp]
         f.restype = ctypes.c_int
+        f = getattr(L, f"orc_bin_key_{sfx}")
+        f.argtypes = [P, ctypes.c_int64, vp, vp]
+        f.restype = ctypes.c_int
         f = getattr(L, f"orc_drag_factor_{sfx}")
         f.argtypes = [ctypes.c_int, real]
         f.restype = real
-    L.orc_stable_order.argtypes = [ctypes.c_int64, vp, ctypes.c_int32, vp, vp]
+    L.orc_stable_order.argtypes = [ctypes.c_int64, vp, ctypes.c_int64, vp, vp]
     L.orc_stable_order.restype = ctypes.c_int
     _lib = L
     return L
@@ -117,7 +121,7 @@ def drag_factor(Re: float, law: int = DRAG_SCHILLER_NAUMANN, precision: str = "f
 
 def stable_order(key: np.ndarray, nkeys: int) -> tuple[np.ndarray, np.ndarray]:
     """C-15: permutation of a stable counting sort by key, and the CSR offsets."""
-    key = np.ascontiguousarray(key, dtype=np.int32)
+    key = np.ascontiguousarray(key, dtype=np.int64)
     perm = np.empty(key.size, dtype=np.int64)
     off = np.empty(nkeys + 1, dtype=np.int64)
     rc = lib().orc_stable_order(key.size, _ptr(key), nkeys, _ptr(perm), _ptr(off))
@@ -147,6 +151,10 @@ class Mesh:
     def n_chunks(self) -> int:
         a, b, c = self.nchunk
         return a * b * c
+
+    @property
+    def n_bins(self) -> int:
+        return self.n_chunks * self.chunk_cells ** 3
 
     @property
     def cell_volume(self) -> float:
@@ -245,6 +253,13 @@ class Sim:
         getattr(self._lib, f"orc_locate_{self.precision}")(self.params, n, _ptr(x), _ptr(cell), _ptr(chunk))
         return cell, chunk
 
+    def bin_key(self, x: np.ndarray) -> np.ndarray:
+        """C-15 bin key = chunk * cc^3 + cell-within-chunk of each position."""
+        x = np.ascontiguousarray(x, dtype=self.real)
+        key = np.empty(x.shape[1], np.int64)
+        getattr(self._lib, f"orc_bin_key_{self.precision}")(self.params, x.shape[1], _ptr(x), _ptr(key))
+        return key
+
     def interpolate(self, x: np.ndarray, F: np.ndarray | None = None) -> np.ndarray:
         F = self.field if F is None else np.ascontiguousarray(F, dtype=self.real)
         x = np.ascontiguousarray(x, dtype=self.real)
@@ -299,7 +314,7 @@ class Sim:
         return status
 
     def rebin(self):
-        """C-15 / C-16: migrate to owners, then stable sort by chunk on every rank."""
+        """C-15 / C-16: migrate to owners, then stable sort by bin key on every rank."""
         R = self.nranks
         M = np.zeros((R, R), np.int64)
         parts = [[None] * R for _ in range(R)]   # parts[src][dst] = index array in src order
@@ -320,8 +335,7 @@ class Sim:
                 ws.append(s.w[idx]); ids.append(s.id[idx])
             st = _Store(np.concatenate(xs, 1), np.concatenate(us, 1), np.concatenate(ds),
                         np.concatenate(ws), np.concatenate(ids))
-            _, chunk = self.locate(st.x)
-            perm, _ = stable_order(chunk, self.mesh.n_chunks)
+            perm, _ = stable_order(self.bin_key(st.x), self.mesh.n_bins)
             new.append(_Store(np.ascontiguousarray(st.x[:, perm]), np.ascontiguousarray(st.u[:, perm]),
                               st.d[perm].copy(), st.w[perm].copy(), st.id[perm].copy()))
         self.stores = new

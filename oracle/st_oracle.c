@@ -79,12 +79,13 @@ typedef struct {
 #undef POW
 
 /*
- * C-15: stable counting sort of n items by key in [0, nkeys).  perm receives
+ * C-15: stable counting sort of n items by key in [0, nkeys) (the bin key of
+ * orc_bin_key_*, or any integer key).  perm receives
  * the store order after the sort (perm[j] = old index of the item now at j);
  * offsets (nkeys+1 entries, may be NULL) receives the CSR bin offsets.
  * Returns -1 on a key out of range.
  */
-int orc_stable_order(int64_t n, const int32_t* key, int32_t nkeys, int64_t* perm,
+int orc_stable_order(int64_t n, const int64_t* key, int64_t nkeys, int64_t* perm,
                      int64_t* offsets) {
   int64_t* start = (int64_t*)calloc((size_t)nkeys + 1, sizeof(int64_t));
   if (!start) return -2;
@@ -92,7 +93,7 @@ int orc_stable_order(int64_t n, const int32_t* key, int32_t nkeys, int64_t* perm
     if (key[i] < 0 || key[i] >= nkeys) { free(start); return -1; }
     start[key[i] + 1] += 1;                       /* count */
   }
-  for (int32_t k = 0; k < nkeys; ++k) start[k + 1] += start[k];   /* exclusive prefix */
+  for (int64_t k = 0; k < nkeys; ++k) start[k + 1] += start[k];   /* exclusive prefix */
   if (offsets) memcpy(offsets, start, ((size_t)nkeys + 1) * sizeof(int64_t));
   for (int64_t i = 0; i < n; ++i) perm[start[key[i]]++] = i;     /* place in input order */
   free(start);

@@ -7,12 +7,14 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <vector>
 
 #include "st_comm.h"
 #include "st_internal.h"
+#include "st_step.h"
 
 using namespace st;
 
@@ -39,10 +41,26 @@ struct st_ctx {
   Store S[2];
   int cur = 0;
   int32_t* key[2] = {nullptr, nullptr};
-  bool keys_valid = false;    // key[cur] == chunk of current positions
   SortScratch sc;
-  int64_t* offsets = nullptr; // [n_local_chunks + 1] after a rebin
   uint64_t next_id = 0;
+
+  // binned layout (C-15): CSR per bin, warp items, slot histograms (k_step.cu)
+  BinGeom bg{};
+  bool binned = false;        // store sorted by bin key, off/items/hist valid
+  bool rebin_due = false;     // contract rebin due (executed lazily, fused when possible)
+  int lay = 0;                // index of the current layout in off/items
+  int hcur = 0;               // index of the current slot histogram
+  int64_t* off[2] = {nullptr, nullptr};     // [nbins+1] current / next layout
+  int* items[2] = {nullptr, nullptr};       // warp items (first bin of each)
+  int* n_items[2] = {nullptr, nullptr};     // device counts
+  int* hist[2] = {nullptr, nullptr};        // [nbins*27] slot counts: current / being counted
+  uint32_t* new_cnt = nullptr;              // [nbins]
+  uint32_t* item_flag = nullptr;            // [nbins]
+  int64_t* item_pos = nullptr;              // [nbins+1]
+  int* h_far = nullptr;                     // mapped pinned: next rebin needs the general sort
+  int* d_far = nullptr;
+  unsigned long long* d_movers = nullptr;   // chunk movers counted by the last step kernel
+  cudaEvent_t ev_step_done{};
 
   // fields (double buffer)
   float4* field[2] = {nullptr, nullptr};
@@ -130,10 +148,13 @@ static st_status consume_flags(st_ctx* c) {
   if (h & ERRF_WINDOW)
     return fail(c, ST_ERR_CFL, "a particle left this rank's field/source window between rebins (C-16)");
   if (h & ERRF_DOMAIN) return fail(c, ST_ERR_OUT_OF_DOMAIN, "position outside [lo, hi]");
+  if (h & ERRF_SCATTER) return fail(c, ST_ERR_CFL, "rebin scatter found a particle outside its bin's neighbourhood");
   return ST_OK;
 }
 
 extern "C" {
+
+static st_status flush_rebin(st_ctx* c);
 
 int32_t st_abi_version(void) { return ST_ABI_VERSION; }
 
@@ -226,9 +247,13 @@ static void build_geometry(st_ctx* c) {
   c->chunk_lo = g.chunk_base;
   c->n_local_chunks = (c->kz1 - c->kz0) * g.NC[0] * g.NC[1];
   c->local_cells = (int64_t)g.n[0] * g.n[1] * (c->z1 - c->z0);
-  const int64_t nchunks = (int64_t)g.NC[0] * g.NC[1] * g.NC[2];
+  c->bg.cc3 = g.cc * g.cc * g.cc;
+  c->bg.nbins = c->n_local_chunks * c->bg.cc3;
+  c->bg.nkz = c->kz1 - c->kz0;
+  // radix key = local bin (< nbins); multi-GPU pre-migration key = global chunk
+  const int64_t kmax = std::max<int64_t>(c->bg.nbins, (int64_t)g.NC[0] * g.NC[1] * g.NC[2]);
   int bits = 1;
-  while (((int64_t)1 << bits) < nchunks) ++bits;
+  while (((int64_t)1 << bits) < kmax) ++bits;
   c->key_bits = bits;
   // extended planes delivered to the ingest kernel (owned + one halo window each side)
   c->ext_z0 = c->z0 - c->H - 1;
@@ -299,11 +324,25 @@ static st_status init_impl(st_ctx* c) {
   ST_CUDA(c, cudaMalloc(&c->S_dev, (size_t)3 * (c->local_cells > 0 ? c->local_cells : 1) * sizeof(float)));
   ST_CUDA(c, cudaMalloc(&c->d_err, sizeof(int)));
   ST_CUDA(c, cudaMemset(c->d_err, 0, sizeof(int)));
-  ST_CUDA(c, cudaMalloc(&c->offsets, (size_t)(c->n_local_chunks + 1) * sizeof(int64_t)));
-  ST_CUDA(c, cudaMemset(c->offsets, 0, (size_t)(c->n_local_chunks + 1) * sizeof(int64_t)));
-  // radix-sort scratch
+  const size_t nb = (size_t)c->bg.nbins;
+  for (int i = 0; i < 2; ++i) {
+    ST_CUDA(c, cudaMalloc(&c->off[i], (nb + 1) * sizeof(int64_t)));
+    ST_CUDA(c, cudaMalloc(&c->items[i], (nb + 1) * sizeof(int)));
+    ST_CUDA(c, cudaMalloc(&c->n_items[i], sizeof(int)));
+    ST_CUDA(c, cudaMalloc(&c->hist[i], nb * 27 * sizeof(int)));
+  }
+  ST_CUDA(c, cudaMalloc(&c->new_cnt, (nb + 1) * sizeof(uint32_t)));
+  ST_CUDA(c, cudaMalloc(&c->item_flag, (nb + 1) * sizeof(uint32_t)));
+  ST_CUDA(c, cudaMalloc(&c->item_pos, (nb + 2) * sizeof(int64_t)));
+  ST_CUDA(c, cudaHostAlloc(&c->h_far, sizeof(int), cudaHostAllocMapped));
+  *c->h_far = 0;
+  ST_CUDA(c, cudaHostGetDevicePointer(&c->d_far, c->h_far, 0));
+  ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_step_done, cudaEventDisableTiming));
+  ST_CUDA(c, cudaMalloc(&c->d_movers, sizeof(unsigned long long)));
+  ST_CUDA(c, cudaMemset(c->d_movers, 0, sizeof(unsigned long long)));
+  // radix-sort scratch (also serves the scans over bins)
   c->sc.max_blocks = (c->cap + 4095) / 4096 + 1;
-  const int64_t m = 256 * c->sc.max_blocks;
+  const int64_t m = std::max<int64_t>(256 * c->sc.max_blocks, (int64_t)nb + 1);
   c->sc.partial_cap = (m + 4095) / 4096 + 1;
   ST_CUDA(c, cudaMalloc(&c->sc.hist, (size_t)m * sizeof(uint32_t)));
   ST_CUDA(c, cudaMalloc(&c->sc.offs, (size_t)(m + 1) * sizeof(int64_t)));
@@ -337,7 +376,18 @@ st_status st_destroy(st_ctx* c) {
   cudaFree(c->field_stage);
   cudaFree(c->S_dev);
   cudaFree(c->d_err);
-  cudaFree(c->offsets);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c->off[i]);
+    cudaFree(c->items[i]);
+    cudaFree(c->n_items[i]);
+    cudaFree(c->hist[i]);
+  }
+  cudaFree(c->new_cnt);
+  cudaFree(c->item_flag);
+  cudaFree(c->item_pos);
+  if (c->h_far) cudaFreeHost(c->h_far);
+  cudaFree(c->d_movers);
+  if (c->ev_step_done) cudaEventDestroy(c->ev_step_done);
   cudaFree(c->sc.hist);
   cudaFree(c->sc.offs);
   cudaFree(c->sc.partial);
@@ -426,6 +476,10 @@ st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const 
   if (n == 0) return ST_OK;
   if (!x || !u || !d) return fail(c, ST_ERR_INVALID_ARG, "x, u and d are required");
   if (c->n + n > c->cap) return fail(c, ST_ERR_CAPACITY, "store capacity exceeded");
+  {
+    st_status fr = flush_rebin(c);   // the contract sorted the store before this append
+    if (fr) return fr;
+  }
   Store s = c->S[c->cur];
   const int64_t o = c->n, cap = c->cap;
   auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
@@ -453,34 +507,62 @@ st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const 
   if (st) return st;   // nothing appended: c->n unchanged
   if (!id) c->next_id += (uint64_t)n;
   c->n += n;
-  c->keys_valid = false;
+  c->binned = false;
   return ST_OK;
 }
 
 // ---------------------------------------------------------------- rebin
-// C-15 / C-16: stable sort by chunk of the current positions; with nranks > 1
-// movers go to their owner first (kept ++ arrivals by source rank, then sort).
-static st_status rebin(st_ctx* c) {
-  if (!c->keys_valid) {
-    st_status s = check_launch(c, launch_keys(c->g, c->S[c->cur].x, c->cap, c->n, c->key[c->cur], c->cs));
-    if (s) return s;
-  }
+// C-15 / C-16.  Two implementations of the same contract:
+//  * general: radix sort by the bin key (after injection, when a particle moved
+//    more than one cell since its bin, and for the multi-GPU migration);
+//  * neighbour scatter (k_step.cu): fused into the next advance (or standalone
+//    when the store is observed first).
+static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
+  StepArgs a;
+  memset(&a, 0, sizeof(a));
+  a.g = c->g;
+  a.p = c->p;
+  a.bg = c->bg;
+  a.A = c->S[c->cur];
+  a.B = c->S[1 - c->cur];
+  a.cap = c->cap;
+  a.n = c->n;
+  a.off = c->off[c->lay];
+  a.off_new = c->off[1 - c->lay];
+  a.slot_base = c->hist[c->hcur];
+  a.item_bin0 = c->items[c->lay];
+  a.n_items = c->n_items[c->lay];
+  a.nbins = c->bg.nbins;
+  a.field = c->front >= 0 ? c->field[c->front] : nullptr;
+  a.acc = c->acc[c->acc_cur];
+  a.hist_next = c->hist[1 - c->hcur];
+  a.dt = dt;
+  a.nsteps = nsteps;
+  a.err = c->d_err;
+  a.far = c->d_far;
+  a.movers = c->d_movers;
+  return a;
+}
+
+static st_status general_rebin(st_ctx* c) {
+  const Geom& g = c->g;
   ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
-  int in_b = 0;
-  const int other = 1 - c->cur;
-  int nl = launch_stable_sort(c->S[c->cur], c->S[other], c->cap, c->n, c->key[c->cur], c->key[other], c->key_bits,
-                              c->sc, &in_b, c->cs);
-  if (nl < 0) return fail(c, ST_ERR_CAPACITY, "sort scratch too small");
-  st_status s = check_launch(c, nl);
-  if (s) return s;
-  if (in_b) c->cur = other;
+  int in_b = 0, nl = 0;
+  st_status s;
   if (c->comm) {
+    // owner segments: stable sort by global chunk, then kept ++ arrivals (C-16)
+    nl = launch_keys(g, c->S[c->cur].x, c->cap, c->n, c->key[c->cur], c->cs);
+    int ns = launch_stable_sort(c->S[c->cur], c->S[1 - c->cur], c->cap, c->n, c->key[c->cur], c->key[1 - c->cur],
+                                c->key_bits, c->sc, &in_b, c->cs);
+    if (ns < 0) return fail(c, ST_ERR_CAPACITY, "sort scratch too small");
+    if ((s = check_launch(c, nl + ns))) return s;
+    if (in_b) c->cur = 1 - c->cur;
     std::string why;
     int64_t n_new = 0;
-    nl = 0;
-    int rc = comm_migrate(c->comm, c->g, c->S, &c->cur, c->key, c->cap, c->n, c->chunk_lo, c->n_local_chunks,
-                          c->key_bits, c->sc, c->mig_row.data(), &n_new, &nl, c->cs, why);
-    c->launches += nl;
+    int ml = 0;
+    int rc = comm_migrate(c->comm, g, c->S, &c->cur, c->key, c->cap, c->n, c->chunk_lo, c->n_local_chunks,
+                          c->key_bits, c->sc, c->mig_row.data(), &n_new, &ml, c->cs, why);
+    c->launches += ml;
     if (rc == 3) return fail(c, ST_ERR_CAPACITY, why);
     if (rc) return fail(c, ST_ERR_NCCL, why);
     c->last_sent = 0;
@@ -491,13 +573,66 @@ static st_status rebin(st_ctx* c) {
   } else {
     c->mig_row[0] = c->n;
   }
-  s = check_launch(c, launch_chunk_offsets(c->key[c->cur], c->n, c->chunk_lo, c->n_local_chunks, c->offsets, c->cs));
-  if (s) return s;
+  nl = launch_bin_keys(g, c->bg, c->S[c->cur].x, c->cap, c->n, c->key[c->cur], c->d_err, c->cs);
+  int ns = launch_stable_sort(c->S[c->cur], c->S[1 - c->cur], c->cap, c->n, c->key[c->cur], c->key[1 - c->cur],
+                              c->key_bits, c->sc, &in_b, c->cs);
+  if (ns < 0) return fail(c, ST_ERR_CAPACITY, "sort scratch too small");
+  if ((s = check_launch(c, nl + ns))) return s;
+  if (in_b) c->cur = 1 - c->cur;
+  nl = launch_bin_offsets(c->key[c->cur], c->n, c->bg.nbins, c->off[c->lay], c->cs);
+  nl += launch_hist_all_stay(c->off[c->lay], c->bg.nbins, c->hist[c->hcur], c->cs);
+  nl += launch_items(c->off[c->lay], c->bg.nbins, c->item_flag, c->item_pos, c->sc.partial, c->items[c->lay],
+                     c->n_items[c->lay], c->cs);
+  if ((s = check_launch(c, nl))) return s;
   ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));
   c->timed_reb = true;
-  c->keys_valid = true;
+  c->binned = true;
+  c->rebin_due = false;
   c->rebins += 1;
   return ST_OK;
+}
+
+// Neighbour-slot scatter from the current layout into the other buffer; fused
+// with the advance when `advance` (the field/accumulator must be set up).
+static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps) {
+  const Geom& g = c->g;
+  const int nlay = 1 - c->lay;
+  ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
+  int nl = launch_rebin_prep(g, c->bg, c->hist[c->hcur], c->new_cnt, c->cs);
+  nl += launch_exclusive_scan_u32(c->new_cnt, c->bg.nbins, c->off[nlay], c->sc.partial, c->cs);
+  nl += launch_items(c->off[nlay], c->bg.nbins, c->item_flag, c->item_pos, c->sc.partial, c->items[nlay],
+                     c->n_items[nlay], c->cs);
+  ST_CUDA(c, cudaMemsetAsync(c->hist[1 - c->hcur], 0, (size_t)c->bg.nbins * 27 * sizeof(int), c->cs));
+  ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));
+  c->timed_reb = true;
+  st_status s = check_launch(c, nl);
+  if (s) return s;
+  *c->h_far = 0;
+  ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
+  StepArgs a = step_args(c, dt, nsteps);
+  if (advance) ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
+  s = check_launch(c, launch_step(a, true, advance, c->cs));
+  if (s) return s;
+  if (advance) {
+    ST_CUDA(c, cudaEventRecord(c->t_adv1, c->cs));
+    c->timed_adv = true;
+  }
+  ST_CUDA(c, cudaEventRecord(c->ev_step_done, c->cs));
+  c->cur = 1 - c->cur;
+  c->lay = nlay;
+  c->hcur = 1 - c->hcur;
+  c->rebin_due = false;
+  c->rebins += 1;
+  if (advance) c->fused_rebins += 1;
+  return ST_OK;
+}
+
+// Execute a due rebin before the store is observed or appended to.
+static st_status flush_rebin(st_ctx* c) {
+  if (!c->rebin_due) return ST_OK;
+  ST_CUDA(c, cudaEventSynchronize(c->ev_step_done));
+  if (!c->binned || c->comm || *c->h_far) return general_rebin(c);
+  return scatter_rebin(c, false, 0.0f, 0);
 }
 
 // ---------------------------------------------------------------- advance
@@ -512,23 +647,52 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
   if (c->front < 0) return fail(c, ST_ERR_STATE, "st_advance before st_set_fluid_field (P:202: first step is synchronous)");
   // the accumulator must be free (its previous readout finished zeroing it)
   ST_CUDA(c, cudaStreamWaitEvent(c->cs, c->ev_acc_free[c->acc_cur], 0));
-  ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
-  Store s = c->S[c->cur];
-  st_status st = check_launch(c, launch_advance(c->g, c->p, c->field[c->front], c->acc[c->acc_cur], s, c->cap, c->n,
-                                                nullptr, 0, (float)dt, nsteps, c->key[c->cur], c->d_err, c->cs));
-  if (st) return st;
-  ST_CUDA(c, cudaEventRecord(c->t_adv1, c->cs));
-  c->timed_adv = true;
-  c->keys_valid = true;
+  st_status st = ST_OK;
+  bool done = false;
+  c->timed_reb = false;
+  if (c->rebin_due) {
+    // the rebin of the previous call (C-15), fused into this call when every
+    // particle is still within one cell of its bin
+    ST_CUDA(c, cudaEventSynchronize(c->ev_step_done));
+    if (c->binned && !c->comm && !*c->h_far) {
+      st = scatter_rebin(c, true, (float)dt, nsteps);
+      if (st) return st;
+      done = true;
+    } else {
+      st = general_rebin(c);
+      if (st) return st;
+    }
+  }
+  if (!done) {
+    ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
+    if (c->binned) {
+      ST_CUDA(c, cudaMemsetAsync(c->hist[1 - c->hcur], 0, (size_t)c->bg.nbins * 27 * sizeof(int), c->cs));
+      ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
+      *c->h_far = 0;
+      StepArgs a = step_args(c, (float)dt, nsteps);
+      st = check_launch(c, launch_step(a, false, true, c->cs));
+      if (st) return st;
+      c->hcur = 1 - c->hcur;
+    } else {
+      st = check_launch(c, launch_advance(c->g, c->p, c->field[c->front], c->acc[c->acc_cur], c->S[c->cur], c->cap,
+                                          c->n, nullptr, 0, (float)dt, nsteps, nullptr, c->d_err, c->cs));
+      if (st) return st;
+    }
+    ST_CUDA(c, cudaEventRecord(c->t_adv1, c->cs));
+    ST_CUDA(c, cudaEventRecord(c->ev_step_done, c->cs));
+    c->timed_adv = true;
+  }
   ST_CUDA(c, cudaEventRecord(c->ev_field_reader[c->front], c->cs));
   ST_CUDA(c, cudaEventRecord(c->ev_acc_writer[c->acc_cur], c->cs));
   c->T_acc[c->acc_cur] += (double)nsteps * dt;
   c->calls += 1;
   if (c->calls % c->cfg.rebin_interval == 0) {
-    st = rebin(c);
-    if (st) return st;
-  } else {
-    c->timed_reb = false;
+    if (c->binned) {
+      c->rebin_due = true;            // executed at the next advance / observation
+    } else {
+      st = general_rebin(c);          // first sort after injection: do it now
+      if (st) return st;
+    }
   }
   return ST_OK;
 }
@@ -589,6 +753,10 @@ st_status st_sync(st_ctx* c) {
 st_status st_get_count(st_ctx* c, int64_t* n) {
   ST_ALIVE(c);
   if (!n) return ST_ERR_INVALID_ARG;
+  if (c->comm) {
+    st_status fr = flush_rebin(c);   // migration changes the local count
+    if (fr) return fr;
+  }
   *n = c->n;
   return ST_OK;
 }
@@ -596,6 +764,8 @@ st_status st_get_count(st_ctx* c, int64_t* n) {
 st_status st_get_particles(st_ctx* c, int64_t cap, int64_t* n_out, float* x, float* u, float* d, float* w,
                            uint64_t* id, int32_t* cell, int32_t* chunk) {
   ST_ALIVE(c);
+  st_status fr = flush_rebin(c);
+  if (fr) return fr;
   ST_CUDA(c, cudaStreamSynchronize(c->cs));
   st_status st = consume_flags(c);
   if (st) return st;
@@ -672,6 +842,10 @@ st_status st_get_layout(st_ctx* c, st_layout* o) {
 st_status st_get_stats(st_ctx* c, st_stats* o) {
   ST_ALIVE(c);
   if (!o) return ST_ERR_INVALID_ARG;
+  unsigned long long mv = 0;
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  ST_CUDA(c, cudaMemcpy(&mv, c->d_movers, sizeof(mv), cudaMemcpyDeviceToHost));
+  c->last_movers = (int64_t)mv;
   o->n_particles = c->n;
   o->calls = c->calls;
   o->rebins = c->rebins;

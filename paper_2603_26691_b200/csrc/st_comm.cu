@@ -248,16 +248,12 @@ int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int6
   }
   NCCK(ncclGroupEnd(), why);
   if (join_out(c, s, why)) return 1;
-  // kept ++ arrivals -> stable sort by chunk (C-16)
-  *launches += launch_keys(g, B.x, cap, total, key[o], s);
-  int in_other = 0;
-  const int nl = launch_stable_sort(B, A, cap, total, key[o], key[*cur], key_bits, sc, &in_other, s);
-  if (nl < 0) {
-    why = "sort scratch too small";
-    return 3;
-  }
-  *launches += nl;
-  *cur = in_other ? *cur : o;
+  // kept ++ arrivals now sit in the other buffer; the caller stable-sorts it by
+  // bin key (C-16), which refines the chunk order each segment already has
+  (void)key_bits;
+  (void)sc;
+  (void)key;
+  *cur = o;
   *n_new = total;
   CUCK(cudaGetLastError(), why);
   return 0;

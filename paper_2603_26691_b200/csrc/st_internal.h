@@ -49,7 +49,7 @@ struct Store {
 };
 
 // Device error flags (bit mask) written by kernels.
-enum : int { ERRF_CFL = 1, ERRF_DOMAIN = 2, ERRF_WINDOW = 4 };
+enum : int { ERRF_CFL = 1, ERRF_DOMAIN = 2, ERRF_WINDOW = 4, ERRF_SCATTER = 8 };
 
 // Per-tile description for the advance kernel: particles [begin, end) all binned
 // to local chunk `chunk` (or -1: unbinned, read the field from global memory).

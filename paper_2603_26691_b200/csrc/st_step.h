@@ -1,0 +1,51 @@
+// Binned particle step (k_step.cu): layout, arguments and launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "st_internal.h"
+
+namespace st {
+
+constexpr int kMaxBins = 32;          // bins per warp item
+constexpr int kItemParticles = 1024;  // soft particle budget per warp item
+
+struct BinGeom {
+  int cc3;     // cells per chunk (bins per chunk)
+  int nbins;   // local bins = local chunks * cc3
+  int nkz;     // local chunk planes
+};
+
+struct StepArgs {
+  Geom g;
+  Phys p;
+  BinGeom bg;
+  Store A, B;                 // input layout / output layout (scatter)
+  int64_t cap, n;
+  const int64_t* off;         // [nbins+1] CSR of A
+  const int64_t* off_new;     // [nbins+1] CSR of B (scatter)
+  const int* slot_base;       // [nbins*27] base[s][j] (scatter; rebin_prep output)
+  const int* item_bin0;       // warp items of A
+  const int* n_items;
+  int nbins;
+  const float4* field;
+  float4* acc;
+  int* hist_next;             // [nbins*27] slot counts of the output layout (zeroed before)
+  float dt;
+  int nsteps;
+  int* err;                   // hard errors (ERRF_*)
+  int* far;                   // set when the next rebin cannot use the neighbour scatter
+  unsigned long long* movers; // particles whose end chunk differs from their output bin's chunk
+};
+
+int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s);
+int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s);
+int launch_hist_all_stay(const int64_t* off, int nbins, int* hist, cudaStream_t s);
+int launch_items(const int64_t* off, int nbins, uint32_t* flag, int64_t* pos, int64_t* partial, int* item_bin0,
+                 int* n_items, cudaStream_t s);
+int launch_bin_offsets(const int32_t* key_sorted, int64_t n, int nbins, int64_t* off, cudaStream_t s);
+int launch_bin_keys(const Geom& g, const BinGeom& bg, const float* x, int64_t xs, int64_t n, int32_t* key, int* err,
+                    cudaStream_t s);
+
+}  // namespace st

@@ -76,30 +76,70 @@ def test_inject_order_and_rebin_bit_exact():
     pg = g.get_particles()
     # C-15 given the GPU's own positions: stable sort of the pre-rebin order (= id order here)
     gi = by_id(pg)
-    _, chunk = o.locate(gi["x"])
-    perm, _ = oracle.stable_order(chunk, wl.dims[0] // 8 * (wl.dims[1] // 8) * (wl.dims[2] // 8))
+    perm, _ = oracle.stable_order(o.bin_key(gi["x"]), o.mesh.n_bins)
     assert np.array_equal(pg["id"], gi["id"][perm])
     assert np.all(np.diff(pg["chunk"]) >= 0)
+    assert np.all(np.diff(o.bin_key(pg["x"])) >= 0)
 
 
-def test_rebin_order_given_gpu_positions():
-    """After many steps (K = 2): feed the GPU's pre-rebin order and post-step positions
-    to the oracle's locate + stable sort; the GPU's own order must come out."""
-    wl = synth.workload("C2", n_particles=200_000)
-    g, o, _, F = _setup(wl, rebin_interval=2)
-    for _ in range(5):
-        g.advance(wl.dt, 1)      # calls 1..5: rebins after 2, 4
-    before = g.get_particles()   # order after call 5 (no rebin at 5)
-    g.advance(wl.dt, 1)          # call 6: advance then rebin
-    after = g.get_particles()
+def _check_rebin_given_gpu_positions(o, before, after):
     pos = {int(i): k for k, i in enumerate(after["id"])}
     idx = np.array([pos[int(i)] for i in before["id"]])
     X = after["x"][:, idx]        # post-step positions in pre-rebin order
-    _, chunk = o.locate(X)
-    perm, _ = oracle.stable_order(chunk, 512)
+    perm, _ = oracle.stable_order(o.bin_key(X), o.mesh.n_bins)
     assert np.array_equal(after["id"], before["id"][perm])
     c2, k2 = o.locate(after["x"])
     assert np.array_equal(after["cell"], c2) and np.array_equal(after["chunk"], k2)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_rebin_order_given_gpu_positions(K):
+    """After many steps at rebin interval K (fused neighbour scatter): feed the GPU's
+    pre-rebin order and post-step positions to the oracle's bin key + stable sort;
+    the GPU's own order must come out (C-15)."""
+    wl = synth.workload("C2", n_particles=200_000)
+    g, o, _, F = _setup(wl, rebin_interval=K)
+    for _ in range(3 * K + K - 1):
+        g.advance(wl.dt, 1)      # the last call leaves no rebin due
+    before = g.get_particles()
+    g.advance(wl.dt, 1)          # this call ends with a rebin
+    after = g.get_particles()    # observing flushes it (standalone scatter)
+    _check_rebin_given_gpu_positions(o, before, after)
+    st = g.stats()
+    assert st["rebins"] >= 4
+
+
+def test_fused_rebin_then_observe():
+    """K = 1: rebins fused into the next advance; observe after several calls."""
+    wl = synth.workload("C3", n_particles=300_000)
+    wl.dims, wl.cell_size = (64, 64, 64), (1 / 16,) * 3
+    g, o, _, F = _setup(wl, rebin_interval=1)
+    g.advance(wl.dt, 1)
+    g.advance(wl.dt, 1)
+    before = g.get_particles()
+    for _ in range(5):
+        g.advance(wl.dt, 1)
+    mid = g.stats()
+    assert mid["fused_rebins"] >= 4, mid
+    before = g.get_particles()
+    g.advance(wl.dt, 1)
+    after = g.get_particles()
+    _check_rebin_given_gpu_positions(o, before, after)
+
+
+def test_far_movers_fall_back_to_general_sort():
+    """Particles moving more than one cell between rebins (K = 8, fast flow) take the
+    general radix path; the order is still the contract's."""
+    wl = synth.workload("C2", n_particles=100_000)
+    g, o, _, F = _setup(wl, rebin_interval=8)
+    F2 = (F * 20.0).astype(np.float32)       # up to 20 m/s: several cells per 8 calls
+    g.set_fluid_field(F2)
+    for _ in range(15):
+        g.advance(wl.dt, 1)
+    before = g.get_particles()
+    g.advance(wl.dt, 1)                       # call 16 ends with a rebin
+    after = g.get_particles()
+    _check_rebin_given_gpu_positions(o, before, after)
 
 
 # ------------------------------------------------------------------ closed form through the GPU
@@ -279,6 +319,7 @@ def test_ragged_chunks_and_multi_substeps():
     c, k = o.locate(pg["x"])
     assert np.array_equal(pg["cell"], c) and np.array_equal(pg["chunk"], k)
     assert np.all(np.diff(pg["chunk"]) >= 0)
+    assert np.all(np.diff(o.bin_key(pg["x"])) >= 0)
 
 
 def test_async_split_readout_and_device_buffers():

@@ -474,6 +474,7 @@ def test_p9_rebin_and_multirank_migration():
         for i in range(a["id"].size):
             pos[int(a["id"][i])] = (r, i)
         assert np.all(np.diff(a["chunk"]) >= 0)
+        assert np.all(np.diff(sim.bin_key(a["x"])) >= 0)
         kz = a["chunk"] // (mesh.nchunk[0] * mesh.nchunk[1])
         lo, hi = ranges[r]
         assert np.all((kz >= lo) & (kz < hi))
@@ -483,13 +484,39 @@ def test_p9_rebin_and_multirank_migration():
         for i in after[r]["id"]:
             M[src_of[int(i)], r] += 1
     assert np.array_equal(M, sim.M)
-    # ties within a chunk: kept particles (source == r) precede arrivals, arrivals by source rank
+    # ties within a bin: kept particles (source == r) precede arrivals, arrivals by source rank
     for r in range(R):
         a = after[r]
-        for c in np.unique(a["chunk"]):
-            srcs = [src_of[int(i)] for i in a["id"][a["chunk"] == c]]
+        bins = sim.bin_key(a["x"])
+        for c in np.unique(bins):
+            srcs = [src_of[int(i)] for i in a["id"][bins == c]]
             key = [(0 if s == r else 1, s) for s in srcs]
             assert key == sorted(key)
+
+
+def test_p9_bin_key_brute_force():
+    """C-15 bin key = chunk * cc^3 + cell-within-chunk, checked against a brute-force
+    enumeration of the chunk boxes and the cells inside each (ragged last chunk)."""
+    mesh = Mesh(dims=(10, 7, 5), cell_size=(0.5, 1.0, 2.0), chunk_cells=4)
+    sim = Sim(mesh, precision="f64")
+    rng = np.random.default_rng(21)
+    x = rng.random((3, 3000)) * np.array([[5.0], [7.0], [10.0]])
+    key = sim.bin_key(x)
+    cell, _ = sim.locate(x)
+    cc, (ncx, ncy, ncz) = 4, mesh.nchunk
+    expect = {}
+    for kz in range(ncz):
+        for ky in range(ncy):
+            for kx in range(ncx):
+                chunk = (kz * ncy + ky) * ncx + kx
+                for lz in range(cc):
+                    for ly in range(cc):
+                        for lx in range(cc):
+                            cx, cy, cz = kx * cc + lx, ky * cc + ly, kz * cc + lz
+                            if cx < 10 and cy < 7 and cz < 5:
+                                expect[(cz * 7 + cy) * 10 + cx] = chunk * cc ** 3 + (lz * cc + ly) * cc + lx
+    assert all(int(k) == expect[int(c)] for k, c in zip(key, cell))
+    assert len(set(expect.values())) == 10 * 7 * 5
 
 
 # ---------------------------------------------------------------- P-10 / P-11
