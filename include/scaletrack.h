@@ -194,6 +194,10 @@ st_status st_locate(st_ctx* ctx, int64_t n, const float* x, int32_t* cell, int32
 st_status st_get_migration_counts(st_ctx* ctx, int64_t* row);
 
 st_status st_get_layout(st_ctx* ctx, st_layout* out);
+
+/* Host-only: validate cfg and compute the layout of cfg->rank without touching
+ * a GPU (the same slab rule st_init uses, C-16).  ST_ERR_INVALID_ARG on a bad cfg. */
+st_status st_plan_layout(const st_config* cfg, st_layout* out);
 st_status st_get_stats(st_ctx* ctx, st_stats* out);
 
 /* Block until all work enqueued by this context has finished. */

@@ -88,6 +88,7 @@ SIGNATURES = {
     "st_locate": (_i32, [_vp, _i64, _vp, _vp, _vp]),
     "st_get_migration_counts": (_i32, [_vp, _vp]),
     "st_get_layout": (_i32, [_vp, ctypes.POINTER(StLayout)]),
+    "st_plan_layout": (_i32, [ctypes.POINTER(StConfig), ctypes.POINTER(StLayout)]),
     "st_get_stats": (_i32, [_vp, ctypes.POINTER(StStats)]),
     "st_sync": (_i32, [_vp]),
     "st_last_timings": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),

@@ -85,6 +85,19 @@ class Config:
         return int(self.dims[0]) * int(self.dims[1]) * int(self.dims[2])
 
 
+def plan_layout(cfg: Config) -> N.StLayout:
+    """Host-only layout of cfg.rank (st_plan_layout): no GPU needed."""
+    lib = N.load()
+    o = N.StLayout()
+    c = cfg.to_c()
+    if cfg.nranks > 1:
+        c.nccl_unique_id = 1   # only checked for non-NULL by the validator
+    rc = lib.st_plan_layout(ctypes.byref(c), ctypes.byref(o))
+    if rc:
+        raise N.StError(rc, lib.st_last_error(None).decode())
+    return o
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     rc = N.load().st_nccl_unique_id(buf)

@@ -839,6 +839,28 @@ st_status st_get_layout(st_ctx* c, st_layout* o) {
   return ST_OK;
 }
 
+st_status st_plan_layout(const st_config* cfg, st_layout* o) {
+  if (!cfg || !o) return ST_ERR_INVALID_ARG;
+  std::string why;
+  st_status s = validate(cfg, why);
+  if (s) {
+    g_init_error = why;
+    return s;
+  }
+  st_ctx tmp;
+  tmp.cfg = *cfg;
+  build_geometry(&tmp);
+  o->z0 = tmp.z0;
+  o->z1 = tmp.z1;
+  o->kz0 = tmp.kz0;
+  o->kz1 = tmp.kz1;
+  o->n_chunks_global = tmp.g.NC[0] * tmp.g.NC[1] * tmp.g.NC[2];
+  for (int a = 0; a < 3; ++a) o->nchunk[a] = tmp.g.NC[a];
+  o->local_cells = tmp.local_cells;
+  o->halo_cells = tmp.H;
+  return ST_OK;
+}
+
 st_status st_get_stats(st_ctx* c, st_stats* o) {
   ST_ALIVE(c);
   if (!o) return ST_ERR_INVALID_ARG;
