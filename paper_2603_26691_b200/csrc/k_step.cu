@@ -6,19 +6,19 @@
 // particle stays within one cell of its bin's cell per axis, so a rebin is a
 // *neighbour-slot* stable counting sort: each particle of source bin s lands in
 // one of the 27 neighbour bins d = s + delta(j).  Its destination is
-//   dest = off_new[d] + base[s][j] + (# earlier particles of s with slot j)
-// where base[s][j] = sum of cnt[s'][j'] over the sources s' < s of d (the
+//   dest = off_new[d] + base[j][s] + (# earlier particles of s with slot j)
+// where base[j][s] = sum of cnt[j'][s'] over the sources s' < s of d (the
 // stable order keeps source bins in ascending order, then the old order).
-// cnt[s][j] is the slot histogram counted by the previous advance.
+// cnt[j][s] (slot-major, coalesced in the prep) is counted by the previous step.
 //
 // One warp owns one "item" (<= kMaxBins consecutive bins); the kernel is
 // persistent (grid-stride over items) and, per particle:
 //   [SCATTER] slot j of the current cell w.r.t. the bin, rank by __match_any_sync,
 //   [ADVANCE] locate -> trilinear u_f (L1-broadcast float4 loads) -> drag + gravity
-//             exponential update -> deposit by warp segmented reduction over
-//             equal cells (one red.global.add.v4.f32 per segment) -> walls / wrap,
-//   [HIST]    slot of the end position w.r.t. the output bin, counted by segmented
-//             reduction + one atomicAdd per segment (input of the next rebin),
+//             exponential update -> deposit: lanes with equal cells are reduced with
+//             a masked butterfly and one red.global.add.v4.f32 per group,
+//   [HIST]    slot of the end position w.r.t. the output bin, one atomicAdd per
+//             (bin, slot) group (input of the next rebin),
 //   then writes the particle to B[dest] (scatter) or back in place.
 #include <cuda_runtime.h>
 
@@ -31,6 +31,7 @@ namespace {
 
 constexpr int kSlots = 27;
 constexpr int kStay = 13;
+constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -44,25 +45,27 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
 }
 
 // ---------------------------------------------------------------- bin geometry
+__device__ __forceinline__ int div_cc(const BinGeom& b, int v, int cc) { return b.sh >= 0 ? (v >> b.sh) : v / cc; }
+
 __device__ __forceinline__ int bin_of_cell(const Geom& g, const BinGeom& b, int cx, int cy, int cz) {
   const int cc = g.cc;
-  const int kx = cx / cc, ky = cy / cc, kz = cz / cc;
-  const int chunk = (kz * g.NC[1] + ky) * g.NC[0] + kx - g.chunk_base;
+  const int kx = div_cc(b, cx, cc), ky = div_cc(b, cy, cc), kz = div_cc(b, cz, cc);
+  const int chunk = ((kz - b.kz0) * g.NC[1] + ky) * g.NC[0] + kx;
   const int lc = ((cz - kz * cc) * cc + (cy - ky * cc)) * cc + (cx - kx * cc);
   return chunk * b.cc3 + lc;
 }
 
+// (amortised: once per bin per item / per prep thread)
 __device__ __forceinline__ void cell_of_bin(const Geom& g, const BinGeom& b, int bin, int& cx, int& cy, int& cz) {
   const int cc = g.cc;
-  const int chunk = bin / b.cc3 + g.chunk_base;
-  const int lc = bin - (bin / b.cc3) * b.cc3;
+  const int chunk = bin / b.cc3;
+  const int lc = bin - chunk * b.cc3;
   const int kx = chunk % g.NC[0];
   const int ky = (chunk / g.NC[0]) % g.NC[1];
-  const int kz = chunk / (g.NC[0] * g.NC[1]);
-  const int lx = lc % cc, ly = (lc / cc) % cc, lz = lc / (cc * cc);
-  cx = kx * cc + lx;
-  cy = ky * cc + ly;
-  cz = kz * cc + lz;
+  const int kz = chunk / (g.NC[0] * g.NC[1]) + b.kz0;
+  cx = kx * cc + lc % cc;
+  cy = ky * cc + (lc / cc) % cc;
+  cz = kz * cc + lc / (cc * cc);
 }
 
 // canonical per-axis delta from -> to in {-1,0,1}; 2 = not a neighbour
@@ -86,7 +89,6 @@ __device__ __forceinline__ int axis_step(int from, int d, int n, int bc, bool& o
   return t;
 }
 
-// slot of cell (cx,cy,cz) relative to the cell (sx,sy,sz); -1 if not a neighbour
 __device__ __forceinline__ int slot_of(const Geom& g, int sx, int sy, int sz, int cx, int cy, int cz) {
   const int dx = axis_delta(sx, cx, g.n[0], g.bc[0]);
   const int dy = axis_delta(sy, cy, g.n[1], g.bc[1]);
@@ -95,43 +97,17 @@ __device__ __forceinline__ int slot_of(const Geom& g, int sx, int sy, int sz, in
   return (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
 }
 
-// ---------------------------------------------------------------- warp helpers
-// Inclusive segmented sum over lanes with equal `key` in consecutive lanes; lanes
-// whose key differs from the next lane's (segment tails) return true.
-__device__ __forceinline__ bool seg_sum3(long long key, float& a, float& b, float& c) {
-  const int lane = threadIdx.x & 31;
-  const long long kprev = __shfl_up_sync(0xffffffffu, key, 1);
-  const long long knext = __shfl_down_sync(0xffffffffu, key, 1);
-  bool head = (lane == 0) || (kprev != key);
-  for (int off = 1; off < 32; off <<= 1) {
-    const float ua = __shfl_up_sync(0xffffffffu, a, off);
-    const float ub = __shfl_up_sync(0xffffffffu, b, off);
-    const float uc = __shfl_up_sync(0xffffffffu, c, off);
-    const int uh = __shfl_up_sync(0xffffffffu, (int)head, off);
-    if (lane >= off && !head) {
-      a += ua;
-      b += ub;
-      c += uc;
-      head = uh;
-    }
+// ---------------------------------------------------------------- warp reductions
+// Sum (a,b,c) over the lanes of `grp` (a lane mask containing the caller when
+// member) with a masked butterfly: every lane gets the group total.
+__device__ __forceinline__ void group_sum3(bool member, float& a, float& b, float& c) {
+  if (!member) a = b = c = 0.0f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(kFull, a, o);
+    b += __shfl_xor_sync(kFull, b, o);
+    c += __shfl_xor_sync(kFull, c, o);
   }
-  return (lane == 31) || (knext != key);
-}
-
-__device__ __forceinline__ bool seg_count(long long key, int& cnt) {
-  const int lane = threadIdx.x & 31;
-  const long long kprev = __shfl_up_sync(0xffffffffu, key, 1);
-  const long long knext = __shfl_down_sync(0xffffffffu, key, 1);
-  bool head = (lane == 0) || (kprev != key);
-  for (int off = 1; off < 32; off <<= 1) {
-    const int u = __shfl_up_sync(0xffffffffu, cnt, off);
-    const int uh = __shfl_up_sync(0xffffffffu, (int)head, off);
-    if (lane >= off && !head) {
-      cnt += u;
-      head = uh;
-    }
-  }
-  return (lane == 31) || (knext != key);
 }
 
 struct Stencil {
@@ -153,8 +129,8 @@ __device__ __forceinline__ float4 lerp4(float4 a, float4 b, float f) {
 }
 
 __device__ __forceinline__ float4 trilinear(const Geom& g, const float4* __restrict__ F, const Stencil& s) {
-  const int64_t pz = (int64_t)g.gy * g.gx;
-  const float4* b = F + (int64_t)s.wz * pz + (int64_t)s.wy * g.gx + s.wx;
+  const int pz = g.gy * g.gx;
+  const float4* b = F + ((int64_t)s.wz * pz + s.wy * g.gx + s.wx);
   const float4 c000 = __ldg(b), c100 = __ldg(b + 1);
   const float4 c010 = __ldg(b + g.gx), c110 = __ldg(b + g.gx + 1);
   const float4 c001 = __ldg(b + pz), c101 = __ldg(b + pz + 1);
@@ -167,43 +143,51 @@ __device__ __forceinline__ float4 trilinear(const Geom& g, const float4* __restr
 
 // ---------------------------------------------------------------- the step kernel
 template <bool SCATTER, bool ADVANCE>
-__global__ void __launch_bounds__(256) k_step(StepArgs a) {
+__global__ void __launch_bounds__(256, 4) k_step(StepArgs a) {
   __shared__ int run_s[8][kMaxBins * kSlots];
-  __shared__ long long off_s[8][kMaxBins + 1];
+  __shared__ int rel_s[8][kMaxBins + 1];     // particle offsets of the item's bins, relative to p0
+  __shared__ int cell_s[8][kMaxBins][3];      // cell coordinates of the item's bins
   const Geom& g = a.g;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   int* run = run_s[wib];
-  long long* offw = off_s[wib];
+  int* rel = rel_s[wib];
   const int n_items = *a.n_items;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t cap = a.cap;
+  const int nbins = a.nbins;
   int flags = 0, farflag = 0;
+  unsigned movers = 0;
 
   for (int item = blockIdx.x * (blockDim.x >> 5) + wib; item < n_items; item += warps_total) {
     const int b0 = a.item_bin0[item];
-    const int b1 = (item + 1 < n_items) ? a.item_bin0[item + 1] : a.nbins;
+    const int b1 = (item + 1 < n_items) ? a.item_bin0[item + 1] : nbins;
     const int nb = b1 - b0;
-    for (int k = lane; k <= nb; k += 32) offw[k] = a.off[b0 + k];
+    const int64_t p0 = a.off[b0];
+    for (int k = lane; k <= nb; k += 32) rel[k] = (int)(a.off[b0 + k] - p0);
+    for (int k = lane; k < nb; k += 32) cell_of_bin(g, a.bg, b0 + k, cell_s[wib][k][0], cell_s[wib][k][1], cell_s[wib][k][2]);
     if (SCATTER)
       for (int k = lane; k < nb * kSlots; k += 32) run[k] = 0;
     __syncwarp();
-    const int64_t p0 = offw[0], p1 = offw[nb];
-    for (int64_t base = p0; base < p1; base += 32) {
-      const int64_t i = base + lane;
-      const bool valid = i < p1;
-      // bin of particle i: last k with offw[k] <= i
-      int lb = 0;
+    const int np = rel[nb];
+    int lb_base = 0;
+    for (int base = 0; base < np; base += 32) {
+      const int r = base + lane;
+      const bool valid = r < np;
+      const int64_t i = p0 + r;
+      // bin of the particle: last k >= lb_base with rel[k] <= r
+      int lb = lb_base;
       if (valid) {
-        int lo = 0, hi = nb - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (offw[mid] <= i) lo = mid;
+        int hi = nb - 1;
+        while (lb < hi) {
+          const int mid = (lb + hi + 1) >> 1;
+          if (rel[mid] <= r) lb = mid;
           else hi = mid - 1;
         }
-        lb = lo;
       }
+      lb_base = __shfl_sync(kFull, lb, 0);
       const int s = b0 + lb;
+      const int sx = cell_s[wib][lb][0], sy = cell_s[wib][lb][1], sz = cell_s[wib][lb][2];
       float xp[3] = {0.f, 0.f, 0.f}, up[3] = {0.f, 0.f, 0.f};
       float dp = 1e-5f, wp = 0.f;
       unsigned long long pid = 0;
@@ -217,34 +201,38 @@ __global__ void __launch_bounds__(256) k_step(StepArgs a) {
       // current cell (deposit cell of the first sub-step; scatter key)
       float t[3];
       int c[3];
+#pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         t[ax] = cell_coord(xp[ax], g.lo[ax], g.ih[ax]);
         c[ax] = cell_from_t(t[ax], g.n[ax]);
       }
-      int sx, sy, sz;
-      cell_of_bin(g, a.bg, s, sx, sy, sz);
-      int obin = s;   // bin of the particle in the output layout
+      // cell of the particle's bin in the output layout
+      int ox = sx, oy = sy, oz = sz;
+      int obin = s;
       int64_t dest = i;
       bool write_ok = valid;
       if (SCATTER) {
-        int j = valid ? slot_of(g, sx, sy, sz, c[0], c[1], c[2]) : -1;
+        const int j = valid ? slot_of(g, sx, sy, sz, c[0], c[1], c[2]) : -1;
         if (valid && j < 0) {
           flags |= ERRF_SCATTER;
           write_ok = false;
         }
-        const int key = (valid && j >= 0) ? lb * kSlots + j : -1 - lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int key = write_ok ? lb * kSlots + j : -1 - lane;
+        const unsigned peers = __match_any_sync(kFull, key);
         const int leader = __ffs(peers) - 1;
         int rbase = 0;
         if (lane == leader && key >= 0) {
           rbase = run[key];
           run[key] = rbase + __popc(peers);
         }
-        rbase = __shfl_sync(0xffffffffu, rbase, leader);
+        rbase = __shfl_sync(kFull, rbase, leader);
         __syncwarp();
         if (write_ok) {
-          obin = bin_of_cell(g, a.bg, c[0], c[1], c[2]);
-          dest = a.off_new[obin] + (int64_t)a.slot_base[(int64_t)s * kSlots + j] + rbase + __popc(peers & lanemask_lt());
+          ox = c[0];
+          oy = c[1];
+          oz = c[2];
+          obin = bin_of_cell(g, a.bg, ox, oy, oz);
+          dest = a.off_new[obin] + (int64_t)a.slot_base[(int64_t)j * nbins + s] + rbase + __popc(peers & lanemask_lt());
           if (dest < 0 || dest >= a.n) {
             flags |= ERRF_SCATTER;
             write_ok = false;
@@ -258,6 +246,7 @@ __global__ void __launch_bounds__(256) k_step(StepArgs a) {
         const float mw = a.p.mass_c * d * d * d * wp;
         for (int sub = 0; sub < a.nsteps; ++sub) {
           if (sub > 0) {
+#pragma unroll
             for (int ax = 0; ax < 3; ++ax) {
               t[ax] = cell_coord(xp[ax], g.lo[ax], g.ih[ax]);
               c[ax] = cell_from_t(t[ax], g.n[ax]);
@@ -287,15 +276,17 @@ __global__ void __launch_bounds__(256) k_step(StepArgs a) {
             float E, M;
             exp_pair(h, E, M);
             const float tM = taue * M;
+#pragma unroll
             for (int ax = 0; ax < 3; ++ax) {
               const float us = fmaf(a.p.g[ax], taue, ufa[ax]);
-              const float rel = up[ax] - us;
-              du[ax] = fmaf(-M, rel, -a.p.g[ax] * a.dt);
-              xp[ax] = fmaf(tM, rel, fmaf(us, a.dt, xp[ax]));
-              up[ax] = fmaf(E, rel, us);
+              const float rl = up[ax] - us;
+              du[ax] = fmaf(-M, rl, -a.p.g[ax] * a.dt);
+              xp[ax] = fmaf(tM, rl, fmaf(us, a.dt, xp[ax]));
+              up[ax] = fmaf(E, rl, us);
             }
           } else {
             const float inv1h = __frcp_rn(1.0f + h);
+#pragma unroll
             for (int ax = 0; ax < 3; ++ax) {
               const float un = (up[ax] + h * ufa[ax] + a.dt * a.p.g[ax]) * inv1h;
               du[ax] = (un - up[ax]) - a.p.g[ax] * a.dt;
@@ -304,16 +295,28 @@ __global__ void __launch_bounds__(256) k_step(StepArgs a) {
             }
           }
           if (a.p.two_way) {
-            // deposit -w m du into the start cell: warp segmented reduction over
-            // equal cells (cell-sorted warps -> one reduction per segment)
+            // deposit -w m du into the start cell: the largest group of lanes with
+            // equal cells (cell-sorted warps) is reduced in registers, the rest red
+            // directly; one red.global.add.v4.f32 per group
             const int az = acc_z(g, c[2]);
             if (valid && az < 0) flags |= ERRF_WINDOW;
             const bool dep = valid && az >= 0;
-            const long long ckey = dep ? ((long long)az * g.n[1] + c[1]) * g.n[0] + c[0] : -1 - lane;
-            float ja = dep ? -mw * du[0] : 0.f, jb = dep ? -mw * du[1] : 0.f, jc = dep ? -mw * du[2] : 0.f;
-            const bool tail = seg_sum3(ckey, ja, jb, jc);
-            if (tail && ckey >= 0) red_add_v4(a.acc + ckey, ja, jb, jc);
+            const int ckey = dep ? (az * g.n[1] + c[1]) * g.n[0] + c[0] : -1 - lane;
+            float ja = -mw * du[0], jb = -mw * du[1], jc = -mw * du[2];
+            const unsigned peers = __match_any_sync(kFull, ckey);
+            const int lead = __shfl_sync(kFull, ckey, 0);
+            const unsigned major = __shfl_sync(kFull, peers, 0);
+            if (__popc(major) >= 4 && lead >= 0) {
+              const bool in = (major >> lane) & 1u;
+              float ra = ja, rb = jb, rc = jc;
+              group_sum3(in, ra, rb, rc);
+              if (lane == 0) red_add_v4(a.acc + lead, ra, rb, rc);
+              if (!in && dep) red_add_v4(a.acc + ckey, ja, jb, jc);
+            } else if (dep) {
+              red_add_v4(a.acc + ckey, ja, jb, jc);
+            }
           }
+#pragma unroll
           for (int ax = 0; ax < 3; ++ax)
             if (apply_bc(g.bc[ax], g.lo[ax], g.hi[ax], g.L[ax], xp[ax], up[ax]) && valid) flags |= ERRF_CFL;
         }
@@ -321,20 +324,18 @@ __global__ void __launch_bounds__(256) k_step(StepArgs a) {
       // slot histogram of the end position w.r.t. the output bin (next rebin's input)
       {
         int e[3];
+#pragma unroll
         for (int ax = 0; ax < 3; ++ax) e[ax] = cell_from_t(cell_coord(xp[ax], g.lo[ax], g.ih[ax]), g.n[ax]);
-        int ox, oy, oz;
-        cell_of_bin(g, a.bg, obin, ox, oy, oz);
         const int j2 = write_ok ? slot_of(g, ox, oy, oz, e[0], e[1], e[2]) : -1;
         if (write_ok && j2 < 0) farflag = 1;
-        const long long hkey = (write_ok && j2 >= 0) ? (long long)obin * kSlots + j2 : -1 - lane;
-        int cnt = (hkey >= 0) ? 1 : 0;
-        const bool tail = seg_count(hkey, cnt);
-        if (tail && hkey >= 0) atomicAdd(a.hist_next + hkey, cnt);
+        const long long hkey = (write_ok && j2 >= 0) ? (long long)j2 * nbins + obin : -1 - lane;
+        const unsigned peers = __match_any_sync(kFull, hkey);
+        if (hkey >= 0 && (peers & lanemask_lt()) == 0) atomicAdd(a.hist_next + hkey, __popc(peers));
         // chunk movers w.r.t. the output bins (the algorithmic rebin traffic)
-        const bool mover = write_ok && ((e[0] / g.cc) != (ox / g.cc) || (e[1] / g.cc) != (oy / g.cc) ||
-                                        (e[2] / g.cc) != (oz / g.cc));
-        const unsigned mb = __ballot_sync(0xffffffffu, mover);
-        if (lane == 0 && mb) atomicAdd(a.movers, (unsigned long long)__popc(mb));
+        const bool mover = write_ok && (div_cc(a.bg, e[0], g.cc) != div_cc(a.bg, ox, g.cc) ||
+                                        div_cc(a.bg, e[1], g.cc) != div_cc(a.bg, oy, g.cc) ||
+                                        div_cc(a.bg, e[2], g.cc) != div_cc(a.bg, oz, g.cc));
+        movers += mover ? 1u : 0u;
       }
       if (write_ok) {
         if (SCATTER) {
@@ -351,13 +352,18 @@ __global__ void __launch_bounds__(256) k_step(StepArgs a) {
     }
     __syncwarp();
   }
+  // warp totals -> one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) movers += __shfl_xor_sync(kFull, movers, o);
+  if (lane == 0 && movers) atomicAdd(a.movers, (unsigned long long)movers);
   if (flags) atomicOr(a.err, flags);
   if (farflag) *(volatile int*)a.far = 1;
 }
 
 // ---------------------------------------------------------------- rebin preparation
 // Per destination bin d: sources s = d - delta over the 27 deltas (canonical,
-// deduplicated), in ascending s; base[s][j] = running sum; new_cnt[d] = total.
+// deduplicated), in ascending s; base[j][s] = running sum; new_cnt[d] = total.
+// The slot-major layout makes consecutive threads touch consecutive words.
 __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cnt_base, uint32_t* __restrict__ new_cnt) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nbins) return;
@@ -367,46 +373,41 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
     new_cnt[d] = 0;
     return;
   }
-  int src[27], slot[27], ns = 0;
-  for (int oz = -1; oz <= 1; ++oz)
-    for (int oy = -1; oy <= 1; ++oy)
-      for (int ox = -1; ox <= 1; ++ox) {
-        bool ok = true;
-        const int sx = axis_step(dx, -ox, g.n[0], g.bc[0], ok);
-        const int sy = axis_step(dy, -oy, g.n[1], g.bc[1], ok);
-        const int sz = axis_step(dz, -oz, g.n[2], g.bc[2], ok);
-        if (!ok) continue;
-        const int kz = sz / g.cc;
-        const int kz_lo = g.chunk_base / (g.NC[0] * g.NC[1]);
-        if (kz < kz_lo || kz >= kz_lo + bg.nkz) continue;   // source outside this rank's bins
-        const int j = slot_of(g, sx, sy, sz, dx, dy, dz);
-        if (j != (oz + 1) * 9 + (oy + 1) * 3 + (ox + 1)) continue;   // non-canonical duplicate
-        const int s = bin_of_cell(g, bg, sx, sy, sz);
-        // insertion by ascending s
-        int q = ns++;
-        while (q > 0 && src[q - 1] > s) {
-          src[q] = src[q - 1];
-          slot[q] = slot[q - 1];
-          --q;
-        }
-        src[q] = s;
-        slot[q] = j;
-      }
-  uint32_t run = 0;
-  for (int q = 0; q < ns; ++q) {
-    int* e = cnt_base + (int64_t)src[q] * kSlots + slot[q];
-    const int v = *e;
-    *e = (int)run;
-    run += (uint32_t)v;
+  const int kz_lo = bg.kz0, kz_hi = bg.kz0 + bg.nkz;
+  // the 27 candidate sources s = d - delta(j); key = bin (INT_MAX if absent)
+  int key[27], cnt[27];
+#pragma unroll
+  for (int j = 0; j < 27; ++j) {
+    const int ox = j % 3 - 1, oy = (j / 3) % 3 - 1, oz = j / 9 - 1;
+    bool ok = true;
+    const int sx = axis_step(dx, -ox, g.n[0], g.bc[0], ok);
+    const int sy = axis_step(dy, -oy, g.n[1], g.bc[1], ok);
+    const int sz = axis_step(dz, -oz, g.n[2], g.bc[2], ok);
+    if (ok) {
+      const int kz = div_cc(bg, sz, g.cc);
+      ok = kz >= kz_lo && kz < kz_hi &&                    // source on this rank
+           slot_of(g, sx, sy, sz, dx, dy, dz) == j;          // canonical (no duplicate)
+    }
+    key[j] = ok ? bin_of_cell(g, bg, sx, sy, sz) : 0x7fffffff;
+    cnt[j] = ok ? cnt_base[(int64_t)j * nbins + key[j]] : 0;
   }
-  new_cnt[d] = run;
+  // stable order = ascending source bin: base of source q = sum of the counts of
+  // the sources with a smaller bin (keys are distinct), all in registers
+  uint32_t total = 0;
+#pragma unroll
+  for (int q = 0; q < 27; ++q) {
+    uint32_t base = 0;
+#pragma unroll
+    for (int p = 0; p < 27; ++p) base += (key[p] < key[q]) ? (uint32_t)cnt[p] : 0u;
+    if (key[q] != 0x7fffffff) cnt_base[(int64_t)q * nbins + key[q]] = (int)base;
+    total += (uint32_t)cnt[q];
+  }
+  new_cnt[d] = total;
 }
 
-__global__ void k_hist_all_stay(const int64_t* __restrict__ off, int nbins, int* __restrict__ hist) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= (int64_t)nbins * kSlots) return;
-  const int s = (int)(q / kSlots), j = (int)(q - (int64_t)s * kSlots);
-  hist[q] = (j == kStay) ? (int)(off[s + 1] - off[s]) : 0;
+__global__ void k_hist_stay(const int64_t* __restrict__ off, int nbins, int* __restrict__ hist_row13) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nbins) hist_row13[s] = (int)(off[s + 1] - off[s]);
 }
 
 // item boundaries: bin s starts an item if s % kMaxBins == 0 or the kItemParticles
@@ -479,12 +480,13 @@ int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s) {
 }
 
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s) {
-  k_rebin_prep<<<blocks_for(bg.nbins), 256, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt);
+  k_rebin_prep<<<blocks_for(bg.nbins), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt);
   return 1;
 }
 
 int launch_hist_all_stay(const int64_t* off, int nbins, int* hist, cudaStream_t s) {
-  k_hist_all_stay<<<blocks_for((int64_t)nbins * kSlots), 256, 0, s>>>(off, nbins, hist);
+  cudaMemsetAsync(hist, 0, (size_t)nbins * kSlots * sizeof(int), s);
+  k_hist_stay<<<blocks_for(nbins), 256, 0, s>>>(off, nbins, hist + (int64_t)kStay * nbins);
   return 1;
 }
 

@@ -250,6 +250,10 @@ static void build_geometry(st_ctx* c) {
   c->bg.cc3 = g.cc * g.cc * g.cc;
   c->bg.nbins = c->n_local_chunks * c->bg.cc3;
   c->bg.nkz = c->kz1 - c->kz0;
+  c->bg.kz0 = c->kz0;
+  c->bg.sh = -1;
+  for (int s = 0; s < 16; ++s)
+    if ((1 << s) == g.cc) c->bg.sh = s;
   // radix key = local bin (< nbins); multi-GPU pre-migration key = global chunk
   const int64_t kmax = std::max<int64_t>(c->bg.nbins, (int64_t)g.NC[0] * g.NC[1] * g.NC[2]);
   int bits = 1;

@@ -15,6 +15,8 @@ struct BinGeom {
   int cc3;     // cells per chunk (bins per chunk)
   int nbins;   // local bins = local chunks * cc3
   int nkz;     // local chunk planes
+  int kz0;     // first local chunk plane
+  int sh;      // log2(chunk_cells) if a power of two, else -1
 };
 
 struct StepArgs {

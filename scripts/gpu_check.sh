@@ -12,3 +12,7 @@ for K in 1 2; do
     > gpurun_out/bench_1e8_K$K.log 2>&1; echo "bench K=$K rc=$?"
   tail -3 gpurun_out/bench_1e8_K$K.log
 done
+if [ -n "$FULL" ]; then
+  timeout 900 python bench.py --steps 10 --warmup 3 --rebin-interval 1 > gpurun_out/bench_full_K1.log 2>&1; echo "bench full rc=$?"
+  tail -2 gpurun_out/bench_full_K1.log
+fi
