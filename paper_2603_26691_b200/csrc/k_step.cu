@@ -480,7 +480,7 @@ int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s) {
 }
 
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s) {
-  k_rebin_prep<<<blocks_for(bg.nbins), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt);
+  k_rebin_prep<<<blocks_for(bg.nbins, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt);
   return 1;
 }
 
