@@ -81,6 +81,9 @@ __global__ void k_check_domain(Geom g, const float* __restrict__ x, int64_t xs, 
       const float v = x[a * xs + i];
       if (!(v >= g.lo[a] && v <= g.hi[a])) bad = 1;
     }
+    // multi-GPU: the particle's cell must lie in this rank's slab
+    const int cz = cell_from_t(cell_coord(x[2 * xs + i], g.lo[2], g.ih[2]), g.n[2]);
+    if (cz < g.oz0 || cz >= g.oz1) bad = 1;
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, ERRF_DOMAIN);
 }

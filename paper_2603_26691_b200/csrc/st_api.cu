@@ -244,6 +244,8 @@ static void build_geometry(st_ctx* c) {
   g.anz = (c->z1 - c->z0) + 2 * c->H;
   g.wrapz = (G > 1 && f.bc[2] == ST_BC_PERIODIC) ? 1 : 0;
   g.chunk_base = c->kz0 * g.NC[0] * g.NC[1];
+  g.oz0 = c->z0;
+  g.oz1 = c->z1;
   c->chunk_lo = g.chunk_base;
   c->n_local_chunks = (c->kz1 - c->kz0) * g.NC[0] * g.NC[1];
   c->local_cells = (int64_t)g.n[0] * g.n[1] * (c->z1 - c->z0);

@@ -28,6 +28,7 @@ struct Geom {
   int az0, anz;
   int wrapz;                        // 1: periodic z with a partial window (nranks > 1)
   int chunk_base;                   // first global chunk id owned by this rank
+  int oz0, oz1;                     // owned cell planes [oz0, oz1)
 };
 
 struct Phys {

@@ -1,0 +1,38 @@
+"""Multi-GPU parity (NCCL over NVLink): torchrun ranks vs the oracle's R-rank
+emulation.  Needs >= 2 visible GPUs (run through `gpurun --gpus 2|4`); skipped
+otherwise.  The host-side protocol is also covered on CPU by
+tests/test_multirank_gloo.py."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+from tests.conftest import gpu_available
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    if not gpu_available():
+        return 0
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("K,bcz", [(1, 1), (2, 1), (1, 0)])
+def test_multigpu_matches_emulation(K, bcz):
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    env = dict(os.environ, MR_K=str(K), MR_BCZ=str(bcz), MR_STEPS=str(6))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + 7 * K + bcz),
+           os.path.join(ROOT, "tests", "mr_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "MR_REPORT" in out
