@@ -20,6 +20,11 @@
 //   [HIST]    slot of the end position w.r.t. the output bin, one atomicAdd per
 //             (bin, slot) group (input of the next rebin),
 //   then writes the particle to B[dest] (scatter) or back in place.
+// The kernel is specialised at compile time on the periodic-axis mask (BCM) and
+// on log2(chunk_cells) (SH) so the hot loop carries no per-particle branches on
+// the configuration; BCM = -1 / SH = 0 are the generic (runtime) fallbacks.
+// Streaming particle traffic uses evict-first loads/stores (__ldcs/__stcs) so
+// L2 keeps the field, the accumulator and the histograms.
 #include <cuda_runtime.h>
 
 #include "st_device.cuh"
@@ -44,12 +49,34 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
                : "memory");
 }
 
-// ---------------------------------------------------------------- bin geometry
-__device__ __forceinline__ int div_cc(const BinGeom& b, int v, int cc) { return b.sh >= 0 ? (v >> b.sh) : v / cc; }
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
+// ---------------------------------------------------------------- configuration helpers
+template <int BCM>
+__device__ __forceinline__ bool periodic(const Geom& g, int ax) {
+  if (BCM < 0) return g.bc[ax] == ST_BC_PERIODIC;
+  return (BCM >> ax) & 1;
+}
+template <int SH>
+__device__ __forceinline__ int dcc(int v, int cc) {
+  if (SH > 0) return v >> SH;
+  return v / cc;
+}
+
+// ---------------------------------------------------------------- bin geometry
+template <int SH>
 __device__ __forceinline__ int bin_of_cell(const Geom& g, const BinGeom& b, int cx, int cy, int cz) {
-  const int cc = g.cc;
-  const int kx = div_cc(b, cx, cc), ky = div_cc(b, cy, cc), kz = div_cc(b, cz, cc);
+  const int cc = SH > 0 ? (1 << SH) : g.cc;
+  const int kx = dcc<SH>(cx, cc), ky = dcc<SH>(cy, cc), kz = dcc<SH>(cz, cc);
   const int chunk = ((kz - b.kz0) * g.NC[1] + ky) * g.NC[0] + kx;
   const int lc = ((cz - kz * cc) * cc + (cy - ky * cc)) * cc + (cx - kx * cc);
   return chunk * b.cc3 + lc;
@@ -69,13 +96,26 @@ __device__ __forceinline__ void cell_of_bin(const Geom& g, const BinGeom& b, int
 }
 
 // canonical per-axis delta from -> to in {-1,0,1}; 2 = not a neighbour
-__device__ __forceinline__ int axis_delta(int from, int to, int n, int bc) {
+template <int BCM>
+__device__ __forceinline__ int axis_delta(const Geom& g, int ax, int from, int to) {
   int d = to - from;
-  if (bc == ST_BC_PERIODIC && n >= 3) {
-    if (d == n - 1) d = -1;
-    else if (d == -(n - 1)) d = 1;
+  if (periodic<BCM>(g, ax)) {
+    const int n = g.n[ax];
+    if (n >= 3) {
+      d = (d == n - 1) ? -1 : d;
+      d = (d == -(n - 1)) ? 1 : d;
+    }
   }
-  return (d >= -1 && d <= 1) ? d : 2;
+  return ((unsigned)(d + 1) <= 2u) ? d : 2;
+}
+
+template <int BCM>
+__device__ __forceinline__ int slot_of(const Geom& g, int sx, int sy, int sz, int cx, int cy, int cz) {
+  const int dx = axis_delta<BCM>(g, 0, sx, cx);
+  const int dy = axis_delta<BCM>(g, 1, sy, cy);
+  const int dz = axis_delta<BCM>(g, 2, sz, cz);
+  const int j = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
+  return (dx == 2 || dy == 2 || dz == 2) ? -1 : j;
 }
 
 __device__ __forceinline__ int axis_step(int from, int d, int n, int bc, bool& ok) {
@@ -89,17 +129,7 @@ __device__ __forceinline__ int axis_step(int from, int d, int n, int bc, bool& o
   return t;
 }
 
-__device__ __forceinline__ int slot_of(const Geom& g, int sx, int sy, int sz, int cx, int cy, int cz) {
-  const int dx = axis_delta(sx, cx, g.n[0], g.bc[0]);
-  const int dy = axis_delta(sy, cy, g.n[1], g.bc[1]);
-  const int dz = axis_delta(sz, cz, g.n[2], g.bc[2]);
-  if (dx == 2 || dy == 2 || dz == 2) return -1;
-  return (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
-}
-
 // ---------------------------------------------------------------- warp reductions
-// Sum (a,b,c) over the lanes of `grp` (a lane mask containing the caller when
-// member) with a masked butterfly: every lane gets the group total.
 __device__ __forceinline__ void group_sum3(bool member, float& a, float& b, float& c) {
   if (!member) a = b = c = 0.0f;
 #pragma unroll
@@ -110,40 +140,23 @@ __device__ __forceinline__ void group_sum3(bool member, float& a, float& b, floa
   }
 }
 
-struct Stencil {
-  int wx, wy, wz;
-  float fx, fy, fz;
-};
-
-__device__ __forceinline__ void stencil_axis(float t, int n, int& i, float& f) {
-  const float s = t - 0.5f;
-  const float fl = floorf(s);
-  i = (int)fl;
-  f = s - fl;
-  if (i < -1) { i = -1; f = 0.0f; }
-  if (i > n - 1) { i = n - 1; f = 1.0f; }
-}
-
 __device__ __forceinline__ float4 lerp4(float4 a, float4 b, float f) {
   return make_float4(fmaf(f, b.x - a.x, a.x), fmaf(f, b.y - a.y, a.y), fmaf(f, b.z - a.z, a.z), 0.0f);
 }
 
-__device__ __forceinline__ float4 trilinear(const Geom& g, const float4* __restrict__ F, const Stencil& s) {
-  const int pz = g.gy * g.gx;
-  const float4* b = F + ((int64_t)s.wz * pz + s.wy * g.gx + s.wx);
-  const float4 c000 = __ldg(b), c100 = __ldg(b + 1);
-  const float4 c010 = __ldg(b + g.gx), c110 = __ldg(b + g.gx + 1);
-  const float4 c001 = __ldg(b + pz), c101 = __ldg(b + pz + 1);
-  const float4 c011 = __ldg(b + pz + g.gx), c111 = __ldg(b + pz + g.gx + 1);
-  const float4 c00 = lerp4(c000, c100, s.fx), c10 = lerp4(c010, c110, s.fx);
-  const float4 c01 = lerp4(c001, c101, s.fx), c11 = lerp4(c011, c111, s.fx);
-  const float4 c0 = lerp4(c00, c10, s.fy), c1 = lerp4(c01, c11, s.fy);
-  return lerp4(c0, c1, s.fz);
+// C-5 from the cell contract: t = (x-lo)*ih, c = cell; fr = t - c in [0,1];
+// stencil base = c-1 (fr < 1/2, weight fr+1/2) or c (weight fr-1/2), i.e.
+// floor(t - 1/2) and its fraction, within the ghost layer [-1, n].
+__device__ __forceinline__ void stencil_from_cell(float t, int c, int& i0, float& f) {
+  const float fr = t - (float)c;
+  const bool lo = fr < 0.5f;
+  i0 = lo ? c - 1 : c;
+  f = lo ? fr + 0.5f : fr - 0.5f;
 }
 
 // ---------------------------------------------------------------- the step kernel
-template <bool SCATTER, bool ADVANCE>
-__global__ void __launch_bounds__(256, 4) k_step(StepArgs a) {
+template <bool SCATTER, bool ADVANCE, int BCM, int SH>
+__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(StepArgs a) {
   __shared__ int run_s[8][kMaxBins * kSlots];
   __shared__ int rel_s[8][kMaxBins + 1];     // particle offsets of the item's bins, relative to p0
   __shared__ int cell_s[8][kMaxBins][3];      // cell coordinates of the item's bins
@@ -156,6 +169,7 @@ __global__ void __launch_bounds__(256, 4) k_step(StepArgs a) {
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t cap = a.cap;
   const int nbins = a.nbins;
+  const int cc = SH > 0 ? (1 << SH) : g.cc;
   int flags = 0, farflag = 0;
   unsigned movers = 0;
 
@@ -170,49 +184,34 @@ __global__ void __launch_bounds__(256, 4) k_step(StepArgs a) {
       for (int k = lane; k < nb * kSlots; k += 32) run[k] = 0;
     __syncwarp();
     const int np = rel[nb];
-    int lb_base = 0;
+    int lb = 0;   // this lane's bin pointer (monotone over its particles)
     for (int base = 0; base < np; base += 32) {
       const int r = base + lane;
       const bool valid = r < np;
       const int64_t i = p0 + r;
-      // bin of the particle: last k >= lb_base with rel[k] <= r
-      int lb = lb_base;
-      if (valid) {
-        int hi = nb - 1;
-        while (lb < hi) {
-          const int mid = (lb + hi + 1) >> 1;
-          if (rel[mid] <= r) lb = mid;
-          else hi = mid - 1;
-        }
-      }
-      lb_base = __shfl_sync(kFull, lb, 0);
+      if (valid)
+        while (rel[lb + 1] <= r) ++lb;
       const int s = b0 + lb;
       const int sx = cell_s[wib][lb][0], sy = cell_s[wib][lb][1], sz = cell_s[wib][lb][2];
-      float xp[3] = {0.f, 0.f, 0.f}, up[3] = {0.f, 0.f, 0.f};
+      float xp0 = 0.f, xp1 = 0.f, xp2 = 0.f, up0 = 0.f, up1 = 0.f, up2 = 0.f;
       float dp = 1e-5f, wp = 0.f;
-      unsigned long long pid = 0;
       if (valid) {
-        xp[0] = a.A.x[i]; xp[1] = a.A.x[cap + i]; xp[2] = a.A.x[2 * cap + i];
-        up[0] = a.A.u[i]; up[1] = a.A.u[cap + i]; up[2] = a.A.u[2 * cap + i];
-        dp = a.A.d[i];
-        wp = a.A.w[i];
-        if (SCATTER) pid = a.A.id[i];
+        xp0 = __ldcs(a.A.x + i); xp1 = __ldcs(a.A.x + cap + i); xp2 = __ldcs(a.A.x + 2 * cap + i);
+        up0 = __ldcs(a.A.u + i); up1 = __ldcs(a.A.u + cap + i); up2 = __ldcs(a.A.u + 2 * cap + i);
+        dp = __ldcs(a.A.d + i);
+        wp = __ldcs(a.A.w + i);
       }
       // current cell (deposit cell of the first sub-step; scatter key)
-      float t[3];
-      int c[3];
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        t[ax] = cell_coord(xp[ax], g.lo[ax], g.ih[ax]);
-        c[ax] = cell_from_t(t[ax], g.n[ax]);
-      }
+      float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
+            t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
+      int c0 = cell_from_t(t0, g.n[0]), c1 = cell_from_t(t1, g.n[1]), c2 = cell_from_t(t2, g.n[2]);
       // cell of the particle's bin in the output layout
       int ox = sx, oy = sy, oz = sz;
       int obin = s;
       int64_t dest = i;
       bool write_ok = valid;
       if (SCATTER) {
-        const int j = valid ? slot_of(g, sx, sy, sz, c[0], c[1], c[2]) : -1;
+        const int j = valid ? slot_of<BCM>(g, sx, sy, sz, c0, c1, c2) : -1;
         if (valid && j < 0) {
           flags |= ERRF_SCATTER;
           write_ok = false;
@@ -228,10 +227,10 @@ __global__ void __launch_bounds__(256, 4) k_step(StepArgs a) {
         rbase = __shfl_sync(kFull, rbase, leader);
         __syncwarp();
         if (write_ok) {
-          ox = c[0];
-          oy = c[1];
-          oz = c[2];
-          obin = bin_of_cell(g, a.bg, ox, oy, oz);
+          ox = c0;
+          oy = c1;
+          oz = c2;
+          obin = bin_of_cell<SH>(g, a.bg, ox, oy, oz);
           dest = a.off_new[obin] + (int64_t)a.slot_base[(int64_t)j * nbins + s] + rbase + __popc(peers & lanemask_lt());
           if (dest < 0 || dest >= a.n) {
             flags |= ERRF_SCATTER;
@@ -242,67 +241,84 @@ __global__ void __launch_bounds__(256, 4) k_step(StepArgs a) {
       if (ADVANCE) {
         const float d = dp;
         const float tau = a.p.tau_c * d * d;
-        const float inv_tau = __frcp_rn(tau);
+        const float inv_tau = rcp_approx(tau);
         const float mw = a.p.mass_c * d * d * d * wp;
+        const float dt = a.dt;
+        const float gx = a.p.g[0], gy = a.p.g[1], gz = a.p.g[2];
         for (int sub = 0; sub < a.nsteps; ++sub) {
           if (sub > 0) {
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-              t[ax] = cell_coord(xp[ax], g.lo[ax], g.ih[ax]);
-              c[ax] = cell_from_t(t[ax], g.n[ax]);
-            }
+            t0 = cell_coord(xp0, g.lo[0], g.ih[0]);
+            t1 = cell_coord(xp1, g.lo[1], g.ih[1]);
+            t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
+            c0 = cell_from_t(t0, g.n[0]);
+            c1 = cell_from_t(t1, g.n[1]);
+            c2 = cell_from_t(t2, g.n[2]);
           }
-          Stencil st;
           int ix, iy, iz;
-          stencil_axis(t[0], g.n[0], ix, st.fx);
-          stencil_axis(t[1], g.n[1], iy, st.fy);
-          stencil_axis(t[2], g.n[2], iz, st.fz);
-          st.wx = ix + 1;
-          st.wy = iy + 1;
-          st.wz = window_z(g, iz);
-          if (st.wz < 0 || st.wz + 1 >= g.wnz) {
+          float fx, fy, fz;
+          stencil_from_cell(t0, c0, ix, fx);
+          stencil_from_cell(t1, c1, iy, fy);
+          stencil_from_cell(t2, c2, iz, fz);
+          int wz = window_z(g, iz);
+          if (wz < 0 || wz + 1 >= g.wnz) {
             if (valid) flags |= ERRF_WINDOW;
-            st.wz = st.wz < 0 ? 0 : g.wnz - 2;
+            wz = wz < 0 ? 0 : g.wnz - 2;
           }
-          const float4 uf = trilinear(g, a.field, st);
-          const float sxv = uf.x - up[0], syv = uf.y - up[1], szv = uf.z - up[2];
-          const float Re = sqrtf(fmaf(sxv, sxv, fmaf(syv, syv, szv * szv))) * d * a.p.inv_nu;
-          const float f = drag_factor(a.p.drag_law, Re);
-          const float taue = tau * __frcp_rn(f);
-          const float h = a.dt * f * inv_tau;
-          const float ufa[3] = {uf.x, uf.y, uf.z};
-          float du[3];
+          const int pz = g.gy * g.gx;
+          const float4* fb = a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
+          const float4 c000 = __ldg(fb), c100 = __ldg(fb + 1);
+          const float4 c010 = __ldg(fb + g.gx), c110 = __ldg(fb + g.gx + 1);
+          const float4 c001 = __ldg(fb + pz), c101 = __ldg(fb + pz + 1);
+          const float4 c011 = __ldg(fb + pz + g.gx), c111 = __ldg(fb + pz + g.gx + 1);
+          const float4 uf = lerp4(lerp4(lerp4(c000, c100, fx), lerp4(c010, c110, fx), fy),
+                                  lerp4(lerp4(c001, c101, fx), lerp4(c011, c111, fx), fy), fz);
+          const float sxv = uf.x - up0, syv = uf.y - up1, szv = uf.z - up2;
+          const float Re = sqrt_approx(fmaf(sxv, sxv, fmaf(syv, syv, szv * szv))) * d * a.p.inv_nu;
+          // C-2 Schiller-Naumann (branch-free): 1 + 0.15 Re^0.687 (Re <= 1000) or 0.44 Re / 24
+          float f = 1.0f + 0.15f * exp2f(0.687f * __log2f(Re));
+          f = (Re <= 1000.0f) ? f : (0.44f / 24.0f) * Re;
+          f = (a.p.drag_law == ST_DRAG_STOKES) ? 1.0f : f;
+          const float taue = tau * rcp_approx(f);
+          const float h = dt * f * inv_tau;
+          float du0, du1, du2;
           if (a.p.integrator == ST_INT_EXPONENTIAL) {
             float E, M;
             exp_pair(h, E, M);
             const float tM = taue * M;
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-              const float us = fmaf(a.p.g[ax], taue, ufa[ax]);
-              const float rl = up[ax] - us;
-              du[ax] = fmaf(-M, rl, -a.p.g[ax] * a.dt);
-              xp[ax] = fmaf(tM, rl, fmaf(us, a.dt, xp[ax]));
-              up[ax] = fmaf(E, rl, us);
-            }
+            const float us0 = fmaf(gx, taue, uf.x), us1 = fmaf(gy, taue, uf.y), us2 = fmaf(gz, taue, uf.z);
+            const float r0 = up0 - us0, r1 = up1 - us1, r2 = up2 - us2;
+            du0 = fmaf(-M, r0, -gx * dt);
+            du1 = fmaf(-M, r1, -gy * dt);
+            du2 = fmaf(-M, r2, -gz * dt);
+            xp0 = fmaf(tM, r0, fmaf(us0, dt, xp0));
+            xp1 = fmaf(tM, r1, fmaf(us1, dt, xp1));
+            xp2 = fmaf(tM, r2, fmaf(us2, dt, xp2));
+            up0 = fmaf(E, r0, us0);
+            up1 = fmaf(E, r1, us1);
+            up2 = fmaf(E, r2, us2);
           } else {
-            const float inv1h = __frcp_rn(1.0f + h);
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-              const float un = (up[ax] + h * ufa[ax] + a.dt * a.p.g[ax]) * inv1h;
-              du[ax] = (un - up[ax]) - a.p.g[ax] * a.dt;
-              xp[ax] = fmaf(a.dt, un, xp[ax]);
-              up[ax] = un;
-            }
+            const float inv1h = rcp_approx(1.0f + h);
+            const float un0 = (up0 + h * uf.x + dt * gx) * inv1h;
+            const float un1 = (up1 + h * uf.y + dt * gy) * inv1h;
+            const float un2 = (up2 + h * uf.z + dt * gz) * inv1h;
+            du0 = (un0 - up0) - gx * dt;
+            du1 = (un1 - up1) - gy * dt;
+            du2 = (un2 - up2) - gz * dt;
+            xp0 = fmaf(dt, un0, xp0);
+            xp1 = fmaf(dt, un1, xp1);
+            xp2 = fmaf(dt, un2, xp2);
+            up0 = un0;
+            up1 = un1;
+            up2 = un2;
           }
           if (a.p.two_way) {
-            // deposit -w m du into the start cell: the largest group of lanes with
-            // equal cells (cell-sorted warps) is reduced in registers, the rest red
-            // directly; one red.global.add.v4.f32 per group
-            const int az = acc_z(g, c[2]);
+            // deposit -w m du into the start cell: the group of lanes sharing lane 0's
+            // cell (cell-sorted warps) is reduced in registers, the rest red directly
+            const int az = acc_z(g, c2);
             if (valid && az < 0) flags |= ERRF_WINDOW;
             const bool dep = valid && az >= 0;
-            const int ckey = dep ? (az * g.n[1] + c[1]) * g.n[0] + c[0] : -1 - lane;
-            float ja = -mw * du[0], jb = -mw * du[1], jc = -mw * du[2];
+            const int ckey = dep ? (az * g.n[1] + c1) * g.n[0] + c0 : -1 - lane;
+            const float ja = -mw * du0, jb = -mw * du1, jc = -mw * du2;
             const unsigned peers = __match_any_sync(kFull, ckey);
             const int lead = __shfl_sync(kFull, ckey, 0);
             const unsigned major = __shfl_sync(kFull, peers, 0);
@@ -316,37 +332,40 @@ __global__ void __launch_bounds__(256, 4) k_step(StepArgs a) {
               red_add_v4(a.acc + ckey, ja, jb, jc);
             }
           }
-#pragma unroll
-          for (int ax = 0; ax < 3; ++ax)
-            if (apply_bc(g.bc[ax], g.lo[ax], g.hi[ax], g.L[ax], xp[ax], up[ax]) && valid) flags |= ERRF_CFL;
+          bool bad = false;
+          bad |= apply_bc(periodic<BCM>(g, 0) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[0], g.hi[0], g.L[0], xp0, up0);
+          bad |= apply_bc(periodic<BCM>(g, 1) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[1], g.hi[1], g.L[1], xp1, up1);
+          bad |= apply_bc(periodic<BCM>(g, 2) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[2], g.hi[2], g.L[2], xp2, up2);
+          if (bad && valid) flags |= ERRF_CFL;
         }
       }
       // slot histogram of the end position w.r.t. the output bin (next rebin's input)
       {
-        int e[3];
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) e[ax] = cell_from_t(cell_coord(xp[ax], g.lo[ax], g.ih[ax]), g.n[ax]);
-        const int j2 = write_ok ? slot_of(g, ox, oy, oz, e[0], e[1], e[2]) : -1;
+        const int e0 = cell_from_t(cell_coord(xp0, g.lo[0], g.ih[0]), g.n[0]);
+        const int e1 = cell_from_t(cell_coord(xp1, g.lo[1], g.ih[1]), g.n[1]);
+        const int e2 = cell_from_t(cell_coord(xp2, g.lo[2], g.ih[2]), g.n[2]);
+        const int j2 = write_ok ? slot_of<BCM>(g, ox, oy, oz, e0, e1, e2) : -1;
         if (write_ok && j2 < 0) farflag = 1;
         const long long hkey = (write_ok && j2 >= 0) ? (long long)j2 * nbins + obin : -1 - lane;
         const unsigned peers = __match_any_sync(kFull, hkey);
         if (hkey >= 0 && (peers & lanemask_lt()) == 0) atomicAdd(a.hist_next + hkey, __popc(peers));
         // chunk movers w.r.t. the output bins (the algorithmic rebin traffic)
-        const bool mover = write_ok && (div_cc(a.bg, e[0], g.cc) != div_cc(a.bg, ox, g.cc) ||
-                                        div_cc(a.bg, e[1], g.cc) != div_cc(a.bg, oy, g.cc) ||
-                                        div_cc(a.bg, e[2], g.cc) != div_cc(a.bg, oz, g.cc));
+        const bool mover = write_ok && ((dcc<SH>(e0, cc) != dcc<SH>(ox, cc)) | (dcc<SH>(e1, cc) != dcc<SH>(oy, cc)) |
+                                        (dcc<SH>(e2, cc) != dcc<SH>(oz, cc)));
         movers += mover ? 1u : 0u;
       }
       if (write_ok) {
         if (SCATTER) {
-          a.B.x[dest] = xp[0]; a.B.x[cap + dest] = xp[1]; a.B.x[2 * cap + dest] = xp[2];
-          a.B.u[dest] = up[0]; a.B.u[cap + dest] = up[1]; a.B.u[2 * cap + dest] = up[2];
-          a.B.d[dest] = dp;
-          a.B.w[dest] = wp;
-          a.B.id[dest] = pid;
+          // the id is only carried: load it late to keep it out of the live range
+          const unsigned long long pid = __ldcs(reinterpret_cast<const unsigned long long*>(a.A.id) + i);
+          __stcs(a.B.x + dest, xp0); __stcs(a.B.x + cap + dest, xp1); __stcs(a.B.x + 2 * cap + dest, xp2);
+          __stcs(a.B.u + dest, up0); __stcs(a.B.u + cap + dest, up1); __stcs(a.B.u + 2 * cap + dest, up2);
+          __stcs(a.B.d + dest, dp);
+          __stcs(a.B.w + dest, wp);
+          __stcs(reinterpret_cast<unsigned long long*>(a.B.id) + dest, pid);
         } else if (ADVANCE) {
-          a.A.x[i] = xp[0]; a.A.x[cap + i] = xp[1]; a.A.x[2 * cap + i] = xp[2];
-          a.A.u[i] = up[0]; a.A.u[cap + i] = up[1]; a.A.u[2 * cap + i] = up[2];
+          __stcs(a.A.x + i, xp0); __stcs(a.A.x + cap + i, xp1); __stcs(a.A.x + 2 * cap + i, xp2);
+          __stcs(a.A.u + i, up0); __stcs(a.A.u + cap + i, up1); __stcs(a.A.u + 2 * cap + i, up2);
         }
       }
     }
@@ -384,11 +403,11 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
     const int sy = axis_step(dy, -oy, g.n[1], g.bc[1], ok);
     const int sz = axis_step(dz, -oz, g.n[2], g.bc[2], ok);
     if (ok) {
-      const int kz = div_cc(bg, sz, g.cc);
-      ok = kz >= kz_lo && kz < kz_hi &&                    // source on this rank
-           slot_of(g, sx, sy, sz, dx, dy, dz) == j;          // canonical (no duplicate)
+      const int kz = sz / g.cc;
+      ok = kz >= kz_lo && kz < kz_hi &&                        // source on this rank
+           slot_of<-1>(g, sx, sy, sz, dx, dy, dz) == j;          // canonical (no duplicate)
     }
-    key[j] = ok ? bin_of_cell(g, bg, sx, sy, sz) : 0x7fffffff;
+    key[j] = ok ? bin_of_cell<0>(g, bg, sx, sy, sz) : 0x7fffffff;
     cnt[j] = ok ? cnt_base[(int64_t)j * nbins + key[j]] : 0;
   }
   // stable order = ascending source bin: base of source q = sum of the counts of
@@ -444,7 +463,7 @@ __global__ void k_bin_keys(Geom g, BinGeom bg, const float* __restrict__ x, int6
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int c[3];
     for (int ax = 0; ax < 3; ++ax) c[ax] = cell_from_t(cell_coord(x[ax * xs + i], g.lo[ax], g.ih[ax]), g.n[ax]);
-    int b = bin_of_cell(g, bg, c[0], c[1], c[2]);
+    int b = bin_of_cell<0>(g, bg, c[0], c[1], c[2]);
     if (b < 0 || b >= bg.nbins) {   // outside this rank's bins (multi-GPU: migrates first)
       atomicOr(err, ERRF_WINDOW);
       b = b < 0 ? 0 : bg.nbins - 1;
@@ -455,28 +474,41 @@ __global__ void k_bin_keys(Geom g, BinGeom bg, const float* __restrict__ x, int6
 
 inline unsigned blocks_for(int64_t n, int bs = 256) { return (unsigned)((n + bs - 1) / bs); }
 
-}  // namespace
-
-int step_occupancy_grid(bool scatter, bool advance) {
-  static int cache[4] = {0, 0, 0, 0};
-  const int idx = (scatter ? 2 : 0) + (advance ? 1 : 0);
-  if (cache[idx]) return cache[idx];
-  int nsm = 148, dev = 0, per = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (scatter && advance) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_step<true, true>, 256, 0);
-  else if (scatter) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_step<true, false>, 256, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_step<false, true>, 256, 0);
-  cache[idx] = nsm * (per > 0 ? per : 1);
-  return cache[idx];
+template <bool S, bool A, int BCM, int SH>
+int launch_variant(const StepArgs& a, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    int nsm = 148, dev = 0, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_step<S, A, BCM, SH>, 256, 0);
+    grid = nsm * (per > 0 ? per : 1);
+  }
+  k_step<S, A, BCM, SH><<<grid, 256, 0, s>>>(a);
+  return 1;
 }
 
+template <bool S, bool A>
+int launch_mode(const StepArgs& a, cudaStream_t s) {
+  const int bcm = (a.g.bc[0] == ST_BC_PERIODIC ? 1 : 0) | (a.g.bc[1] == ST_BC_PERIODIC ? 2 : 0) |
+                  (a.g.bc[2] == ST_BC_PERIODIC ? 4 : 0);
+  if (a.g.cc == 8) {
+    switch (bcm) {
+      case 0: return launch_variant<S, A, 0, 3>(a, s);
+      case 7: return launch_variant<S, A, 7, 3>(a, s);
+      case 3: return launch_variant<S, A, 3, 3>(a, s);
+      default: return launch_variant<S, A, -1, 3>(a, s);
+    }
+  }
+  return launch_variant<S, A, -1, 0>(a, s);
+}
+
+}  // namespace
+
 int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s) {
-  const int grid = step_occupancy_grid(scatter, advance);
-  if (scatter && advance) k_step<true, true><<<grid, 256, 0, s>>>(a);
-  else if (scatter) k_step<true, false><<<grid, 256, 0, s>>>(a);
-  else k_step<false, true><<<grid, 256, 0, s>>>(a);
-  return 1;
+  if (scatter && advance) return launch_mode<true, true>(a, s);
+  if (scatter) return launch_mode<true, false>(a, s);
+  return launch_mode<false, true>(a, s);
 }
 
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s) {

@@ -16,10 +16,10 @@ __device__ __forceinline__ float cell_coord(float x, float lo, float ih) {
   return __fmul_rn(__fsub_rn(x, lo), ih);
 }
 __device__ __forceinline__ int cell_from_t(float t, int n) {
-  float f = floorf(t);
-  if (!(f >= 0.0f)) return 0;     // also NaN
-  if (f >= (float)n) return n - 1;
-  return (int)f;
+  // cvt.rmi (floor; NaN -> 0, saturating) then clamp to [0, n-1]: identical to
+  // "floor; <0 or NaN -> 0; >= n -> n-1" of the contract
+  const int f = __float2int_rd(t);
+  return min(max(f, 0), n - 1);
 }
 
 __device__ __forceinline__ int64_t cell_linear(const Geom& g, int cx, int cy, int cz) {
