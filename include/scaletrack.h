@@ -147,8 +147,11 @@ st_status st_set_fluid_field(st_ctx* ctx, const float* u);
  * on the GPUs").  x,u: [3][n]; d: [n] diameters (> 0); w: [n] parcel
  * multiplicity or NULL = 1; id: [n] or NULL = auto ((rank<<40)+counter).
  * Positions must satisfy lo <= x <= hi per axis, else ST_ERR_OUT_OF_DOMAIN and
- * nothing is appended.  With nranks > 1 a rank injects only particles whose cell
- * lies in its own z-slab (st_get_layout z0..z1), else ST_ERR_OUT_OF_DOMAIN. */
+ * nothing is appended.  With nranks > 1 the call is collective (every rank calls
+ * it, n may be 0) and a rank injects only particles whose cell lies in its own
+ * z-slab (st_get_layout z0..z1), else ST_ERR_OUT_OF_DOMAIN.  st_get_particles
+ * and st_get_count are collective too when nranks > 1 (they may execute a due
+ * rebin, which exchanges movers). */
 st_status st_inject(st_ctx* ctx, int64_t n, const float* x, const float* u,
                     const float* d, const float* w, const uint64_t* id);
 

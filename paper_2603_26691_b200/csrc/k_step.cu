@@ -82,6 +82,20 @@ __device__ __forceinline__ int bin_of_cell(const Geom& g, const BinGeom& b, int 
   return chunk * b.cc3 + lc;
 }
 
+// virtual bin of a cell (x,y) of a neighbour plane: the receiver's bin order
+template <int SH>
+__device__ __forceinline__ int vbin_of_cell(const Geom& g, int cx, int cy, int cc) {
+  const int kx = dcc<SH>(cx, cc), ky = dcc<SH>(cy, cc);
+  return ((ky * g.NC[0] + kx) * cc + (cy - ky * cc)) * cc + (cx - kx * cc);
+}
+__device__ __forceinline__ void cell_of_vbin(const Geom& g, int v, int& cx, int& cy) {
+  const int cc = g.cc;
+  const int lx = v % cc, ly = (v / cc) % cc;
+  const int kk = v / (cc * cc);
+  cx = (kk % g.NC[0]) * cc + lx;
+  cy = (kk / g.NC[0]) * cc + ly;
+}
+
 // (amortised: once per bin per item / per prep thread)
 __device__ __forceinline__ void cell_of_bin(const Geom& g, const BinGeom& b, int bin, int& cx, int& cy, int& cz) {
   const int cc = g.cc;
@@ -210,6 +224,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
       int obin = s;
       int64_t dest = i;
       bool write_ok = valid;
+      int vside = -1;   // >= 0: mover into a neighbour rank's plane (multi-GPU scatter)
       if (SCATTER) {
         const int j = valid ? slot_of<BCM>(g, sx, sy, sz, c0, c1, c2) : -1;
         if (valid && j < 0) {
@@ -230,11 +245,21 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
           ox = c0;
           oy = c1;
           oz = c2;
-          obin = bin_of_cell<SH>(g, a.bg, ox, oy, oz);
-          dest = a.off_new[obin] + (int64_t)a.slot_base[(int64_t)j * nbins + s] + rbase + __popc(peers & lanemask_lt());
-          if (dest < 0 || dest >= a.n) {
-            flags |= ERRF_SCATTER;
-            write_ok = false;
+          const int64_t within = (int64_t)a.slot_base[(int64_t)j * nbins + s] + rbase + __popc(peers & lanemask_lt());
+          vside = (c2 == a.bg.vz[0]) ? 0 : ((c2 == a.bg.vz[1]) ? 1 : -1);
+          if (vside >= 0) {
+            dest = a.voff[vside][vbin_of_cell<SH>(g, c0, c1, cc)] + within;
+            if (dest < 0 || dest >= a.scap) {
+              flags |= ERRF_SCATTER;
+              write_ok = false;
+            }
+          } else {
+            obin = bin_of_cell<SH>(g, a.bg, ox, oy, oz);
+            dest = a.off_new[obin] + within;
+            if (dest < 0 || dest >= a.n) {
+              flags |= ERRF_SCATTER;
+              write_ok = false;
+            }
           }
         }
       }
@@ -344,9 +369,10 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
         const int e0 = cell_from_t(cell_coord(xp0, g.lo[0], g.ih[0]), g.n[0]);
         const int e1 = cell_from_t(cell_coord(xp1, g.lo[1], g.ih[1]), g.n[1]);
         const int e2 = cell_from_t(cell_coord(xp2, g.lo[2], g.ih[2]), g.n[2]);
-        const int j2 = write_ok ? slot_of<BCM>(g, ox, oy, oz, e0, e1, e2) : -1;
-        if (write_ok && j2 < 0) farflag = 1;
-        const long long hkey = (write_ok && j2 >= 0) ? (long long)j2 * nbins + obin : -1 - lane;
+        const bool here = write_ok && vside < 0;   // movers to a neighbour are counted by the receiver
+        const int j2 = here ? slot_of<BCM>(g, ox, oy, oz, e0, e1, e2) : -1;
+        if (here && j2 < 0) farflag = 1;
+        const long long hkey = (here && j2 >= 0) ? (long long)j2 * nbins + obin : -1 - lane;
         const unsigned peers = __match_any_sync(kFull, hkey);
         if (hkey >= 0 && (peers & lanemask_lt()) == 0) atomicAdd(a.hist_next + hkey, __popc(peers));
         // chunk movers w.r.t. the output bins (the algorithmic rebin traffic)
@@ -358,11 +384,13 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
         if (SCATTER) {
           // the id is only carried: load it late to keep it out of the live range
           const unsigned long long pid = __ldcs(reinterpret_cast<const unsigned long long*>(a.A.id) + i);
-          __stcs(a.B.x + dest, xp0); __stcs(a.B.x + cap + dest, xp1); __stcs(a.B.x + 2 * cap + dest, xp2);
-          __stcs(a.B.u + dest, up0); __stcs(a.B.u + cap + dest, up1); __stcs(a.B.u + 2 * cap + dest, up2);
-          __stcs(a.B.d + dest, dp);
-          __stcs(a.B.w + dest, wp);
-          __stcs(reinterpret_cast<unsigned long long*>(a.B.id) + dest, pid);
+          const Store& o = vside < 0 ? a.B : a.sbuf[vside];
+          const int64_t oc = vside < 0 ? cap : a.scap;
+          __stcs(o.x + dest, xp0); __stcs(o.x + oc + dest, xp1); __stcs(o.x + 2 * oc + dest, xp2);
+          __stcs(o.u + dest, up0); __stcs(o.u + oc + dest, up1); __stcs(o.u + 2 * oc + dest, up2);
+          __stcs(o.d + dest, dp);
+          __stcs(o.w + dest, wp);
+          __stcs(reinterpret_cast<unsigned long long*>(o.id) + dest, pid);
         } else if (ADVANCE) {
           __stcs(a.A.x + i, xp0); __stcs(a.A.x + cap + i, xp1); __stcs(a.A.x + 2 * cap + i, xp2);
           __stcs(a.A.u + i, up0); __stcs(a.A.u + cap + i, up1); __stcs(a.A.u + 2 * cap + i, up2);
@@ -383,12 +411,20 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
 // Per destination bin d: sources s = d - delta over the 27 deltas (canonical,
 // deduplicated), in ascending s; base[j][s] = running sum; new_cnt[d] = total.
 // The slot-major layout makes consecutive threads touch consecutive words.
+// Destinations d >= nbins are the virtual bins of the neighbour planes (multi-GPU):
+// d = nbins + side * nvb + v.
 __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cnt_base, uint32_t* __restrict__ new_cnt) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= nbins) return;
+  if (d >= nbins + 2 * bg.nvb) return;
   int dx, dy, dz;
-  cell_of_bin(g, bg, d, dx, dy, dz);
-  if (dx >= g.n[0] || dy >= g.n[1] || dz >= g.n[2]) {   // ragged chunk: no such cell
+  if (d < nbins) {
+    cell_of_bin(g, bg, d, dx, dy, dz);
+  } else {
+    const int side = (d - nbins) / bg.nvb;
+    cell_of_vbin(g, d - nbins - side * bg.nvb, dx, dy);
+    dz = bg.vz[side];
+  }
+  if (dx >= g.n[0] || dy >= g.n[1] || dz < 0 || dz >= g.n[2]) {   // ragged chunk / no neighbour
     new_cnt[d] = 0;
     return;
   }
@@ -422,6 +458,57 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
     total += (uint32_t)cnt[q];
   }
   new_cnt[d] = total;
+}
+
+// Arrival counts from the neighbours land after the local particles of the
+// boundary-plane bins (C-16: kept first, then arrivals).
+__global__ void k_vcombine(Geom g, BinGeom bg, uint32_t* __restrict__ new_cnt, const uint32_t* __restrict__ rcnt_dn,
+                           const uint32_t* __restrict__ rcnt_up, uint32_t* __restrict__ kept_dn,
+                           uint32_t* __restrict__ kept_up, int oz0, int oz1) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= bg.nvb) return;
+  int x, y;
+  cell_of_vbin(g, v, x, y);
+  if (x >= g.n[0] || y >= g.n[1]) return;
+  const int db = bin_of_cell<0>(g, bg, x, y, oz0);
+  kept_dn[v] = new_cnt[db];
+  new_cnt[db] += rcnt_dn[v];
+  const int dt = bin_of_cell<0>(g, bg, x, y, oz1 - 1);
+  kept_up[v] = new_cnt[dt];
+  new_cnt[dt] += rcnt_up[v];
+}
+
+// Insert the arrivals of one side into B and count their slots for the next rebin.
+__global__ void k_insert(InsertArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.count) return;
+  int lo = 0, hi = a.bg.nvb;   // last v with roff[v] <= i
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.roff[mid] <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  const int v = lo;
+  int x, y;
+  cell_of_vbin(a.g, v, x, y);
+  const int d = bin_of_cell<0>(a.g, a.bg, x, y, a.plane);
+  const int64_t dest = a.off_new[d] + a.kept[v] + (i - a.roff[v]);
+  const Store& r = a.rbuf;
+  const int64_t rc = a.rcap, cap = a.cap;
+  float xv[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    xv[ax] = r.x[ax * rc + i];
+    a.B.x[ax * cap + dest] = xv[ax];
+    a.B.u[ax * cap + dest] = r.u[ax * rc + i];
+  }
+  a.B.d[dest] = r.d[i];
+  a.B.w[dest] = r.w[i];
+  a.B.id[dest] = r.id[i];
+  int e[3];
+  for (int ax = 0; ax < 3; ++ax) e[ax] = cell_from_t(cell_coord(xv[ax], a.g.lo[ax], a.g.ih[ax]), a.g.n[ax]);
+  const int j = slot_of<-1>(a.g, x, y, a.plane, e[0], e[1], e[2]);
+  if (j < 0) *(volatile int*)a.far = 1;
+  else atomicAdd(a.hist_next + (int64_t)j * a.nbins + d, 1);
 }
 
 __global__ void k_hist_stay(const int64_t* __restrict__ off, int nbins, int* __restrict__ hist_row13) {
@@ -512,7 +599,20 @@ int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s) {
 }
 
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s) {
-  k_rebin_prep<<<blocks_for(bg.nbins, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt);
+  k_rebin_prep<<<blocks_for((int64_t)bg.nbins + 2 * bg.nvb, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt);
+  return 1;
+}
+
+int launch_vcombine(const Geom& g, const BinGeom& bg, uint32_t* new_cnt, const uint32_t* rcnt_dn, const uint32_t* rcnt_up,
+                    uint32_t* kept_dn, uint32_t* kept_up, int oz0, int oz1, cudaStream_t s) {
+  if (bg.nvb <= 0) return 0;
+  k_vcombine<<<blocks_for(bg.nvb), 256, 0, s>>>(g, bg, new_cnt, rcnt_dn, rcnt_up, kept_dn, kept_up, oz0, oz1);
+  return 1;
+}
+
+int launch_insert(const InsertArgs& a, cudaStream_t s) {
+  if (a.count <= 0) return 0;
+  k_insert<<<blocks_for(a.count), 256, 0, s>>>(a);
   return 1;
 }
 

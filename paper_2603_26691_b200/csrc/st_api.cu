@@ -60,6 +60,17 @@ struct st_ctx {
   int* h_far = nullptr;                     // mapped pinned: next rebin needs the general sort
   int* d_far = nullptr;
   unsigned long long* d_movers = nullptr;   // chunk movers counted by the last step kernel
+  // multi-GPU fused rebin (virtual neighbour planes)
+  int64_t* voff[2] = {nullptr, nullptr};    // [nvb+1] offsets in the send buffers
+  uint32_t* rcnt[2] = {nullptr, nullptr};   // [nvb] arrival counts (0: from below, 1: from above)
+  int64_t* roff[2] = {nullptr, nullptr};    // [nvb+1]
+  uint32_t* kept[2] = {nullptr, nullptr};   // [nvb]
+  Store sbuf[2], rbuf[2];
+  int64_t scap = 0;
+  int64_t* h_tot = nullptr;                 // pinned: send_lo, send_hi, recv_dn, recv_up
+  int* h_farg = nullptr;                    // pinned: global far flag
+  int* d_farg = nullptr;
+  cudaEvent_t ev_tot{};
   cudaEvent_t ev_step_done{};
 
   // fields (double buffer)
@@ -256,6 +267,10 @@ static void build_geometry(st_ctx* c) {
   c->bg.sh = -1;
   for (int s = 0; s < 16; ++s)
     if ((1 << s) == g.cc) c->bg.sh = s;
+  c->bg.nvb = G > 1 ? g.NC[0] * g.NC[1] * g.cc * g.cc : 0;
+  const bool pz = f.bc[2] == ST_BC_PERIODIC;
+  c->bg.vz[0] = G > 1 ? (c->z0 > 0 ? c->z0 - 1 : (pz ? g.n[2] - 1 : -1)) : -1;
+  c->bg.vz[1] = G > 1 ? (c->z1 < g.n[2] ? c->z1 : (pz ? 0 : -1)) : -1;
   // radix key = local bin (< nbins); multi-GPU pre-migration key = global chunk
   const int64_t kmax = std::max<int64_t>(c->bg.nbins, (int64_t)g.NC[0] * g.NC[1] * g.NC[2]);
   int bits = 1;
@@ -275,8 +290,8 @@ static void build_geometry(st_ctx* c) {
   p.two_way = f.coupling == ST_TWO_WAY;
 }
 
-static st_status alloc_store(st_ctx* c, Store& s) {
-  const int64_t cap = c->cap > 0 ? c->cap : 1;
+static st_status alloc_store(st_ctx* c, Store& s, int64_t cap_in) {
+  const int64_t cap = cap_in > 0 ? cap_in : 1;
   const size_t bytes = (size_t)cap * (6 * sizeof(float) + 2 * sizeof(float) + sizeof(uint64_t)) + 1024;
   void* b = nullptr;
   ST_CUDA(c, cudaMalloc(&b, bytes));
@@ -308,7 +323,7 @@ static st_status init_impl(st_ctx* c) {
   }
   ST_CUDA(c, cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking));
   for (int i = 0; i < 2; ++i) {
-    st_status s = alloc_store(c, c->S[i]);
+    st_status s = alloc_store(c, c->S[i], c->cap);
     if (s) return s;
     ST_CUDA(c, cudaMalloc(&c->key[i], (size_t)(c->cap > 0 ? c->cap : 1) * sizeof(int32_t)));
     ST_CUDA(c, cudaMalloc(&c->field[i], (size_t)g.wnz * g.gy * g.gx * sizeof(float4)));
@@ -337,7 +352,26 @@ static st_status init_impl(st_ctx* c) {
     ST_CUDA(c, cudaMalloc(&c->n_items[i], sizeof(int)));
     ST_CUDA(c, cudaMalloc(&c->hist[i], nb * 27 * sizeof(int)));
   }
-  ST_CUDA(c, cudaMalloc(&c->new_cnt, (nb + 1) * sizeof(uint32_t)));
+  ST_CUDA(c, cudaMalloc(&c->new_cnt, (nb + 2 * (size_t)c->bg.nvb + 1) * sizeof(uint32_t)));
+  if (c->bg.nvb > 0) {
+    const size_t nv = (size_t)c->bg.nvb;
+    c->scap = std::max<int64_t>(1 << 20, c->cap / 16);
+    for (int i = 0; i < 2; ++i) {
+      ST_CUDA(c, cudaMalloc(&c->voff[i], (nv + 1) * sizeof(int64_t)));
+      ST_CUDA(c, cudaMalloc(&c->rcnt[i], nv * sizeof(uint32_t)));
+      ST_CUDA(c, cudaMemset(c->rcnt[i], 0, nv * sizeof(uint32_t)));
+      ST_CUDA(c, cudaMalloc(&c->roff[i], (nv + 1) * sizeof(int64_t)));
+      ST_CUDA(c, cudaMalloc(&c->kept[i], nv * sizeof(uint32_t)));
+      st_status s2 = alloc_store(c, c->sbuf[i], c->scap);
+      if (s2) return s2;
+      s2 = alloc_store(c, c->rbuf[i], c->scap);
+      if (s2) return s2;
+    }
+    ST_CUDA(c, cudaHostAlloc(&c->h_tot, 4 * sizeof(int64_t), cudaHostAllocDefault));
+    ST_CUDA(c, cudaHostAlloc(&c->h_farg, sizeof(int), cudaHostAllocDefault));
+    ST_CUDA(c, cudaMalloc(&c->d_farg, sizeof(int)));
+    ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_tot, cudaEventDisableTiming));
+  }
   ST_CUDA(c, cudaMalloc(&c->item_flag, (nb + 1) * sizeof(uint32_t)));
   ST_CUDA(c, cudaMalloc(&c->item_pos, (nb + 2) * sizeof(int64_t)));
   ST_CUDA(c, cudaHostAlloc(&c->h_far, sizeof(int), cudaHostAllocMapped));
@@ -393,6 +427,18 @@ st_status st_destroy(st_ctx* c) {
   cudaFree(c->item_pos);
   if (c->h_far) cudaFreeHost(c->h_far);
   cudaFree(c->d_movers);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c->voff[i]);
+    cudaFree(c->rcnt[i]);
+    cudaFree(c->roff[i]);
+    cudaFree(c->kept[i]);
+    cudaFree(c->sbuf[i].base);
+    cudaFree(c->rbuf[i].base);
+  }
+  if (c->h_tot) cudaFreeHost(c->h_tot);
+  if (c->h_farg) cudaFreeHost(c->h_farg);
+  cudaFree(c->d_farg);
+  if (c->ev_tot) cudaEventDestroy(c->ev_tot);
   if (c->ev_step_done) cudaEventDestroy(c->ev_step_done);
   cudaFree(c->sc.hist);
   cudaFree(c->sc.offs);
@@ -479,13 +525,16 @@ st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const 
                     const uint64_t* id) {
   ST_ALIVE(c);
   if (n < 0) return fail(c, ST_ERR_INVALID_ARG, "n < 0");
-  if (n == 0) return ST_OK;
-  if (!x || !u || !d) return fail(c, ST_ERR_INVALID_ARG, "x, u and d are required");
-  if (c->n + n > c->cap) return fail(c, ST_ERR_CAPACITY, "store capacity exceeded");
   {
     st_status fr = flush_rebin(c);   // the contract sorted the store before this append
     if (fr) return fr;
   }
+  if (n == 0) {
+    if (c->comm) c->binned = false;   // collective: every rank leaves the binned state together
+    return ST_OK;
+  }
+  if (!x || !u || !d) return fail(c, ST_ERR_INVALID_ARG, "x, u and d are required");
+  if (c->n + n > c->cap) return fail(c, ST_ERR_CAPACITY, "store capacity exceeded");
   Store s = c->S[c->cur];
   const int64_t o = c->n, cap = c->cap;
   auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
@@ -547,6 +596,11 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.err = c->d_err;
   a.far = c->d_far;
   a.movers = c->d_movers;
+  for (int k = 0; k < 2; ++k) {
+    a.voff[k] = c->voff[k];
+    a.sbuf[k] = c->sbuf[k];
+  }
+  a.scap = c->scap;
   return a;
 }
 
@@ -600,25 +654,104 @@ static st_status general_rebin(st_ctx* c) {
 
 // Neighbour-slot scatter from the current layout into the other buffer; fused
 // with the advance when `advance` (the field/accumulator must be set up).
-static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps) {
+// nranks > 1: the movers into the neighbour planes are scattered into send
+// buffers, the counts are exchanged before the layout scan and the arrivals are
+// inserted after the kernel (C-16); the "far" flag is reduced over all ranks and
+// any rank's far particle makes every rank take the general path (*fell_back).
+static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bool* fell_back) {
+  *fell_back = false;
   const Geom& g = c->g;
   const int nlay = 1 - c->lay;
+  const int nb = c->bg.nbins, nv = c->bg.nvb;
   ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
   int nl = launch_rebin_prep(g, c->bg, c->hist[c->hcur], c->new_cnt, c->cs);
-  nl += launch_exclusive_scan_u32(c->new_cnt, c->bg.nbins, c->off[nlay], c->sc.partial, c->cs);
-  nl += launch_items(c->off[nlay], c->bg.nbins, c->item_flag, c->item_pos, c->sc.partial, c->items[nlay],
-                     c->n_items[nlay], c->cs);
-  ST_CUDA(c, cudaMemsetAsync(c->hist[1 - c->hcur], 0, (size_t)c->bg.nbins * 27 * sizeof(int), c->cs));
+  st_status s;
+  if (c->comm) {
+    if ((s = check_launch(c, nl))) return s;
+    nl = 0;
+    int farv = (*c->h_far || !c->binned) ? 1 : 0;
+    ST_CUDA(c, cudaMemcpyAsync(c->d_farg, &farv, sizeof(int), cudaMemcpyHostToDevice, c->cs));
+    std::string why;
+    if (comm_rebin_counts(c->comm, c->new_cnt + nb, c->new_cnt + nb + nv, c->rcnt[0], c->rcnt[1], nv, c->d_farg,
+                          g.bc[2] == ST_BC_PERIODIC, c->cs, why))
+      return fail(c, ST_ERR_NCCL, why);
+    nl += launch_vcombine(g, c->bg, c->new_cnt, c->rcnt[0], c->rcnt[1], c->kept[0], c->kept[1], c->z0, c->z1, c->cs);
+    nl += launch_exclusive_scan_u32(c->new_cnt + nb, nv, c->voff[0], c->sc.partial, c->cs);
+    nl += launch_exclusive_scan_u32(c->new_cnt + nb + nv, nv, c->voff[1], c->sc.partial, c->cs);
+    nl += launch_exclusive_scan_u32(c->rcnt[0], nv, c->roff[0], c->sc.partial, c->cs);
+    nl += launch_exclusive_scan_u32(c->rcnt[1], nv, c->roff[1], c->sc.partial, c->cs);
+    ST_CUDA(c, cudaMemcpyAsync(c->h_tot + 0, c->voff[0] + nv, sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
+    ST_CUDA(c, cudaMemcpyAsync(c->h_tot + 1, c->voff[1] + nv, sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
+    ST_CUDA(c, cudaMemcpyAsync(c->h_tot + 2, c->roff[0] + nv, sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
+    ST_CUDA(c, cudaMemcpyAsync(c->h_tot + 3, c->roff[1] + nv, sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
+    ST_CUDA(c, cudaMemcpyAsync(c->h_farg, c->d_farg, sizeof(int), cudaMemcpyDeviceToHost, c->cs));
+    ST_CUDA(c, cudaEventRecord(c->ev_tot, c->cs));
+  }
+  nl += launch_exclusive_scan_u32(c->new_cnt, nb, c->off[nlay], c->sc.partial, c->cs);
+  nl += launch_items(c->off[nlay], nb, c->item_flag, c->item_pos, c->sc.partial, c->items[nlay], c->n_items[nlay],
+                     c->cs);
+  ST_CUDA(c, cudaMemsetAsync(c->hist[1 - c->hcur], 0, (size_t)nb * 27 * sizeof(int), c->cs));
   ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));
   c->timed_reb = true;
-  st_status s = check_launch(c, nl);
-  if (s) return s;
+  if ((s = check_launch(c, nl))) return s;
+  int64_t n_new = c->n;
+  if (c->comm) {
+    ST_CUDA(c, cudaEventSynchronize(c->ev_tot));
+    if (*c->h_farg) {
+      *fell_back = true;
+      return general_rebin(c);
+    }
+    for (int k = 0; k < 4; ++k)
+      if (c->h_tot[k] > c->scap) return fail(c, ST_ERR_CAPACITY, "migration buffer too small (more movers than cap/16)");
+    n_new = c->n - c->h_tot[0] - c->h_tot[1] + c->h_tot[2] + c->h_tot[3];
+    if (n_new > c->cap) return fail(c, ST_ERR_CAPACITY, "migration would exceed the store capacity");
+  }
   *c->h_far = 0;
   ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
   StepArgs a = step_args(c, dt, nsteps);
+  a.n = n_new;
   if (advance) ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
-  s = check_launch(c, launch_step(a, true, advance, c->cs));
-  if (s) return s;
+  if ((s = check_launch(c, launch_step(a, true, advance, c->cs)))) return s;
+  if (c->comm) {
+    std::string why;
+    if (comm_rebin_payload(c->comm, c->sbuf, c->scap, c->h_tot[0], c->h_tot[1], c->rbuf, c->scap, c->h_tot[2],
+                           c->h_tot[3], g.bc[2] == ST_BC_PERIODIC, c->cs, why))
+      return fail(c, ST_ERR_NCCL, why);
+    nl = 0;
+    for (int side = 0; side < 2; ++side) {
+      InsertArgs ia;
+      memset(&ia, 0, sizeof(ia));
+      ia.g = g;
+      ia.bg = c->bg;
+      ia.rbuf = c->rbuf[side];
+      ia.rcap = c->scap;
+      ia.count = c->h_tot[2 + side];
+      ia.roff = c->roff[side];
+      ia.kept = c->kept[side];
+      ia.plane = side == 0 ? c->z0 : c->z1 - 1;
+      ia.B = c->S[1 - c->cur];
+      ia.cap = c->cap;
+      ia.off_new = c->off[nlay];
+      ia.nbins = nb;
+      ia.hist_next = c->hist[1 - c->hcur];
+      ia.far = c->d_far;
+      ia.err = c->d_err;
+      nl += launch_insert(ia, c->cs);
+    }
+    if ((s = check_launch(c, nl))) return s;
+    c->mig_row.assign(c->cfg.nranks, 0);
+    const int G = c->cfg.nranks, r = c->cfg.rank;
+    const bool pz = g.bc[2] == ST_BC_PERIODIC;
+    const int up = (r + 1 < G) ? r + 1 : (pz ? 0 : -1), dn = (r > 0) ? r - 1 : (pz ? G - 1 : -1);
+    if (up >= 0) c->mig_row[up] += c->h_tot[1];
+    if (dn >= 0) c->mig_row[dn] += c->h_tot[0];
+    c->mig_row[r] = c->n - c->h_tot[0] - c->h_tot[1];
+    c->last_sent = c->h_tot[0] + c->h_tot[1];
+    c->last_recv = c->h_tot[2] + c->h_tot[3];
+    c->n = n_new;
+  } else {
+    c->mig_row[0] = c->n;
+  }
   if (advance) {
     ST_CUDA(c, cudaEventRecord(c->t_adv1, c->cs));
     c->timed_adv = true;
@@ -633,12 +766,14 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps) {
   return ST_OK;
 }
 
-// Execute a due rebin before the store is observed or appended to.
+// Execute a due rebin before the store is observed or appended to (collective
+// when nranks > 1).
 static st_status flush_rebin(st_ctx* c) {
   if (!c->rebin_due) return ST_OK;
   ST_CUDA(c, cudaEventSynchronize(c->ev_step_done));
-  if (!c->binned || c->comm || *c->h_far) return general_rebin(c);
-  return scatter_rebin(c, false, 0.0f, 0);
+  if (!c->binned || (!c->comm && *c->h_far)) return general_rebin(c);
+  bool fell_back = false;
+  return scatter_rebin(c, false, 0.0f, 0, &fell_back);
 }
 
 // ---------------------------------------------------------------- advance
@@ -660,10 +795,11 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
     // the rebin of the previous call (C-15), fused into this call when every
     // particle is still within one cell of its bin
     ST_CUDA(c, cudaEventSynchronize(c->ev_step_done));
-    if (c->binned && !c->comm && !*c->h_far) {
-      st = scatter_rebin(c, true, (float)dt, nsteps);
+    if (c->binned && (c->comm || !*c->h_far)) {
+      bool fell_back = false;
+      st = scatter_rebin(c, true, (float)dt, nsteps, &fell_back);
       if (st) return st;
-      done = true;
+      done = !fell_back;
     } else {
       st = general_rebin(c);
       if (st) return st;

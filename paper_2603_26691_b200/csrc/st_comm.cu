@@ -259,6 +259,61 @@ int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int6
   return 0;
 }
 
+namespace {
+void neighbours(const Comm* c, bool periodic, int& up, int& dn) {
+  const int G = c->nranks, r = c->rank;
+  up = (r + 1 < G) ? r + 1 : (periodic ? 0 : -1);
+  dn = (r > 0) ? r - 1 : (periodic ? G - 1 : -1);
+}
+
+int send_store(Comm* c, const Store& b, int64_t cap, int64_t n, int peer, std::string& why) {
+  for (int a = 0; a < 3; ++a) NCCK(ncclSend(b.x + a * cap, n, ncclFloat, peer, c->nc, c->ns), why);
+  for (int a = 0; a < 3; ++a) NCCK(ncclSend(b.u + a * cap, n, ncclFloat, peer, c->nc, c->ns), why);
+  NCCK(ncclSend(b.d, n, ncclFloat, peer, c->nc, c->ns), why);
+  NCCK(ncclSend(b.w, n, ncclFloat, peer, c->nc, c->ns), why);
+  NCCK(ncclSend(b.id, n, ncclUint64, peer, c->nc, c->ns), why);
+  return 0;
+}
+
+int recv_store(Comm* c, const Store& b, int64_t cap, int64_t n, int peer, std::string& why) {
+  for (int a = 0; a < 3; ++a) NCCK(ncclRecv(b.x + a * cap, n, ncclFloat, peer, c->nc, c->ns), why);
+  for (int a = 0; a < 3; ++a) NCCK(ncclRecv(b.u + a * cap, n, ncclFloat, peer, c->nc, c->ns), why);
+  NCCK(ncclRecv(b.d, n, ncclFloat, peer, c->nc, c->ns), why);
+  NCCK(ncclRecv(b.w, n, ncclFloat, peer, c->nc, c->ns), why);
+  NCCK(ncclRecv(b.id, n, ncclUint64, peer, c->nc, c->ns), why);
+  return 0;
+}
+}  // namespace
+
+int comm_rebin_counts(Comm* c, const uint32_t* vcnt_lo, const uint32_t* vcnt_hi, uint32_t* rcnt_dn, uint32_t* rcnt_up,
+                      int nvb, int* d_far, bool periodic, cudaStream_t s, std::string& why) {
+  int up, dn;
+  neighbours(c, periodic, up, dn);
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclAllReduce(d_far, d_far, 1, ncclInt32, ncclMax, c->nc, c->ns), why);
+  NCCK(ncclGroupStart(), why);
+  if (up >= 0) NCCK(ncclSend(vcnt_hi, nvb, ncclUint32, up, c->nc, c->ns), why);
+  if (dn >= 0) NCCK(ncclSend(vcnt_lo, nvb, ncclUint32, dn, c->nc, c->ns), why);
+  if (dn >= 0) NCCK(ncclRecv(rcnt_dn, nvb, ncclUint32, dn, c->nc, c->ns), why);
+  if (up >= 0) NCCK(ncclRecv(rcnt_up, nvb, ncclUint32, up, c->nc, c->ns), why);
+  NCCK(ncclGroupEnd(), why);
+  return join_out(c, s, why);
+}
+
+int comm_rebin_payload(Comm* c, const Store* sbuf, int64_t scap, int64_t send_lo, int64_t send_hi, const Store* rbuf,
+                       int64_t rcap, int64_t recv_dn, int64_t recv_up, bool periodic, cudaStream_t s, std::string& why) {
+  int up, dn;
+  neighbours(c, periodic, up, dn);
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclGroupStart(), why);
+  if (up >= 0 && send_hi > 0 && send_store(c, sbuf[1], scap, send_hi, up, why)) return 1;
+  if (dn >= 0 && send_lo > 0 && send_store(c, sbuf[0], scap, send_lo, dn, why)) return 1;
+  if (dn >= 0 && recv_dn > 0 && recv_store(c, rbuf[0], rcap, recv_dn, dn, why)) return 1;
+  if (up >= 0 && recv_up > 0 && recv_store(c, rbuf[1], rcap, recv_up, up, why)) return 1;
+  NCCK(ncclGroupEnd(), why);
+  return join_out(c, s, why);
+}
+
 }  // namespace st
 
 extern "C" st_status st_nccl_unique_id(void* out) {

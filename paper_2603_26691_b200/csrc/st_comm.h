@@ -36,6 +36,18 @@ int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int6
                  int32_t chunk_lo, int32_t n_local_chunks, int key_bits, SortScratch& sc, int64_t* row,
                  int64_t* n_new, int* launches, cudaStream_t s, std::string& why);
 
+// Fused neighbour-scatter rebin (C-16 without a global sort): all-reduce(max)
+// of the "far" flag, then the virtual-plane counts: vcnt_hi (movers into the
+// plane above) -> upper neighbour, vcnt_lo -> lower neighbour; rcnt_dn receives
+// the lower neighbour's counts for my bottom plane, rcnt_up the upper's for my
+// top plane.  Missing neighbours (walls) leave the receive arrays untouched.
+int comm_rebin_counts(Comm* c, const uint32_t* vcnt_lo, const uint32_t* vcnt_hi, uint32_t* rcnt_dn, uint32_t* rcnt_up,
+                      int nvb, int* d_far, bool periodic, cudaStream_t s, std::string& why);
+// Payload of the movers: sbuf[1] (send_hi particles) -> up, sbuf[0] (send_lo) ->
+// down; rbuf[0] <- down (recv_dn), rbuf[1] <- up (recv_up).  SoA x,u,d,w,id.
+int comm_rebin_payload(Comm* c, const Store* sbuf, int64_t scap, int64_t send_lo, int64_t send_hi, const Store* rbuf,
+                       int64_t rcap, int64_t recv_dn, int64_t recv_up, bool periodic, cudaStream_t s, std::string& why);
+
 }  // namespace st
 
 extern "C" {

@@ -17,6 +17,11 @@ struct BinGeom {
   int nkz;     // local chunk planes
   int kz0;     // first local chunk plane
   int sh;      // log2(chunk_cells) if a power of two, else -1
+  // multi-GPU: the cell plane just below / above the slab belongs to the
+  // neighbour rank; its cells are "virtual bins" v = ((ky*NCx+kx)*cc+ly)*cc+lx
+  // (the receiver's bin order within one plane), nvb per side
+  int nvb;
+  int vz[2];   // global z of the lower / upper virtual plane, -1 if none (wall or 1 rank)
 };
 
 struct StepArgs {
@@ -39,7 +44,32 @@ struct StepArgs {
   int* err;                   // hard errors (ERRF_*)
   int* far;                   // set when the next rebin cannot use the neighbour scatter
   unsigned long long* movers; // particles whose end chunk differs from their output bin's chunk
+  // multi-GPU scatter: movers into the neighbour planes go to send buffers
+  const int64_t* voff[2];     // [nvb+1] offsets of the virtual bins in sbuf[side]
+  Store sbuf[2];
+  int64_t scap;               // capacity (particles) of each send buffer
 };
+
+// Multi-GPU rebin helpers (k_step.cu)
+int launch_vcombine(const Geom& g, const BinGeom& bg, uint32_t* new_cnt, const uint32_t* rcnt_dn,
+                    const uint32_t* rcnt_up, uint32_t* kept_dn, uint32_t* kept_up, int oz0, int oz1, cudaStream_t s);
+struct InsertArgs {
+  Geom g;
+  BinGeom bg;
+  Store rbuf;                 // arrivals of one side (SoA, capacity rcap)
+  int64_t rcap, count;
+  const int64_t* roff;        // [nvb+1]
+  const uint32_t* kept;       // [nvb] local count of the destination bin before arrivals
+  int plane;                  // owned plane the arrivals land in (z0 or z1-1)
+  Store B;
+  int64_t cap;
+  const int64_t* off_new;
+  int nbins;
+  int* hist_next;
+  int* far;
+  int* err;
+};
+int launch_insert(const InsertArgs& a, cudaStream_t s);
 
 int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s);
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s);
