@@ -23,8 +23,9 @@
 // The kernel is specialised at compile time on the periodic-axis mask (BCM) and
 // on log2(chunk_cells) (SH) so the hot loop carries no per-particle branches on
 // the configuration; BCM = -1 / SH = 0 are the generic (runtime) fallbacks.
-// Streaming particle traffic uses evict-first loads/stores (__ldcs/__stcs) so
-// L2 keeps the field, the accumulator and the histograms.
+// Particle input is staged per warp with TMA bulk copies (cp.async.bulk +
+// mbarrier, kStages batches ahead), so the DRAM stream is exact 16-byte aligned
+// segments and never pollutes L1; in-place results use evict-first stores.
 #include <cuda_runtime.h>
 
 #include "st_device.cuh"
@@ -47,6 +48,68 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(0.0f)
                : "memory");
+}
+
+// ---------------------------------------------------------------- TMA bulk-copy pipeline
+// Each warp prefetches the SoA segments of its next kStages batches of 32
+// particles into shared memory with cp.async.bulk (the Blackwell bulk-copy
+// engine, SASS UBLKCP); completion is tracked by one mbarrier per stage.
+constexpr int kStages = 3;
+constexpr int kSeg = 36;   // floats per staged segment: 32 + 16-byte alignment slack
+struct alignas(16) Stage {
+  float f[8][kSeg];                 // x0 x1 x2 u0 u1 u2 d w
+  unsigned long long id[kSeg / 2 + 16];  // 34 used (32 + alignment slack)
+};
+
+__host__ __device__ constexpr int warp_smem_bytes(bool scatter) {
+  return (int)((kStages * sizeof(Stage) + kStages * 8 + (kMaxBins + 1) * 4 + kMaxBins * 12 +
+                (scatter ? kMaxBins * kSlots * 4 : 0) + 15) / 16 * 16);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// Stage the batch starting at store index i0 (lane 0 only).  Segments are copied
+// from the 16-byte aligned index below i0; `lim` bounds the copy (<= capacity).
+__device__ __forceinline__ void stage_issue(Stage* stg, unsigned long long* bar, const Store& A, int64_t cap, int64_t i0,
+                                            int64_t lim, bool with_id) {
+  const int64_t f0 = i0 & ~(int64_t)3;
+  int64_t f1 = (i0 + 32 + 3) & ~(int64_t)3;
+  if (f1 > lim) f1 = lim;
+  const uint32_t fb = (uint32_t)(f1 - f0) * 4u;
+  uint32_t total = 8u * fb;
+  int64_t q0 = 0, q1 = 0;
+  if (with_id) {
+    q0 = i0 & ~(int64_t)1;
+    q1 = (i0 + 32 + 1) & ~(int64_t)1;
+    if (q1 > lim) q1 = lim;
+    total += (uint32_t)(q1 - q0) * 8u;
+  }
+  mbar_expect_tx(bar, total);
+  const float* src[8] = {A.x, A.x + cap, A.x + 2 * cap, A.u, A.u + cap, A.u + 2 * cap, A.d, A.w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) bulk_g2s(stg->f[k], src[k] + f0, fb, bar);
+  if (with_id) bulk_g2s(stg->id, A.id + q0, (uint32_t)(q1 - q0) * 8u, bar);
 }
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -171,14 +234,17 @@ __device__ __forceinline__ void stencil_from_cell(float t, int c, int& i0, float
 // ---------------------------------------------------------------- the step kernel
 template <bool SCATTER, bool ADVANCE, int BCM, int SH>
 __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(StepArgs a) {
-  __shared__ int run_s[8][kMaxBins * kSlots];
-  __shared__ int rel_s[8][kMaxBins + 1];     // particle offsets of the item's bins, relative to p0
-  __shared__ int cell_s[8][kMaxBins][3];      // cell coordinates of the item's bins
+  // dynamic shared memory, one slice per warp (see warp_smem_bytes)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geom& g = a.g;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  int* run = run_s[wib];
-  int* rel = rel_s[wib];
+  unsigned char* ws = smem_raw + (size_t)wib * warp_smem_bytes(SCATTER);
+  Stage* stg = reinterpret_cast<Stage*>(ws);                                   // TMA-staged segments
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kStages * sizeof(Stage));
+  int* rel = reinterpret_cast<int*>(bar + kStages);                            // [kMaxBins+1] bin offsets
+  int (*cell_w)[3] = reinterpret_cast<int (*)[3]>(rel + kMaxBins + 1);         // [kMaxBins][3] bin cells
+  int* run = reinterpret_cast<int*>(cell_w + kMaxBins);                        // [kMaxBins*27] (scatter)
   const int n_items = *a.n_items;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t cap = a.cap;
@@ -186,6 +252,12 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
   const int cc = SH > 0 ? (1 << SH) : g.cc;
   int flags = 0, farflag = 0;
   unsigned movers = 0;
+  uint32_t phase = 0;   // parity bit per stage
+  if (lane == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(bar + k, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
 
   for (int item = blockIdx.x * (blockDim.x >> 5) + wib; item < n_items; item += warps_total) {
     const int b0 = a.item_bin0[item];
@@ -193,27 +265,39 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
     const int nb = b1 - b0;
     const int64_t p0 = a.off[b0];
     for (int k = lane; k <= nb; k += 32) rel[k] = (int)(a.off[b0 + k] - p0);
-    for (int k = lane; k < nb; k += 32) cell_of_bin(g, a.bg, b0 + k, cell_s[wib][k][0], cell_s[wib][k][1], cell_s[wib][k][2]);
+    for (int k = lane; k < nb; k += 32) cell_of_bin(g, a.bg, b0 + k, cell_w[k][0], cell_w[k][1], cell_w[k][2]);
     if (SCATTER)
       for (int k = lane; k < nb * kSlots; k += 32) run[k] = 0;
     __syncwarp();
     const int np = rel[nb];
+    const int nbatch = (np + 31) >> 5;
+    // prime the pipeline
+    if (lane == 0) {
+      fence_proxy_async();
+      for (int k = 0; k < kStages && k < nbatch; ++k) stage_issue(stg + k, bar + k, a.A, cap, p0 + 32 * k, cap, SCATTER);
+    }
     int lb = 0;   // this lane's bin pointer (monotone over its particles)
-    for (int base = 0; base < np; base += 32) {
+    for (int bi = 0; bi < nbatch; ++bi) {
+      const int base = bi << 5;
+      const int sk = bi % kStages;
       const int r = base + lane;
       const bool valid = r < np;
       const int64_t i = p0 + r;
       if (valid)
         while (rel[lb + 1] <= r) ++lb;
       const int s = b0 + lb;
-      const int sx = cell_s[wib][lb][0], sy = cell_s[wib][lb][1], sz = cell_s[wib][lb][2];
+      const int sx = cell_w[lb][0], sy = cell_w[lb][1], sz = cell_w[lb][2];
+      mbar_wait(bar + sk, (phase >> sk) & 1u);
+      phase ^= 1u << sk;
+      const Stage& S = stg[sk];
+      const int so = (int)((p0 + base) & 3) + lane;   // slot of this lane's particle in the segments
       float xp0 = 0.f, xp1 = 0.f, xp2 = 0.f, up0 = 0.f, up1 = 0.f, up2 = 0.f;
       float dp = 1e-5f, wp = 0.f;
       if (valid) {
-        xp0 = __ldcs(a.A.x + i); xp1 = __ldcs(a.A.x + cap + i); xp2 = __ldcs(a.A.x + 2 * cap + i);
-        up0 = __ldcs(a.A.u + i); up1 = __ldcs(a.A.u + cap + i); up2 = __ldcs(a.A.u + 2 * cap + i);
-        dp = __ldcs(a.A.d + i);
-        wp = __ldcs(a.A.w + i);
+        xp0 = S.f[0][so]; xp1 = S.f[1][so]; xp2 = S.f[2][so];
+        up0 = S.f[3][so]; up1 = S.f[4][so]; up2 = S.f[5][so];
+        dp = S.f[6][so];
+        wp = S.f[7][so];
       }
       // current cell (deposit cell of the first sub-step; scatter key)
       float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
@@ -382,19 +466,27 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
       }
       if (write_ok) {
         if (SCATTER) {
-          // the id is only carried: load it late to keep it out of the live range
-          const unsigned long long pid = __ldcs(reinterpret_cast<const unsigned long long*>(a.A.id) + i);
+          // the id is only carried: read it from the stage late, out of the live range
+          const unsigned long long pid = S.id[(int)((p0 + base) & 1) + lane];
           const Store& o = vside < 0 ? a.B : a.sbuf[vside];
           const int64_t oc = vside < 0 ? cap : a.scap;
-          __stcs(o.x + dest, xp0); __stcs(o.x + oc + dest, xp1); __stcs(o.x + 2 * oc + dest, xp2);
-          __stcs(o.u + dest, up0); __stcs(o.u + oc + dest, up1); __stcs(o.u + 2 * oc + dest, up2);
-          __stcs(o.d + dest, dp);
-          __stcs(o.w + dest, wp);
-          __stcs(reinterpret_cast<unsigned long long*>(o.id) + dest, pid);
+          // normal L2 policy: the runs of consecutive destinations written by
+          // neighbouring warps merge into full sectors before write-back
+          o.x[dest] = xp0; o.x[oc + dest] = xp1; o.x[2 * oc + dest] = xp2;
+          o.u[dest] = up0; o.u[oc + dest] = up1; o.u[2 * oc + dest] = up2;
+          o.d[dest] = dp;
+          o.w[dest] = wp;
+          reinterpret_cast<unsigned long long*>(o.id)[dest] = pid;
         } else if (ADVANCE) {
           __stcs(a.A.x + i, xp0); __stcs(a.A.x + cap + i, xp1); __stcs(a.A.x + 2 * cap + i, xp2);
           __stcs(a.A.u + i, up0); __stcs(a.A.u + cap + i, up1); __stcs(a.A.u + 2 * cap + i, up2);
         }
+      }
+      // the stage is consumed: refill it with the batch kStages ahead
+      __syncwarp();
+      if (lane == 0 && bi + kStages < nbatch) {
+        fence_proxy_async();
+        stage_issue(stg + sk, bar + sk, a.A, cap, p0 + 32 * (bi + kStages), cap, SCATTER);
       }
     }
     __syncwarp();
@@ -564,14 +656,16 @@ inline unsigned blocks_for(int64_t n, int bs = 256) { return (unsigned)((n + bs 
 template <bool S, bool A, int BCM, int SH>
 int launch_variant(const StepArgs& a, cudaStream_t s) {
   static int grid = 0;
+  const int smem = 8 * warp_smem_bytes(S);
   if (!grid) {
     int nsm = 148, dev = 0, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_step<S, A, BCM, SH>, 256, 0);
+    cudaFuncSetAttribute(k_step<S, A, BCM, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_step<S, A, BCM, SH>, 256, smem);
     grid = nsm * (per > 0 ? per : 1);
   }
-  k_step<S, A, BCM, SH><<<grid, 256, 0, s>>>(a);
+  k_step<S, A, BCM, SH><<<grid, 256, smem, s>>>(a);
   return 1;
 }
 

@@ -314,7 +314,9 @@ static st_status init_impl(st_ctx* c) {
   build_geometry(c);
   const Geom& g = c->g;
   if (g.wrapz && g.wnz > g.n[2]) return fail(c, ST_ERR_UNSUPPORTED, "periodic z needs (slab + 2 halos + 2) <= nz per rank");
-  c->cap = c->cfg.capacity;
+  // SoA stride rounded to 32 particles: every component segment is 16-byte
+  // aligned for the bulk (TMA) copies of k_step
+  c->cap = (c->cfg.capacity + 31) / 32 * 32;
   if (c->cfg.stream) {
     c->cs = (cudaStream_t)c->cfg.stream;
   } else {
