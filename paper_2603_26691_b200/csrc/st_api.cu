@@ -536,7 +536,7 @@ st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const 
     return ST_OK;
   }
   if (!x || !u || !d) return fail(c, ST_ERR_INVALID_ARG, "x, u and d are required");
-  if (c->n + n > c->cap) return fail(c, ST_ERR_CAPACITY, "store capacity exceeded");
+  if (c->n + n > c->cfg.capacity) return fail(c, ST_ERR_CAPACITY, "store capacity exceeded");
   Store s = c->S[c->cur];
   const int64_t o = c->n, cap = c->cap;
   auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
@@ -706,7 +706,7 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     for (int k = 0; k < 4; ++k)
       if (c->h_tot[k] > c->scap) return fail(c, ST_ERR_CAPACITY, "migration buffer too small (more movers than cap/16)");
     n_new = c->n - c->h_tot[0] - c->h_tot[1] + c->h_tot[2] + c->h_tot[3];
-    if (n_new > c->cap) return fail(c, ST_ERR_CAPACITY, "migration would exceed the store capacity");
+    if (n_new > c->cfg.capacity) return fail(c, ST_ERR_CAPACITY, "migration would exceed the store capacity");
   }
   *c->h_far = 0;
   ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
