@@ -193,7 +193,8 @@ st_status st_get_particles(st_ctx* ctx, int64_t cap, int64_t* n_out,
 st_status st_locate(st_ctx* ctx, int64_t n, const float* x, int32_t* cell, int32_t* chunk);
 
 /* Migration counts of the last rebin: row[dst] = particles this rank sent to dst
- * (row[rank] = particles kept).  row has nranks entries. */
+ * (row[rank] = particles kept).  row has nranks entries.  Executes a due rebin
+ * first (collective when nranks > 1). */
 st_status st_get_migration_counts(st_ctx* ctx, int64_t* row);
 
 st_status st_get_layout(st_ctx* ctx, st_layout* out);

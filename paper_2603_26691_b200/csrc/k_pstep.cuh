@@ -1,0 +1,291 @@
+// k_step v6 — instruction-lean step kernel (included by k_step.cu, which defines
+// the helpers: Stage/TMA pipeline, bin geometry, slots, reductions, physics bits).
+//
+// Differences from the generic loop, all aimed at issue slots per particle:
+//  * items are one chunk row (<= 8 consecutive bins when chunk_cells == 8);
+//  * the item's fluid neighbourhood (bin cells +-2: a 12 x 5 x 5 float4 box) is
+//    staged in shared memory once per item, so the 8 trilinear corners are 8
+//    LDS.128 with compile-time offsets; particles outside the box (only after a
+//    far move or multi-sub-step drift) take the global-memory path;
+//  * invalid lanes of a partial batch compute on a clamped copy of a valid
+//    particle and only their side effects are predicated off (no divergence);
+//  * 32-bit (bin, slot) keys for the rank and the histogram.
+#pragma once
+
+constexpr int kBoxX = 12, kBoxY = 5, kBoxZ = 5;            // (8 + 4) x 5 x 5 cells
+constexpr int kBoxCells = kBoxX * kBoxY * kBoxZ;           // 300 float4 = 4.8 KB
+constexpr int kRowBins = 8;
+
+constexpr int kBarBytes = 32;                               // kStages mbarriers, padded to 16 B
+__host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
+  return (int)((kStages * sizeof(Stage) + kBarBytes + kBoxCells * 16 + (kRowBins + 1) * 4 +
+                (scatter ? kRowBins * kSlots * 4 : 0) + 15) / 16 * 16);
+}
+
+template <bool SCATTER, bool ADVANCE, int BCM>
+__global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
+  constexpr int SH = 3;   // chunk_cells == 8
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geom& g = a.g;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char* ws = smem_raw + (size_t)wib * pwarp_smem_bytes(SCATTER);
+  Stage* stg = reinterpret_cast<Stage*>(ws);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kStages * sizeof(Stage));
+  float4* box = reinterpret_cast<float4*>(ws + kStages * sizeof(Stage) + kBarBytes);   // 16-byte aligned
+  int* rel = reinterpret_cast<int*>(box + kBoxCells);                         // [kRowBins+1]
+  int* run = rel + (kRowBins + 1);                                            // [kRowBins*27]
+  const int n_items = *a.n_items;
+  const int warps_total = gridDim.x * (blockDim.x >> 5);
+  const int64_t cap = a.cap;
+  const int nbins = a.nbins;
+  const int pz = g.gy * g.gx;
+  int flags = 0, farflag = 0;
+  unsigned movers = 0;
+  uint32_t phase = 0;
+  if (lane == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(bar + k, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  for (int item = blockIdx.x * (blockDim.x >> 5) + wib; item < n_items; item += warps_total) {
+    const int b0 = a.item_bin0[item];
+    const int b1 = (item + 1 < n_items) ? a.item_bin0[item + 1] : nbins;
+    const int nb = b1 - b0;                       // <= kRowBins, one chunk row
+    const int64_t p0 = a.off[b0];
+    if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
+    if (SCATTER)
+      for (int k = lane; k < nb * kSlots; k += 32) run[k] = 0;
+    // cell of the row's first bin; the row runs along +x
+    int rx, ry, rz;
+    cell_of_bin(g, a.bg, b0, rx, ry, rz);
+    const int bx0 = rx - 2, by0 = ry - 2, bz0 = rz - 2;
+    // stage the fluid neighbourhood (window indices clamped: cells outside the
+    // window are never read by a valid stencil)
+    for (int q = lane; q < kBoxCells; q += 32) {
+      const int qx = q % kBoxX, qy = (q / kBoxX) % kBoxY, qz = q / (kBoxX * kBoxY);
+      int wx = bx0 + qx + 1, wy = by0 + qy + 1, wz = window_z(g, bz0 + qz);
+      wx = min(max(wx, 0), g.gx - 1);
+      wy = min(max(wy, 0), g.gy - 1);
+      wz = wz < 0 ? (bz0 + qz < g.wz0 + 1 ? 0 : g.wnz - 1) : wz;
+      box[q] = __ldg(a.field + ((int64_t)wz * pz + wy * g.gx + wx));
+    }
+    __syncwarp();
+    const int np = rel[nb];
+    const int nbatch = (np + 31) >> 5;
+    if (lane == 0) {
+      fence_proxy_async();
+      for (int k = 0; k < kStages && k < nbatch; ++k) stage_issue(stg + k, bar + k, a.A, cap, p0 + 32 * k, cap, SCATTER);
+    }
+    int lb = 0;
+    for (int bi = 0; bi < nbatch; ++bi) {
+      const int base = bi << 5;
+      const int sk = bi % kStages;
+      const bool valid = base + lane < np;
+      const int r = valid ? base + lane : np - 1;          // invalid lanes mirror a valid particle
+      while (rel[lb + 1] <= r) ++lb;
+      const int s = b0 + lb;
+      const int sx = rx + lb, sy = ry, sz = rz;             // bin cell (row along x)
+      mbar_wait(bar + sk, (phase >> sk) & 1u);
+      phase ^= 1u << sk;
+      const Stage& S = stg[sk];
+      const int so = (int)((p0 + base) & 3) + (r - base);
+      float xp0 = S.f[0][so], xp1 = S.f[1][so], xp2 = S.f[2][so];
+      float up0 = S.f[3][so], up1 = S.f[4][so], up2 = S.f[5][so];
+      const float dp = S.f[6][so], wp = S.f[7][so];
+      float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
+            t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
+      int c0 = cell_from_t(t0, g.n[0]), c1 = cell_from_t(t1, g.n[1]), c2 = cell_from_t(t2, g.n[2]);
+      int ox = sx, oy = sy, oz = sz, obin = s, vside = -1;
+      int64_t dest = p0 + r;
+      bool write_ok = valid;
+      if (SCATTER) {
+        const int j = slot_of<BCM>(g, sx, sy, sz, c0, c1, c2);
+        if (valid && j < 0) {
+          flags |= ERRF_SCATTER;
+          write_ok = false;
+        }
+        const int key = write_ok ? lb * kSlots + j : -1 - lane;
+        const unsigned peers = __match_any_sync(kFull, key);
+        const int leader = __ffs(peers) - 1;
+        int rbase = 0;
+        if (lane == leader && key >= 0) {
+          rbase = run[key];
+          run[key] = rbase + __popc(peers);
+        }
+        rbase = __shfl_sync(kFull, rbase, leader) + __popc(peers & lanemask_lt());
+        __syncwarp();
+        ox = c0;
+        oy = c1;
+        oz = c2;
+        const int jj = j < 0 ? kStay : j;
+        const int within = a.slot_base[(int64_t)jj * nbins + s] + rbase;
+        vside = (c2 == a.bg.vz[0]) ? 0 : ((c2 == a.bg.vz[1]) ? 1 : -1);
+        if (vside >= 0) {
+          dest = a.voff[vside][vbin_of_cell<SH>(g, c0, c1, 8)] + within;
+          if (write_ok && (dest < 0 || dest >= a.scap)) {
+            flags |= ERRF_SCATTER;
+            write_ok = false;
+          }
+        } else {
+          obin = bin_of_cell<SH>(g, a.bg, ox, oy, oz);
+          dest = a.off_new[obin] + within;
+          if (write_ok && (dest < 0 || dest >= a.n)) {
+            flags |= ERRF_SCATTER;
+            write_ok = false;
+          }
+        }
+      }
+      if (ADVANCE) {
+        const float d = dp;
+        const float tau = a.p.tau_c * d * d;
+        const float inv_tau = rcp_approx(tau);
+        const float mw = a.p.mass_c * d * d * d * wp;
+        const float dt = a.dt;
+        const float gx = a.p.g[0], gy = a.p.g[1], gz = a.p.g[2];
+        for (int sub = 0; sub < a.nsteps; ++sub) {
+          if (sub > 0) {
+            t0 = cell_coord(xp0, g.lo[0], g.ih[0]);
+            t1 = cell_coord(xp1, g.lo[1], g.ih[1]);
+            t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
+            c0 = cell_from_t(t0, g.n[0]);
+            c1 = cell_from_t(t1, g.n[1]);
+            c2 = cell_from_t(t2, g.n[2]);
+          }
+          int ix, iy, iz;
+          float fx, fy, fz;
+          stencil_from_cell(t0, c0, ix, fx);
+          stencil_from_cell(t1, c1, iy, fy);
+          stencil_from_cell(t2, c2, iz, fz);
+          const int qx = ix - bx0, qy = iy - by0, qz = iz - bz0;
+          float4 c000, c100, c010, c110, c001, c101, c011, c111;
+          if ((unsigned)qx < (unsigned)(kBoxX - 1) && (unsigned)qy < (unsigned)(kBoxY - 1) &&
+              (unsigned)qz < (unsigned)(kBoxZ - 1)) {
+            const float4* q = box + (qz * kBoxY + qy) * kBoxX + qx;
+            c000 = q[0]; c100 = q[1];
+            c010 = q[kBoxX]; c110 = q[kBoxX + 1];
+            c001 = q[kBoxX * kBoxY]; c101 = q[kBoxX * kBoxY + 1];
+            c011 = q[kBoxX * kBoxY + kBoxX]; c111 = q[kBoxX * kBoxY + kBoxX + 1];
+          } else {   // outside the staged box: global path (window-checked)
+            int wz = window_z(g, iz);
+            if (wz < 0 || wz + 1 >= g.wnz) {
+              if (valid) flags |= ERRF_WINDOW;
+              wz = wz < 0 ? 0 : g.wnz - 2;
+            }
+            const float4* fb = a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
+            c000 = __ldg(fb); c100 = __ldg(fb + 1);
+            c010 = __ldg(fb + g.gx); c110 = __ldg(fb + g.gx + 1);
+            c001 = __ldg(fb + pz); c101 = __ldg(fb + pz + 1);
+            c011 = __ldg(fb + pz + g.gx); c111 = __ldg(fb + pz + g.gx + 1);
+          }
+          const float4 uf = lerp4(lerp4(lerp4(c000, c100, fx), lerp4(c010, c110, fx), fy),
+                                  lerp4(lerp4(c001, c101, fx), lerp4(c011, c111, fx), fy), fz);
+          const float sxv = uf.x - up0, syv = uf.y - up1, szv = uf.z - up2;
+          const float Re = sqrt_approx(fmaf(sxv, sxv, fmaf(syv, syv, szv * szv))) * d * a.p.inv_nu;
+          float f = 1.0f + 0.15f * exp2f(0.687f * __log2f(Re));
+          f = (Re <= 1000.0f) ? f : (0.44f / 24.0f) * Re;
+          f = (a.p.drag_law == ST_DRAG_STOKES) ? 1.0f : f;
+          const float taue = tau * rcp_approx(f);
+          const float h = dt * f * inv_tau;
+          float du0, du1, du2;
+          if (a.p.integrator == ST_INT_EXPONENTIAL) {
+            float E, M;
+            exp_pair(h, E, M);
+            const float tM = taue * M;
+            const float us0 = fmaf(gx, taue, uf.x), us1 = fmaf(gy, taue, uf.y), us2 = fmaf(gz, taue, uf.z);
+            const float r0 = up0 - us0, r1 = up1 - us1, r2 = up2 - us2;
+            du0 = fmaf(-M, r0, -gx * dt);
+            du1 = fmaf(-M, r1, -gy * dt);
+            du2 = fmaf(-M, r2, -gz * dt);
+            xp0 = fmaf(tM, r0, fmaf(us0, dt, xp0));
+            xp1 = fmaf(tM, r1, fmaf(us1, dt, xp1));
+            xp2 = fmaf(tM, r2, fmaf(us2, dt, xp2));
+            up0 = fmaf(E, r0, us0);
+            up1 = fmaf(E, r1, us1);
+            up2 = fmaf(E, r2, us2);
+          } else {
+            const float inv1h = rcp_approx(1.0f + h);
+            const float un0 = (up0 + h * uf.x + dt * gx) * inv1h;
+            const float un1 = (up1 + h * uf.y + dt * gy) * inv1h;
+            const float un2 = (up2 + h * uf.z + dt * gz) * inv1h;
+            du0 = (un0 - up0) - gx * dt;
+            du1 = (un1 - up1) - gy * dt;
+            du2 = (un2 - up2) - gz * dt;
+            xp0 = fmaf(dt, un0, xp0);
+            xp1 = fmaf(dt, un1, xp1);
+            xp2 = fmaf(dt, un2, xp2);
+            up0 = un0;
+            up1 = un1;
+            up2 = un2;
+          }
+          if (a.p.two_way) {
+            const int az = acc_z(g, c2);
+            if (valid && az < 0) flags |= ERRF_WINDOW;
+            const bool dep = valid && az >= 0;
+            const int ckey = dep ? (az * g.n[1] + c1) * g.n[0] + c0 : -1 - lane;
+            const float ja = -mw * du0, jb = -mw * du1, jc = -mw * du2;
+            const unsigned peers = __match_any_sync(kFull, ckey);
+            const int lead = __shfl_sync(kFull, ckey, 0);
+            const unsigned major = __shfl_sync(kFull, peers, 0);
+            if (__popc(major) >= 4 && lead >= 0) {
+              const bool in = (major >> lane) & 1u;
+              float ra = ja, rb = jb, rc = jc;
+              group_sum3(in, ra, rb, rc);
+              if (lane == 0) red_add_v4(a.acc + lead, ra, rb, rc);
+              if (!in && dep) red_add_v4(a.acc + ckey, ja, jb, jc);
+            } else if (dep) {
+              red_add_v4(a.acc + ckey, ja, jb, jc);
+            }
+          }
+          bool bad = false;
+          bad |= apply_bc(periodic<BCM>(g, 0) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[0], g.hi[0], g.L[0], xp0, up0);
+          bad |= apply_bc(periodic<BCM>(g, 1) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[1], g.hi[1], g.L[1], xp1, up1);
+          bad |= apply_bc(periodic<BCM>(g, 2) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[2], g.hi[2], g.L[2], xp2, up2);
+          if (bad && valid) flags |= ERRF_CFL;
+        }
+      }
+      // slot histogram of the end position w.r.t. the output bin (next rebin's input)
+      {
+        const int e0 = cell_from_t(cell_coord(xp0, g.lo[0], g.ih[0]), g.n[0]);
+        const int e1 = cell_from_t(cell_coord(xp1, g.lo[1], g.ih[1]), g.n[1]);
+        const int e2 = cell_from_t(cell_coord(xp2, g.lo[2], g.ih[2]), g.n[2]);
+        const bool here = write_ok && vside < 0;
+        const int j2 = slot_of<BCM>(g, ox, oy, oz, e0, e1, e2);
+        if (here && j2 < 0) farflag = 1;
+        // 32-bit key (st_init checks nbins * 27 < 2^31)
+        const int hkey = (here && j2 >= 0) ? obin * kSlots + j2 : -1 - lane;
+        const unsigned peers = __match_any_sync(kFull, hkey);
+        if (hkey >= 0 && (peers & lanemask_lt()) == 0) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, __popc(peers));
+        const bool mover = write_ok && (((e0 >> SH) != (ox >> SH)) | ((e1 >> SH) != (oy >> SH)) | ((e2 >> SH) != (oz >> SH)));
+        movers += mover ? 1u : 0u;
+      }
+      if (write_ok) {
+        if (SCATTER) {
+          const unsigned long long pid = S.id[(int)((p0 + base) & 1) + (r - base)];
+          const Store& o = vside < 0 ? a.B : a.sbuf[vside];
+          const int64_t oc = vside < 0 ? cap : a.scap;
+          o.x[dest] = xp0; o.x[oc + dest] = xp1; o.x[2 * oc + dest] = xp2;
+          o.u[dest] = up0; o.u[oc + dest] = up1; o.u[2 * oc + dest] = up2;
+          o.d[dest] = dp;
+          o.w[dest] = wp;
+          reinterpret_cast<unsigned long long*>(o.id)[dest] = pid;
+        } else if (ADVANCE) {
+          __stcs(a.A.x + dest, xp0); __stcs(a.A.x + cap + dest, xp1); __stcs(a.A.x + 2 * cap + dest, xp2);
+          __stcs(a.A.u + dest, up0); __stcs(a.A.u + cap + dest, up1); __stcs(a.A.u + 2 * cap + dest, up2);
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && bi + kStages < nbatch) {
+        fence_proxy_async();
+        stage_issue(stg + sk, bar + sk, a.A, cap, p0 + 32 * (bi + kStages), cap, SCATTER);
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) movers += __shfl_xor_sync(kFull, movers, o);
+  if (lane == 0 && movers) atomicAdd(a.movers, (unsigned long long)movers);
+  if (flags) atomicOr(a.err, flags);
+  if (farflag) *(volatile int*)a.far = 1;
+}

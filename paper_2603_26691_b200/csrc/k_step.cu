@@ -499,6 +499,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
   if (farflag) *(volatile int*)a.far = 1;
 }
 
+#include "k_pstep.cuh"
+
 // ---------------------------------------------------------------- rebin preparation
 // Per destination bin d: sources s = d - delta over the 27 deltas (canonical,
 // deduplicated), in ascending s; base[j][s] = running sum; new_cnt[d] = total.
@@ -610,10 +612,10 @@ __global__ void k_hist_stay(const int64_t* __restrict__ off, int nbins, int* __r
 
 // item boundaries: bin s starts an item if s % kMaxBins == 0 or the kItemParticles
 // window of its first particle differs from that of bin s-1's first particle.
-__global__ void k_item_flags(const int64_t* __restrict__ off, int nbins, uint32_t* __restrict__ flag) {
+__global__ void k_item_flags(const int64_t* __restrict__ off, int nbins, int row, uint32_t* __restrict__ flag) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nbins) return;
-  uint32_t f = (s % kMaxBins) == 0;
+  uint32_t f = (s % row) == 0;
   if (!f) f = (off[s] / kItemParticles) != (off[s - 1] / kItemParticles);
   flag[s] = f;
 }
@@ -669,16 +671,32 @@ int launch_variant(const StepArgs& a, cudaStream_t s) {
   return 1;
 }
 
+template <bool S, bool A, int BCM>
+int launch_pvariant(const StepArgs& a, cudaStream_t s) {
+  static int grid = 0;
+  const int smem = 8 * pwarp_smem_bytes(S);
+  if (!grid) {
+    int nsm = 148, dev = 0, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_pstep<S, A, BCM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pstep<S, A, BCM>, 256, smem);
+    grid = nsm * (per > 0 ? per : 1);
+  }
+  k_pstep<S, A, BCM><<<grid, 256, smem, s>>>(a);
+  return 1;
+}
+
 template <bool S, bool A>
 int launch_mode(const StepArgs& a, cudaStream_t s) {
   const int bcm = (a.g.bc[0] == ST_BC_PERIODIC ? 1 : 0) | (a.g.bc[1] == ST_BC_PERIODIC ? 2 : 0) |
                   (a.g.bc[2] == ST_BC_PERIODIC ? 4 : 0);
-  if (a.g.cc == 8) {
+  if (a.g.cc == 8) {   // chunk-row items with the staged fluid box (k_pstep.cuh)
     switch (bcm) {
-      case 0: return launch_variant<S, A, 0, 3>(a, s);
-      case 7: return launch_variant<S, A, 7, 3>(a, s);
-      case 3: return launch_variant<S, A, 3, 3>(a, s);
-      default: return launch_variant<S, A, -1, 3>(a, s);
+      case 0: return launch_pvariant<S, A, 0>(a, s);
+      case 7: return launch_pvariant<S, A, 7>(a, s);
+      case 3: return launch_pvariant<S, A, 3>(a, s);
+      default: return launch_pvariant<S, A, -1>(a, s);
     }
   }
   return launch_variant<S, A, -1, 0>(a, s);
@@ -716,9 +734,11 @@ int launch_hist_all_stay(const int64_t* off, int nbins, int* hist, cudaStream_t 
   return 1;
 }
 
-int launch_items(const int64_t* off, int nbins, uint32_t* flag, int64_t* pos, int64_t* partial, int* item_bin0,
-                 int* n_items, cudaStream_t s) {
-  k_item_flags<<<blocks_for(nbins), 256, 0, s>>>(off, nbins, flag);
+int launch_items(const int64_t* off, int nbins, int cc, uint32_t* flag, int64_t* pos, int64_t* partial,
+                 int* item_bin0, int* n_items, cudaStream_t s) {
+  // 8^3 chunks: one chunk row (<= 8 bins) per item for k_pstep; else <= kMaxBins bins
+  const int row = cc == 8 ? kRowBins : kMaxBins;
+  k_item_flags<<<blocks_for(nbins), 256, 0, s>>>(off, nbins, row, flag);
   int nl = 1 + launch_exclusive_scan_u32(flag, nbins, pos, partial, s);
   k_item_fill<<<blocks_for(nbins), 256, 0, s>>>(flag, pos, nbins, item_bin0, n_items);
   return nl + 1;

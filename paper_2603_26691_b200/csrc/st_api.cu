@@ -205,7 +205,12 @@ static st_status validate(const st_config* c, std::string& why) {
     if (!(c->cell_size[a] > 0.0)) { why = "cell_size must be > 0"; return ST_ERR_INVALID_ARG; }
     if (c->bc[a] != ST_BC_PERIODIC && c->bc[a] != ST_BC_REFLECT) { why = "bad bc"; return ST_ERR_INVALID_ARG; }
   }
-  if ((int64_t)c->dims[0] * c->dims[1] * c->dims[2] > (int64_t)INT32_MAX) { why = "too many cells"; return ST_ERR_INVALID_ARG; }
+  if (c->chunk_cells >= 1) {
+    // chunk-padded bins x 27 slots must fit the 32-bit keys of the step kernel
+    const int64_t cc = c->chunk_cells;
+    const int64_t pad = ((c->dims[0] + cc - 1) / cc) * ((c->dims[1] + cc - 1) / cc) * ((c->dims[2] + cc - 1) / cc) * cc * cc * cc;
+    if (pad * 27 > (int64_t)INT32_MAX) { why = "too many cells (padded bins x 27 must be < 2^31)"; return ST_ERR_INVALID_ARG; }
+  }
   if (c->chunk_cells < 1) { why = "chunk_cells must be >= 1"; return ST_ERR_INVALID_ARG; }
   if (!(c->rho_f > 0 && c->nu_f > 0 && c->rho_p > 0)) { why = "densities and viscosity must be > 0"; return ST_ERR_INVALID_ARG; }
   if (c->drag_law < 0 || c->drag_law > 1 || c->integrator < 0 || c->integrator > 1 || c->coupling < 0 ||
@@ -643,7 +648,7 @@ static st_status general_rebin(st_ctx* c) {
   if (in_b) c->cur = 1 - c->cur;
   nl = launch_bin_offsets(c->key[c->cur], c->n, c->bg.nbins, c->off[c->lay], c->cs);
   nl += launch_hist_all_stay(c->off[c->lay], c->bg.nbins, c->hist[c->hcur], c->cs);
-  nl += launch_items(c->off[c->lay], c->bg.nbins, c->item_flag, c->item_pos, c->sc.partial, c->items[c->lay],
+  nl += launch_items(c->off[c->lay], c->bg.nbins, g.cc, c->item_flag, c->item_pos, c->sc.partial, c->items[c->lay],
                      c->n_items[c->lay], c->cs);
   if ((s = check_launch(c, nl))) return s;
   ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));
@@ -690,7 +695,7 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     ST_CUDA(c, cudaEventRecord(c->ev_tot, c->cs));
   }
   nl += launch_exclusive_scan_u32(c->new_cnt, nb, c->off[nlay], c->sc.partial, c->cs);
-  nl += launch_items(c->off[nlay], nb, c->item_flag, c->item_pos, c->sc.partial, c->items[nlay], c->n_items[nlay],
+  nl += launch_items(c->off[nlay], nb, g.cc, c->item_flag, c->item_pos, c->sc.partial, c->items[nlay], c->n_items[nlay],
                      c->cs);
   ST_CUDA(c, cudaMemsetAsync(c->hist[1 - c->hcur], 0, (size_t)nb * 27 * sizeof(int), c->cs));
   ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));
@@ -965,6 +970,8 @@ st_status st_locate(st_ctx* c, int64_t n, const float* x, int32_t* cell, int32_t
 st_status st_get_migration_counts(st_ctx* c, int64_t* row) {
   ST_ALIVE(c);
   if (!row) return ST_ERR_INVALID_ARG;
+  st_status fr = flush_rebin(c);   // the contract's last rebin may still be pending
+  if (fr) return fr;
   for (int r = 0; r < c->cfg.nranks; ++r) row[r] = c->mig_row[r];
   return ST_OK;
 }

@@ -74,8 +74,8 @@ int launch_insert(const InsertArgs& a, cudaStream_t s);
 int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s);
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s);
 int launch_hist_all_stay(const int64_t* off, int nbins, int* hist, cudaStream_t s);
-int launch_items(const int64_t* off, int nbins, uint32_t* flag, int64_t* pos, int64_t* partial, int* item_bin0,
-                 int* n_items, cudaStream_t s);
+int launch_items(const int64_t* off, int nbins, int cc, uint32_t* flag, int64_t* pos, int64_t* partial,
+                 int* item_bin0, int* n_items, cudaStream_t s);
 int launch_bin_offsets(const int32_t* key_sorted, int64_t n, int nbins, int64_t* off, cudaStream_t s);
 int launch_bin_keys(const Geom& g, const BinGeom& bg, const float* x, int64_t xs, int64_t n, int32_t* key, int* err,
                     cudaStream_t s);
