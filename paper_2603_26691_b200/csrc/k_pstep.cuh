@@ -22,7 +22,7 @@ __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
                 (scatter ? kRowBins * kSlots * 4 : 0) + 15) / 16 * 16);
 }
 
-template <bool SCATTER, bool ADVANCE, int BCM>
+template <bool SCATTER, bool ADVANCE, int BCM, int FEAT = 0xff>
 __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
   constexpr int SH = 3;   // chunk_cells == 8
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
           }
         }
       }
-      if (ADVANCE) {
+      if (ADVANCE && (FEAT & 1)) {
         const float d = dp;
         const float tau = a.p.tau_c * d * d;
         const float inv_tau = rcp_approx(tau);
@@ -179,8 +179,9 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
             c001 = __ldg(fb + pz); c101 = __ldg(fb + pz + 1);
             c011 = __ldg(fb + pz + g.gx); c111 = __ldg(fb + pz + g.gx + 1);
           }
-          const float4 uf = lerp4(lerp4(lerp4(c000, c100, fx), lerp4(c010, c110, fx), fy),
-                                  lerp4(lerp4(c001, c101, fx), lerp4(c011, c111, fx), fy), fz);
+          const float4 uf = (FEAT & 2) ? lerp4(lerp4(lerp4(c000, c100, fx), lerp4(c010, c110, fx), fy),
+                                               lerp4(lerp4(c001, c101, fx), lerp4(c011, c111, fx), fy), fz)
+                                       : make_float4(0.1f, 0.0f, 0.0f, 0.0f);   // ablation only
           const float sxv = uf.x - up0, syv = uf.y - up1, szv = uf.z - up2;
           const float Re = sqrt_approx(fmaf(sxv, sxv, fmaf(syv, syv, szv * szv))) * d * a.p.inv_nu;
           float f = 1.0f + 0.15f * exp2f(0.687f * __log2f(Re));
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
             up1 = un1;
             up2 = un2;
           }
-          if (a.p.two_way) {
+          if ((FEAT & 4) && a.p.two_way) {
             const int az = acc_z(g, c2);
             if (valid && az < 0) flags |= ERRF_WINDOW;
             const bool dep = valid && az >= 0;
@@ -245,8 +246,7 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
           if (bad && valid) flags |= ERRF_CFL;
         }
       }
-      // slot histogram of the end position w.r.t. the output bin (next rebin's input)
-      {
+      if (FEAT & 8) {   // slot histogram of the end position w.r.t. the output bin
         const int e0 = cell_from_t(cell_coord(xp0, g.lo[0], g.ih[0]), g.n[0]);
         const int e1 = cell_from_t(cell_coord(xp1, g.lo[1], g.ih[1]), g.n[1]);
         const int e2 = cell_from_t(cell_coord(xp2, g.lo[2], g.ih[2]), g.n[2]);
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
         const bool mover = write_ok && (((e0 >> SH) != (ox >> SH)) | ((e1 >> SH) != (oy >> SH)) | ((e2 >> SH) != (oz >> SH)));
         movers += mover ? 1u : 0u;
       }
-      if (write_ok) {
+      if ((FEAT & 16) && write_ok) {
         if (SCATTER) {
           const unsigned long long pid = S.id[(int)((p0 + base) & 1) + (r - base)];
           const Store& o = vside < 0 ? a.B : a.sbuf[vside];
