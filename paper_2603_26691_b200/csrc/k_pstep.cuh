@@ -12,6 +12,21 @@
 //  * 32-bit (bin, slot) keys for the rank and the histogram.
 #pragma once
 
+// Lanes holding the same key (what __match_any_sync returns), found by iterating
+// over the distinct keys with one SHFL + one VOTE each: cell-sorted warps hold few
+// distinct keys, and MATCH.ANY measured as the most expensive instruction of the
+// step (scripts/gpu_ablate.sh).  Invalid lanes share one key.
+__device__ __forceinline__ unsigned peers_of(int key) {
+  unsigned todo = kFull, mine = 0;
+  while (todo) {
+    const int k = __shfl_sync(kFull, key, __ffs(todo) - 1);
+    const unsigned m = __ballot_sync(kFull, key == k);
+    mine = (key == k) ? m : mine;
+    todo &= ~m;
+  }
+  return mine;
+}
+
 constexpr int kBoxX = 12, kBoxY = 5, kBoxZ = 5;            // (8 + 4) x 5 x 5 cells
 constexpr int kBoxCells = kBoxX * kBoxY * kBoxZ;           // 300 float4 = 4.8 KB
 constexpr int kRowBins = 8;
@@ -106,8 +121,8 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
           flags |= ERRF_SCATTER;
           write_ok = false;
         }
-        const int key = write_ok ? lb * kSlots + j : -1 - lane;
-        const unsigned peers = __match_any_sync(kFull, key);
+        const int key = write_ok ? lb * kSlots + j : -1;
+        const unsigned peers = peers_of(key);
         const int leader = __ffs(peers) - 1;
         int rbase = 0;
         if (lane == leader && key >= 0) {
@@ -224,11 +239,11 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
             const int az = acc_z(g, c2);
             if (valid && az < 0) flags |= ERRF_WINDOW;
             const bool dep = valid && az >= 0;
-            const int ckey = dep ? (az * g.n[1] + c1) * g.n[0] + c0 : -1 - lane;
+            const int ckey = dep ? (az * g.n[1] + c1) * g.n[0] + c0 : -1;
             const float ja = -mw * du0, jb = -mw * du1, jc = -mw * du2;
-            const unsigned peers = __match_any_sync(kFull, ckey);
+            // the group of lane 0's cell is reduced in registers; the rest red directly
             const int lead = __shfl_sync(kFull, ckey, 0);
-            const unsigned major = __shfl_sync(kFull, peers, 0);
+            const unsigned major = __ballot_sync(kFull, ckey == lead);
             if (__popc(major) >= 4 && lead >= 0) {
               const bool in = (major >> lane) & 1u;
               float ra = ja, rb = jb, rc = jc;
@@ -254,9 +269,12 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
         const int j2 = slot_of<BCM>(g, ox, oy, oz, e0, e1, e2);
         if (here && j2 < 0) farflag = 1;
         // 32-bit key (st_init checks nbins * 27 < 2^31)
-        const int hkey = (here && j2 >= 0) ? obin * kSlots + j2 : -1 - lane;
-        const unsigned peers = __match_any_sync(kFull, hkey);
-        if (hkey >= 0 && (peers & lanemask_lt()) == 0) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, __popc(peers));
+        const int hkey = (here && j2 >= 0) ? obin * kSlots + j2 : -1;
+        // lane 0's (bin, slot) group counts with one atomic; the others add 1 each
+        const int lead = __shfl_sync(kFull, hkey, 0);
+        const unsigned major = __ballot_sync(kFull, hkey == lead);
+        if (lane == 0 && lead >= 0) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, __popc(major));
+        if (hkey >= 0 && !((major >> lane) & 1u)) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, 1);
         const bool mover = write_ok && (((e0 >> SH) != (ox >> SH)) | ((e1 >> SH) != (oy >> SH)) | ((e2 >> SH) != (oz >> SH)));
         movers += mover ? 1u : 0u;
       }
