@@ -1,21 +1,22 @@
-// k_step v6 — instruction-lean step kernel (included by k_step.cu, which defines
-// the helpers: Stage/TMA pipeline, bin geometry, slots, reductions, physics bits).
+// k_step v7 — latency-lean step kernel for 8^3-cell chunks (included by k_step.cu,
+// which defines the helpers: Stage/TMA pipeline, bin geometry, slots, reductions).
 //
-// Differences from the generic loop, all aimed at issue slots per particle:
-//  * items are one chunk row (<= 8 consecutive bins when chunk_cells == 8);
-//  * the item's fluid neighbourhood (bin cells +-2: a 12 x 5 x 5 float4 box) is
-//    staged in shared memory once per item, so the 8 trilinear corners are 8
-//    LDS.128 with compile-time offsets; particles outside the box (only after a
-//    far move or multi-sub-step drift) take the global-memory path;
-//  * invalid lanes of a partial batch compute on a clamped copy of a valid
-//    particle and only their side effects are predicated off (no divergence);
-//  * 32-bit (bin, slot) keys for the rank and the histogram.
+// Measured on C5 (1e9 particles, scripts/gpu_ablate.sh): data movement alone runs
+// at ~86 % of HBM peak, so the step is bound by the per-batch dependency chain of
+// each warp.  This variant removes every global load from that chain:
+//  * items are one chunk row (<= 8 consecutive bins);
+//  * at item start the warp computes, for each (bin, slot) of the item, the base
+//    of its destination run (off_new[d] + base[j][s], or the send-buffer offset of a
+//    neighbour plane) into shared memory; a particle's destination is then
+//    smem base + run counter + rank — no dependent L2 loads per batch;
+//  * particle input arrives through a 2-stage TMA bulk pipeline (cp.async.bulk +
+//    mbarrier); the fluid corners are L1-cached __ldg loads (cell-coherent warps);
+//  * groups of equal keys use SHFL + VOTE (no MATCH.ANY); invalid lanes of a
+//    partial batch mirror a valid particle with predicated side effects.
 #pragma once
 
 // Lanes holding the same key (what __match_any_sync returns), found by iterating
-// over the distinct keys with one SHFL + one VOTE each: cell-sorted warps hold few
-// distinct keys, and MATCH.ANY measured as the most expensive instruction of the
-// step (scripts/gpu_ablate.sh).  Invalid lanes share one key.
+// over the distinct keys with one SHFL + one VOTE each; invalid lanes share one key.
 __device__ __forceinline__ unsigned peers_of(int key) {
   unsigned todo = kFull, mine = 0;
   while (todo) {
@@ -27,18 +28,17 @@ __device__ __forceinline__ unsigned peers_of(int key) {
   return mine;
 }
 
-constexpr int kBoxX = 12, kBoxY = 5, kBoxZ = 5;            // (8 + 4) x 5 x 5 cells
-constexpr int kBoxCells = kBoxX * kBoxY * kBoxZ;           // 300 float4 = 4.8 KB
 constexpr int kRowBins = 8;
-
-constexpr int kBarBytes = 32;                               // kStages mbarriers, padded to 16 B
+constexpr int kPStages = 2;
+constexpr int kBarBytes = 16;                               // kPStages mbarriers
 __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
-  return (int)((kStages * sizeof(Stage) + kBarBytes + kBoxCells * 16 + (kRowBins + 1) * 4 +
-                (scatter ? kRowBins * kSlots * 4 : 0) + 15) / 16 * 16);
+  return (int)((kPStages * sizeof(Stage) + kBarBytes +
+                (scatter ? kRowBins * kSlots * 8 + kRowBins * kSlots * 4 + kRowBins * kSlots : 0) +
+                (kRowBins + 1) * 4 + 15) / 16 * 16);
 }
 
 template <bool SCATTER, bool ADVANCE, int BCM, int FEAT = 0xff>
-__global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
+__global__ void __launch_bounds__(256, 4) k_pstep(StepArgs a) {
   constexpr int SH = 3;   // chunk_cells == 8
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geom& g = a.g;
@@ -46,10 +46,12 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
   const int wib = threadIdx.x >> 5;
   unsigned char* ws = smem_raw + (size_t)wib * pwarp_smem_bytes(SCATTER);
   Stage* stg = reinterpret_cast<Stage*>(ws);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kStages * sizeof(Stage));
-  float4* box = reinterpret_cast<float4*>(ws + kStages * sizeof(Stage) + kBarBytes);   // 16-byte aligned
-  int* rel = reinterpret_cast<int*>(box + kBoxCells);                         // [kRowBins+1]
-  int* run = rel + (kRowBins + 1);                                            // [kRowBins*27]
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kPStages * sizeof(Stage));
+  unsigned char* tail = ws + kPStages * sizeof(Stage) + kBarBytes;
+  long long* dbase = reinterpret_cast<long long*>(tail);                      // [8*27] destination run bases
+  int* run = reinterpret_cast<int*>(dbase + (SCATTER ? kRowBins * kSlots : 0));   // [8*27] run counters
+  signed char* dside = reinterpret_cast<signed char*>(run + (SCATTER ? kRowBins * kSlots : 0));  // [8*27]
+  int* rel = reinterpret_cast<int*>(tail + (SCATTER ? (kRowBins * kSlots * 13 + 15) / 16 * 16 : 0));  // [9]
   const int n_items = *a.n_items;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t cap = a.cap;
@@ -59,7 +61,7 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
   unsigned movers = 0;
   uint32_t phase = 0;
   if (lane == 0) {
-    for (int k = 0; k < kStages; ++k) mbar_init(bar + k, 1);
+    for (int k = 0; k < kPStages; ++k) mbar_init(bar + k, 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -70,33 +72,41 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
     const int nb = b1 - b0;                       // <= kRowBins, one chunk row
     const int64_t p0 = a.off[b0];
     if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
-    if (SCATTER)
-      for (int k = lane; k < nb * kSlots; k += 32) run[k] = 0;
-    // cell of the row's first bin; the row runs along +x
-    int rx, ry, rz;
+    int rx, ry, rz;                               // cell of the row's first bin (row along +x)
     cell_of_bin(g, a.bg, b0, rx, ry, rz);
-    const int bx0 = rx - 2, by0 = ry - 2, bz0 = rz - 2;
-    // stage the fluid neighbourhood (window indices clamped: cells outside the
-    // window are never read by a valid stencil)
-    for (int q = lane; q < kBoxCells; q += 32) {
-      const int qx = q % kBoxX, qy = (q / kBoxX) % kBoxY, qz = q / (kBoxX * kBoxY);
-      int wx = bx0 + qx + 1, wy = by0 + qy + 1, wz = window_z(g, bz0 + qz);
-      wx = min(max(wx, 0), g.gx - 1);
-      wy = min(max(wy, 0), g.gy - 1);
-      wz = wz < 0 ? (bz0 + qz < g.wz0 + 1 ? 0 : g.wnz - 1) : wz;
-      box[q] = __ldg(a.field + ((int64_t)wz * pz + wy * g.gx + wx));
+    if (SCATTER) {
+      // destination run bases of every (bin, slot) of the item
+      for (int k = lane; k < nb * kSlots; k += 32) {
+        const int lb = k / kSlots, j = k - lb * kSlots;
+        bool ok = true;
+        const int dx = axis_step(rx + lb, j % 3 - 1, g.n[0], g.bc[0], ok);
+        const int dy = axis_step(ry, (j / 3) % 3 - 1, g.n[1], g.bc[1], ok);
+        const int dz = axis_step(rz, j / 9 - 1, g.n[2], g.bc[2], ok);
+        long long db = -1;
+        signed char side = -1;
+        if (ok) {
+          const int within = a.slot_base[(int64_t)j * nbins + b0 + lb];
+          side = (dz == a.bg.vz[0]) ? 0 : ((dz == a.bg.vz[1]) ? 1 : -1);
+          if (side >= 0) db = a.voff[side][vbin_of_cell<SH>(g, dx, dy, 8)] + within;
+          else if ((dz >> 3) >= a.bg.kz0 && (dz >> 3) < a.bg.kz0 + a.bg.nkz)
+            db = a.off_new[bin_of_cell<SH>(g, a.bg, dx, dy, dz)] + within;
+        }
+        dbase[k] = db;
+        dside[k] = side;
+        run[k] = 0;
+      }
     }
     __syncwarp();
     const int np = rel[nb];
     const int nbatch = (np + 31) >> 5;
     if (lane == 0) {
       fence_proxy_async();
-      for (int k = 0; k < kStages && k < nbatch; ++k) stage_issue(stg + k, bar + k, a.A, cap, p0 + 32 * k, cap, SCATTER);
+      for (int k = 0; k < kPStages && k < nbatch; ++k) stage_issue(stg + k, bar + k, a.A, cap, p0 + 32 * k, cap, SCATTER);
     }
     int lb = 0;
     for (int bi = 0; bi < nbatch; ++bi) {
       const int base = bi << 5;
-      const int sk = bi % kStages;
+      const int sk = bi & (kPStages - 1);
       const bool valid = base + lane < np;
       const int r = valid ? base + lane : np - 1;          // invalid lanes mirror a valid particle
       while (rel[lb + 1] <= r) ++lb;
@@ -109,6 +119,14 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
       float xp0 = S.f[0][so], xp1 = S.f[1][so], xp2 = S.f[2][so];
       float up0 = S.f[3][so], up1 = S.f[4][so], up2 = S.f[5][so];
       const float dp = S.f[6][so], wp = S.f[7][so];
+      unsigned long long pid = 0;
+      if (SCATTER) pid = S.id[(int)((p0 + base) & 1) + (r - base)];
+      // the stage is consumed: refill it with the batch kPStages ahead
+      __syncwarp();
+      if (lane == 0 && bi + kPStages < nbatch) {
+        fence_proxy_async();
+        stage_issue(stg + sk, bar + sk, a.A, cap, p0 + 32 * (bi + kPStages), cap, SCATTER);
+      }
       float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
             t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
       int c0 = cell_from_t(t0, g.n[0]), c1 = cell_from_t(t1, g.n[1]), c2 = cell_from_t(t2, g.n[2]);
@@ -117,11 +135,13 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
       bool write_ok = valid;
       if (SCATTER) {
         const int j = slot_of<BCM>(g, sx, sy, sz, c0, c1, c2);
-        if (valid && j < 0) {
+        const int k = lb * kSlots + (j < 0 ? kStay : j);
+        const long long db = dbase[k];
+        if (valid && (j < 0 || db < 0)) {
           flags |= ERRF_SCATTER;
           write_ok = false;
         }
-        const int key = write_ok ? lb * kSlots + j : -1;
+        const int key = write_ok ? k : -1;
         const unsigned peers = peers_of(key);
         const int leader = __ffs(peers) - 1;
         int rbase = 0;
@@ -134,22 +154,12 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
         ox = c0;
         oy = c1;
         oz = c2;
-        const int jj = j < 0 ? kStay : j;
-        const int within = a.slot_base[(int64_t)jj * nbins + s] + rbase;
-        vside = (c2 == a.bg.vz[0]) ? 0 : ((c2 == a.bg.vz[1]) ? 1 : -1);
-        if (vside >= 0) {
-          dest = a.voff[vside][vbin_of_cell<SH>(g, c0, c1, 8)] + within;
-          if (write_ok && (dest < 0 || dest >= a.scap)) {
-            flags |= ERRF_SCATTER;
-            write_ok = false;
-          }
-        } else {
-          obin = bin_of_cell<SH>(g, a.bg, ox, oy, oz);
-          dest = a.off_new[obin] + within;
-          if (write_ok && (dest < 0 || dest >= a.n)) {
-            flags |= ERRF_SCATTER;
-            write_ok = false;
-          }
+        vside = dside[k];
+        dest = db + rbase;
+        if (vside < 0) obin = bin_of_cell<SH>(g, a.bg, ox, oy, oz);
+        if (write_ok && (dest < 0 || dest >= (vside < 0 ? a.n : a.scap))) {
+          flags |= ERRF_SCATTER;
+          write_ok = false;
         }
       }
       if (ADVANCE && (FEAT & 1)) {
@@ -173,30 +183,21 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
           stencil_from_cell(t0, c0, ix, fx);
           stencil_from_cell(t1, c1, iy, fy);
           stencil_from_cell(t2, c2, iz, fz);
-          const int qx = ix - bx0, qy = iy - by0, qz = iz - bz0;
-          float4 c000, c100, c010, c110, c001, c101, c011, c111;
-          if ((unsigned)qx < (unsigned)(kBoxX - 1) && (unsigned)qy < (unsigned)(kBoxY - 1) &&
-              (unsigned)qz < (unsigned)(kBoxZ - 1)) {
-            const float4* q = box + (qz * kBoxY + qy) * kBoxX + qx;
-            c000 = q[0]; c100 = q[1];
-            c010 = q[kBoxX]; c110 = q[kBoxX + 1];
-            c001 = q[kBoxX * kBoxY]; c101 = q[kBoxX * kBoxY + 1];
-            c011 = q[kBoxX * kBoxY + kBoxX]; c111 = q[kBoxX * kBoxY + kBoxX + 1];
-          } else {   // outside the staged box: global path (window-checked)
-            int wz = window_z(g, iz);
-            if (wz < 0 || wz + 1 >= g.wnz) {
-              if (valid) flags |= ERRF_WINDOW;
-              wz = wz < 0 ? 0 : g.wnz - 2;
-            }
-            const float4* fb = a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
-            c000 = __ldg(fb); c100 = __ldg(fb + 1);
-            c010 = __ldg(fb + g.gx); c110 = __ldg(fb + g.gx + 1);
-            c001 = __ldg(fb + pz); c101 = __ldg(fb + pz + 1);
-            c011 = __ldg(fb + pz + g.gx); c111 = __ldg(fb + pz + g.gx + 1);
+          int wz = window_z(g, iz);
+          if (wz < 0 || wz + 1 >= g.wnz) {
+            if (valid) flags |= ERRF_WINDOW;
+            wz = wz < 0 ? 0 : g.wnz - 2;
           }
-          const float4 uf = (FEAT & 2) ? lerp4(lerp4(lerp4(c000, c100, fx), lerp4(c010, c110, fx), fy),
-                                               lerp4(lerp4(c001, c101, fx), lerp4(c011, c111, fx), fy), fz)
-                                       : make_float4(0.1f, 0.0f, 0.0f, 0.0f);   // ablation only
+          float4 uf = make_float4(0.1f, 0.0f, 0.0f, 0.0f);   // (ablation value)
+          if (FEAT & 2) {
+            const float4* fb = a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
+            const float4 c000 = __ldg(fb), c100 = __ldg(fb + 1);
+            const float4 c010 = __ldg(fb + g.gx), c110 = __ldg(fb + g.gx + 1);
+            const float4 c001 = __ldg(fb + pz), c101 = __ldg(fb + pz + 1);
+            const float4 c011 = __ldg(fb + pz + g.gx), c111 = __ldg(fb + pz + g.gx + 1);
+            uf = lerp4(lerp4(lerp4(c000, c100, fx), lerp4(c010, c110, fx), fy),
+                       lerp4(lerp4(c001, c101, fx), lerp4(c011, c111, fx), fy), fz);
+          }
           const float sxv = uf.x - up0, syv = uf.y - up1, szv = uf.z - up2;
           const float Re = sqrt_approx(fmaf(sxv, sxv, fmaf(syv, syv, szv * szv))) * d * a.p.inv_nu;
           float f = 1.0f + 0.15f * exp2f(0.687f * __log2f(Re));
@@ -206,8 +207,10 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
           const float h = dt * f * inv_tau;
           float du0, du1, du2;
           if (a.p.integrator == ST_INT_EXPONENTIAL) {
-            float E, M;
-            exp_pair(h, E, M);
+            // E = exp(-h); M = 1 - E (series below h = 1/8): both evaluated, selected
+            const float E = __expf(-h);
+            const float Ms = h * (1.0f - h * (0.5f - h * (1.0f / 6.0f - h * (1.0f / 24.0f - h * (1.0f / 120.0f - h * (1.0f / 720.0f))))));
+            const float M = h < 0.125f ? Ms : 1.0f - E;
             const float tM = taue * M;
             const float us0 = fmaf(gx, taue, uf.x), us1 = fmaf(gy, taue, uf.y), us2 = fmaf(gz, taue, uf.z);
             const float r0 = up0 - us0, r1 = up1 - us1, r2 = up2 - us2;
@@ -268,7 +271,6 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
         const bool here = write_ok && vside < 0;
         const int j2 = slot_of<BCM>(g, ox, oy, oz, e0, e1, e2);
         if (here && j2 < 0) farflag = 1;
-        // 32-bit key (st_init checks nbins * 27 < 2^31)
         const int hkey = (here && j2 >= 0) ? obin * kSlots + j2 : -1;
         // lane 0's (bin, slot) group counts with one atomic; the others add 1 each
         const int lead = __shfl_sync(kFull, hkey, 0);
@@ -280,7 +282,6 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
       }
       if ((FEAT & 16) && write_ok) {
         if (SCATTER) {
-          const unsigned long long pid = S.id[(int)((p0 + base) & 1) + (r - base)];
           const Store& o = vside < 0 ? a.B : a.sbuf[vside];
           const int64_t oc = vside < 0 ? cap : a.scap;
           o.x[dest] = xp0; o.x[oc + dest] = xp1; o.x[2 * oc + dest] = xp2;
@@ -292,11 +293,6 @@ __global__ void __launch_bounds__(256, 3) k_pstep(StepArgs a) {
           __stcs(a.A.x + dest, xp0); __stcs(a.A.x + cap + dest, xp1); __stcs(a.A.x + 2 * cap + dest, xp2);
           __stcs(a.A.u + dest, up0); __stcs(a.A.u + cap + dest, up1); __stcs(a.A.u + 2 * cap + dest, up2);
         }
-      }
-      __syncwarp();
-      if (lane == 0 && bi + kStages < nbatch) {
-        fence_proxy_async();
-        stage_issue(stg + sk, bar + sk, a.A, cap, p0 + 32 * (bi + kStages), cap, SCATTER);
       }
     }
     __syncwarp();
