@@ -38,7 +38,7 @@ __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
 }
 
 template <bool SCATTER, bool ADVANCE, int BCM, int FEAT = 0xff>
-__global__ void __launch_bounds__(256, 4) k_pstep(StepArgs a) {
+__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(StepArgs a) {
   constexpr int SH = 3;   // chunk_cells == 8
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geom& g = a.g;
