@@ -31,10 +31,11 @@ __device__ __forceinline__ unsigned peers_of(int key) {
 constexpr int kRowBins = 8;
 constexpr int kPStages = 2;
 constexpr int kBarBytes = 16;                               // kPStages mbarriers
+// per-warp slice: stages | mbarriers | [scatter: dbase i64, run i32, side i8 — padded to 16] | rel[9]
+constexpr int kScatterTable = (kRowBins * kSlots * 13 + 15) / 16 * 16;
 __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
-  return (int)((kPStages * sizeof(Stage) + kBarBytes +
-                (scatter ? kRowBins * kSlots * 8 + kRowBins * kSlots * 4 + kRowBins * kSlots : 0) +
-                (kRowBins + 1) * 4 + 15) / 16 * 16);
+  return (int)((kPStages * sizeof(Stage) + kBarBytes + (scatter ? kScatterTable : 0) + (kRowBins + 1) * 4 + 15) /
+               16 * 16);
 }
 
 template <bool SCATTER, bool ADVANCE, int BCM, int FEAT = 0xff>
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(Ste
   long long* dbase = reinterpret_cast<long long*>(tail);                      // [8*27] destination run bases
   int* run = reinterpret_cast<int*>(dbase + (SCATTER ? kRowBins * kSlots : 0));   // [8*27] run counters
   signed char* dside = reinterpret_cast<signed char*>(run + (SCATTER ? kRowBins * kSlots : 0));  // [8*27]
-  int* rel = reinterpret_cast<int*>(tail + (SCATTER ? (kRowBins * kSlots * 13 + 15) / 16 * 16 : 0));  // [9]
+  int* rel = reinterpret_cast<int*>(tail + (SCATTER ? kScatterTable : 0));  // [kRowBins+1]
   const int n_items = *a.n_items;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t cap = a.cap;
