@@ -245,18 +245,24 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(Ste
             const bool dep = valid && az >= 0;
             const int ckey = dep ? (az * g.n[1] + c1) * g.n[0] + c0 : -1;
             const float ja = -mw * du0, jb = -mw * du1, jc = -mw * du2;
-            // the group of lane 0's cell is reduced in registers; the rest red directly
-            const int lead = __shfl_sync(kFull, ckey, 0);
-            const unsigned major = __ballot_sync(kFull, ckey == lead);
-            if (__popc(major) >= 4 && lead >= 0) {
-              const bool in = (major >> lane) & 1u;
+            // anchors: the bin cells of lanes 0 and 31 (the first and last bin of the
+            // batch) — their stayers, the bulk of a cell-sorted warp, are reduced in
+            // registers with one red per anchor; the other lanes red individually
+            const int bk = (acc_z(g, sz) * g.n[1] + sy) * g.n[0] + sx;
+            const int kA = __shfl_sync(kFull, bk, 0), kB = __shfl_sync(kFull, bk, 31);
+            const bool inA = dep && ckey == kA, inB = dep && kB != kA && ckey == kB;
+            const unsigned mA = __ballot_sync(kFull, inA), mB = __ballot_sync(kFull, inB);
+            if (mA) {
               float ra = ja, rb = jb, rc = jc;
-              group_sum3(in, ra, rb, rc);
-              if (lane == 0) red_add_v4(a.acc + lead, ra, rb, rc);
-              if (!in && dep) red_add_v4(a.acc + ckey, ja, jb, jc);
-            } else if (dep) {
-              red_add_v4(a.acc + ckey, ja, jb, jc);
+              group_sum3(inA, ra, rb, rc);
+              if (lane == 0) red_add_v4(a.acc + kA, ra, rb, rc);
             }
+            if (mB) {
+              float ra = ja, rb = jb, rc = jc;
+              group_sum3(inB, ra, rb, rc);
+              if (lane == 31) red_add_v4(a.acc + kB, ra, rb, rc);
+            }
+            if (dep && !inA && !inB) red_add_v4(a.acc + ckey, ja, jb, jc);
           }
           bool bad = false;
           bad |= apply_bc(periodic<BCM>(g, 0) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[0], g.hi[0], g.L[0], xp0, up0);
@@ -273,11 +279,15 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(Ste
         const int j2 = slot_of<BCM>(g, ox, oy, oz, e0, e1, e2);
         if (here && j2 < 0) farflag = 1;
         const int hkey = (here && j2 >= 0) ? obin * kSlots + j2 : -1;
-        // lane 0's (bin, slot) group counts with one atomic; the others add 1 each
-        const int lead = __shfl_sync(kFull, hkey, 0);
-        const unsigned major = __ballot_sync(kFull, hkey == lead);
-        if (lane == 0 && lead >= 0) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, __popc(major));
-        if (hkey >= 0 && !((major >> lane) & 1u)) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, 1);
+        // anchors: (bin, stay) of lanes 0 and 31 — one atomic per anchor group; the
+        // remaining lanes (cell movers) add 1 each
+        const int hb = s * kSlots + kStay;
+        const int hA = __shfl_sync(kFull, hb, 0), hB = __shfl_sync(kFull, hb, 31);
+        const bool inA = hkey == hA, inB = hkey == hB && hB != hA;
+        const unsigned mA = __ballot_sync(kFull, inA), mB = __ballot_sync(kFull, inB);
+        if (lane == 0 && mA) atomicAdd(a.hist_next + (int64_t)kStay * nbins + hA / kSlots, __popc(mA));
+        if (lane == 31 && mB) atomicAdd(a.hist_next + (int64_t)kStay * nbins + hB / kSlots, __popc(mB));
+        if (hkey >= 0 && !inA && !inB) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, 1);
         const bool mover = write_ok && (((e0 >> SH) != (ox >> SH)) | ((e1 >> SH) != (oy >> SH)) | ((e2 >> SH) != (oz >> SH)));
         movers += mover ? 1u : 0u;
       }
