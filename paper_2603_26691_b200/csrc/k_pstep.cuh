@@ -1,23 +1,25 @@
-// k_step v7 — latency-lean step kernel for 8^3-cell chunks (included by k_step.cu,
-// which defines the helpers: Stage/TMA pipeline, bin geometry, slots, reductions).
+// k_step v8 — issue-lean step kernel for 8^3-cell chunks (included by k_step.cu,
+// which defines the helpers: bin geometry, slots, reductions, mbarrier helpers).
 //
-// Measured on C5 (1e9 particles, scripts/gpu_ablate.sh): data movement alone runs
-// at ~86 % of HBM peak, so the step is bound by the per-batch dependency chain of
-// each warp.  This variant removes every global load from that chain:
-//  * items are one chunk row (<= 8 consecutive bins);
-//  * at item start the warp computes, for each (bin, slot) of the item, the base
-//    of its destination run (off_new[d] + base[j][s], or the send-buffer offset of a
-//    neighbour plane) into shared memory; a particle's destination is then
-//    smem base + run counter + rank — no dependent L2 loads per batch;
-//  * particle input arrives through a 2-stage TMA bulk pipeline (cp.async.bulk +
-//    mbarrier); the fluid corners are L1-cached __ldg loads (cell-coherent warps);
-//  * groups of equal keys use SHFL + VOTE (no MATCH.ANY); invalid lanes of a
-//    partial batch mirror a valid particle with predicated side effects.
+// Measured on C5 (scripts/gpu_ablate.sh, profiles/README.md): data movement alone
+// runs near the HBM roofline, so the step is bound by instruction issue per
+// 32-particle batch.  v8 cuts the per-batch work of each warp:
+//  * particle input: ONE 2-D TMA tensor copy of the 8 float rows (x0 x1 x2 u0 u1 u2
+//    d w, contiguous rows of stride cap) + one copy of the ids per batch,
+//    through a per-warp mbarrier pipeline (no per-array bulk copies);
+//  * items are one chunk row (<= 8 bins); at item start the warp computes, for each
+//    (bin, slot), the base of its destination run (off_new[d] + base[j][s], or the
+//    send-buffer offset of a neighbour plane) into shared memory;
+//  * stayers (end cell == bin cell, the bulk of a cell-sorted warp): rank from
+//    segment ballots (lanes of one bin are contiguous), deposit and slot count
+//    accumulated in registers per lane and flushed once per (lane, bin);
+//  * movers: rank via MATCH.ANY over (bin, slot), individual red / atomic.
 #pragma once
 
-// Lanes holding the same key (what __match_any_sync returns), found by iterating
-// over the distinct keys with one SHFL + one VOTE each; invalid lanes share one key.
-__device__ __forceinline__ unsigned peers_of(int key) {
+#ifndef ST_DBG
+#define ST_DBG 0
+#endif
+__device__ __forceinline__ unsigned dbg_peers(int key) {
   unsigned todo = kFull, mine = 0;
   while (todo) {
     const int k = __shfl_sync(kFull, key, __ffs(todo) - 1);
@@ -27,37 +29,75 @@ __device__ __forceinline__ unsigned peers_of(int key) {
   }
   return mine;
 }
+__device__ __forceinline__ int dbg_sum(int v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
 
 constexpr int kRowBins = 8;
-constexpr int kPStages = 2;
-constexpr int kBarBytes = 16;                               // kPStages mbarriers
-// per-warp slice: stages | mbarriers | [scatter: dbase i64, run i32, side i8 — padded to 16] | rel[9]
+constexpr int kPStages = 3;
+// A tensor-copy box must start 16-byte aligned along the inner dimension (a
+// misaligned start traps as an illegal instruction — measured, scripts/tma_probe.cu),
+// so a batch at store index i0 is staged from i0 & ~3 (floats) / i0 & ~1 (ids) with
+// 4 / 2 elements of slack.
+constexpr int kBoxF = 36, kBoxI = 34;
+struct alignas(128) TStage {
+  float f[8][kBoxF];                // box {36, 8} of the float rows
+  unsigned long long id[kBoxI];     // box {34, 1} of the ids (offset 1152: 128-B aligned)
+};
+constexpr int kTStageBytes = (int)sizeof(TStage);                   // 1536
+constexpr uint32_t kTxF = 8 * kBoxF * 4, kTxI = kBoxI * 8;
 constexpr int kScatterTable = (kRowBins * kSlots * 13 + 15) / 16 * 16;
+// per-warp slice: stages | mbarriers | [scatter: dbase i64, run i32, side i8] | rel[9]; 128-B multiple
 __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
-  return (int)((kPStages * sizeof(Stage) + kBarBytes + (scatter ? kScatterTable : 0) + (kRowBins + 1) * 4 + 15) /
-               16 * 16);
+  return (kPStages * kTStageBytes + 8 * kPStages + (scatter ? kScatterTable : 0) + (kRowBins + 1) * 4 + 127) / 128 *
+         128;
+}
+constexpr int kPSmemAlign = 128;   // slack for aligning the dynamic smem base
+
+__device__ __forceinline__ void tma_rows(void* dst, const void* tmap, int c0, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_ids(void* dst, const void* tmap, int c0, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tstage_issue(TStage* st, unsigned long long* bar, const void* tm_f, const void* tm_id,
+                                             int i0, bool with_id) {
+  mbar_expect_tx(bar, with_id ? kTxF + kTxI : kTxF);
+  tma_rows(st->f, tm_f, i0 & ~3, bar);
+  if (with_id) tma_ids(st->id, tm_id, i0 & ~1, bar);
 }
 
 template <bool SCATTER, bool ADVANCE, int BCM, int FEAT = 0xff>
-__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(StepArgs a) {
+__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(const __grid_constant__ StepArgs a) {
   constexpr int SH = 3;   // chunk_cells == 8
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char psmem_raw[];
   const Geom& g = a.g;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  unsigned char* ws = smem_raw + (size_t)wib * pwarp_smem_bytes(SCATTER);
-  Stage* stg = reinterpret_cast<Stage*>(ws);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kPStages * sizeof(Stage));
-  unsigned char* tail = ws + kPStages * sizeof(Stage) + kBarBytes;
-  long long* dbase = reinterpret_cast<long long*>(tail);                      // [8*27] destination run bases
-  int* run = reinterpret_cast<int*>(dbase + (SCATTER ? kRowBins * kSlots : 0));   // [8*27] run counters
-  signed char* dside = reinterpret_cast<signed char*>(run + (SCATTER ? kRowBins * kSlots : 0));  // [8*27]
-  int* rel = reinterpret_cast<int*>(tail + (SCATTER ? kScatterTable : 0));  // [kRowBins+1]
+  unsigned char* sbase = psmem_raw + ((kPSmemAlign - (smem_u32(psmem_raw) & (kPSmemAlign - 1))) & (kPSmemAlign - 1));
+  unsigned char* ws = sbase + (size_t)wib * pwarp_smem_bytes(SCATTER);
+  TStage* stg = reinterpret_cast<TStage*>(ws);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kPStages * kTStageBytes);
+  unsigned char* tail = ws + kPStages * kTStageBytes + 8 * kPStages;
+  long long* dbase = reinterpret_cast<long long*>(tail);                                 // [8*27]
+  int* run = reinterpret_cast<int*>(dbase + (SCATTER ? kRowBins * kSlots : 0));          // [8*27]
+  signed char* dside = reinterpret_cast<signed char*>(run + (SCATTER ? kRowBins * kSlots : 0));
+  int* rel = reinterpret_cast<int*>(tail + (SCATTER ? kScatterTable : 0));               // [kRowBins+1]
   const int n_items = *a.n_items;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t cap = a.cap;
   const int nbins = a.nbins;
   const int pz = g.gy * g.gx;
+  const bool two_way = (FEAT & 4) && a.p.two_way;
   int flags = 0, farflag = 0;
   unsigned movers = 0;
   uint32_t phase = 0;
@@ -72,62 +112,109 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(Ste
     const int b1 = (item + 1 < n_items) ? a.item_bin0[item + 1] : nbins;
     const int nb = b1 - b0;                       // <= kRowBins, one chunk row
     const int64_t p0 = a.off[b0];
+    const int64_t pe = a.off[b1];
+    const int np = (int)(pe - p0);
+    const int nbatch = (np + 31) >> 5;
+    // prime the pipeline first: its latency overlaps the table set-up below
+    if (lane == 0 && !(ST_DBG & 16)) {
+      fence_proxy_async();
+      for (int k = 0; k < kPStages && k < nbatch; ++k)
+        tstage_issue(stg + k, bar + k, &a.tm_f, &a.tm_id, (int)(p0 + 32 * k), SCATTER && !(ST_DBG & 4));
+    }
+    __syncwarp();
     if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
     int rx, ry, rz;                               // cell of the row's first bin (row along +x)
     cell_of_bin(g, a.bg, b0, rx, ry, rz);
     if (SCATTER) {
       // destination run bases of every (bin, slot) of the item
-      for (int k = lane; k < nb * kSlots; k += 32) {
-        const int lb = k / kSlots, j = k - lb * kSlots;
-        bool ok = true;
-        const int dx = axis_step(rx + lb, j % 3 - 1, g.n[0], g.bc[0], ok);
-        const int dy = axis_step(ry, (j / 3) % 3 - 1, g.n[1], g.bc[1], ok);
-        const int dz = axis_step(rz, j / 9 - 1, g.n[2], g.bc[2], ok);
-        long long db = -1;
-        signed char side = -1;
-        if (ok) {
-          const int within = a.slot_base[(int64_t)j * nbins + b0 + lb];
-          side = (dz == a.bg.vz[0]) ? 0 : ((dz == a.bg.vz[1]) ? 1 : -1);
-          if (side >= 0) db = a.voff[side][vbin_of_cell<SH>(g, dx, dy, 8)] + within;
-          else if ((dz >> 3) >= a.bg.kz0 && (dz >> 3) < a.bg.kz0 + a.bg.nkz)
-            db = a.off_new[bin_of_cell<SH>(g, a.bg, dx, dy, dz)] + within;
+#pragma unroll
+      for (int it = 0; it < (kRowBins * kSlots + 31) / 32; ++it) {
+        const int k = lane + 32 * it;
+        if (k < nb * kSlots) {
+          const int lb = k / kSlots, j = k - lb * kSlots;
+          bool ok = true;
+          const int dx = axis_step(rx + lb, j % 3 - 1, g.n[0], g.bc[0], ok);
+          const int dy = axis_step(ry, (j / 3) % 3 - 1, g.n[1], g.bc[1], ok);
+          const int dz = axis_step(rz, j / 9 - 1, g.n[2], g.bc[2], ok);
+          long long db = -1;
+          signed char side = -1;
+          if (ok) {
+            const int within = a.slot_base[(int64_t)j * nbins + b0 + lb];
+            side = (dz == a.bg.vz[0]) ? 0 : ((dz == a.bg.vz[1]) ? 1 : -1);
+            if (side >= 0) db = a.voff[side][vbin_of_cell<SH>(g, dx, dy, 8)] + within;
+            else if ((dz >> 3) >= a.bg.kz0 && (dz >> 3) < a.bg.kz0 + a.bg.nkz)
+              db = a.off_new[bin_of_cell<SH>(g, a.bg, dx, dy, dz)] + within;
+          }
+          dbase[k] = db;
+          dside[k] = side;
+          run[k] = 0;
         }
-        dbase[k] = db;
-        dside[k] = side;
-        run[k] = 0;
       }
     }
     __syncwarp();
-    const int np = rel[nb];
-    const int nbatch = (np + 31) >> 5;
-    if (lane == 0) {
-      fence_proxy_async();
-      for (int k = 0; k < kPStages && k < nbatch; ++k) stage_issue(stg + k, bar + k, a.A, cap, p0 + 32 * k, cap, SCATTER);
-    }
+    const int az_row = acc_z(g, rz);
     int lb = 0;
-    for (int bi = 0; bi < nbatch; ++bi) {
+    // per-lane stayer accumulators of bin st_lb: deposit (da*) and slot count (hcnt)
+    int st_lb = -1, hcnt = 0;
+    float da0 = 0.f, da1 = 0.f, da2 = 0.f;
+    int carry_lb = -1, carry = 0;                 // stayers of bin carry_lb placed by earlier batches
+    for (int bi = 0; bi <= nbatch; ++bi) {
+      const bool last = bi == nbatch;             // extra pass: flush only
       const int base = bi << 5;
-      const int sk = bi & (kPStages - 1);
-      const bool valid = base + lane < np;
-      const int r = valid ? base + lane : np - 1;          // invalid lanes mirror a valid particle
-      while (rel[lb + 1] <= r) ++lb;
+      const bool valid = !last && base + lane < np;
+      const int r = valid ? base + lane : np - 1;            // invalid lanes mirror a valid particle
+      if (!last)
+        while (rel[lb + 1] <= r) ++lb;
+      // flush the stayer accumulators of lanes whose bin changed (one group per bin)
+      {
+        const bool fl = !(ST_DBG & 8) && st_lb >= 0 && (last || lb != st_lb);
+        unsigned todo = __ballot_sync(kFull, fl);
+        while (todo) {
+          const int ld = __ffs(todo) - 1;
+          const int kb = __shfl_sync(kFull, st_lb, ld);
+          const bool in = fl && st_lb == kb;
+          todo &= ~__ballot_sync(kFull, in);
+          const int hc = (ST_DBG & 2) ? dbg_sum(in ? hcnt : 0) : (int)__reduce_add_sync(kFull, in ? (unsigned)hcnt : 0u);
+          if (two_way) {
+            float ra = da0, rb = da1, rc = da2;
+            group_sum3(in, ra, rb, rc);
+            if (lane == ld) red_add_v4(a.acc + ((int64_t)az_row * g.n[1] + ry) * g.n[0] + rx + kb, ra, rb, rc);
+          }
+          if ((FEAT & 8) && lane == ld && hc) atomicAdd(a.hist_next + (int64_t)kStay * nbins + b0 + kb, hc);
+        }
+        if (fl || st_lb < 0) {
+          st_lb = lb;
+          hcnt = 0;
+          da0 = da1 = da2 = 0.f;
+        }
+      }
+      if (last) break;
+      const int sk = bi % kPStages;
       const int s = b0 + lb;
       const int sx = rx + lb, sy = ry, sz = rz;             // bin cell (row along x)
-      mbar_wait(bar + sk, (phase >> sk) & 1u);
+      if (!(ST_DBG & 16)) mbar_wait(bar + sk, (phase >> sk) & 1u);
+      __syncwarp();
       phase ^= 1u << sk;
-      const Stage& S = stg[sk];
-      const int so = (int)((p0 + base) & 3) + (r - base);
+      const TStage& S = stg[sk];
+      const int so = (int)((p0 + base) & 3) + (r - base);   // slot in the aligned-down box
       float xp0 = S.f[0][so], xp1 = S.f[1][so], xp2 = S.f[2][so];
       float up0 = S.f[3][so], up1 = S.f[4][so], up2 = S.f[5][so];
-      const float dp = S.f[6][so], wp = S.f[7][so];
+      float dp = S.f[6][so], wp = S.f[7][so];
+      if (ST_DBG & 16) {
+        const int64_t q = p0 + r;
+        xp0 = a.A.x[q]; xp1 = a.A.x[cap + q]; xp2 = a.A.x[2 * cap + q];
+        up0 = a.A.u[q]; up1 = a.A.u[cap + q]; up2 = a.A.u[2 * cap + q];
+        dp = a.A.d[q]; wp = a.A.w[q];
+      }
       unsigned long long pid = 0;
-      if (SCATTER) pid = S.id[(int)((p0 + base) & 1) + (r - base)];
+      if (SCATTER) pid = (ST_DBG & 4) ? a.A.id[p0 + r] : S.id[(int)((p0 + base) & 1) + (r - base)];
       // the stage is consumed: refill it with the batch kPStages ahead
       __syncwarp();
-      if (lane == 0 && bi + kPStages < nbatch) {
+      if (lane == 0 && bi + kPStages < nbatch && !(ST_DBG & 16)) {
         fence_proxy_async();
-        stage_issue(stg + sk, bar + sk, a.A, cap, p0 + 32 * (bi + kPStages), cap, SCATTER);
+        tstage_issue(stg + sk, bar + sk, &a.tm_f, &a.tm_id, (int)(p0 + 32 * (bi + kPStages)), SCATTER && !(ST_DBG & 4));
       }
+      __syncwarp();
       float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
             t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
       int c0 = cell_from_t(t0, g.n[0]), c1 = cell_from_t(t1, g.n[1]), c2 = cell_from_t(t2, g.n[2]);
@@ -142,15 +229,32 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(Ste
           flags |= ERRF_SCATTER;
           write_ok = false;
         }
-        const int key = write_ok ? k : -1;
-        const unsigned peers = peers_of(key);
-        const int leader = __ffs(peers) - 1;
-        int rbase = 0;
-        if (lane == leader && key >= 0) {
-          rbase = run[key];
-          run[key] = rbase + __popc(peers);
+        const bool stay = write_ok && j == kStay;
+        // stayers: rank inside the lane's bin segment (lanes of one bin are contiguous)
+        const unsigned mstay = __ballot_sync(kFull, stay);
+        const int lb_up = __shfl_up_sync(kFull, lb, 1);
+        const unsigned starts = __ballot_sync(kFull, lane == 0 || lb != lb_up);
+        const unsigned lt = lanemask_lt();
+        const int ss = 31 - __clz(starts & (lt | (1u << lane)));
+        int rbase = (lb == carry_lb ? carry : 0) + __popc(mstay & lt & ~((1u << ss) - 1u));
+        {
+          const int lb31 = __shfl_sync(kFull, lb, 31);
+          const int ss31 = 31 - __clz(starts);
+          carry = (lb31 == carry_lb ? carry : 0) + __popc(mstay & ~((1u << ss31) - 1u));
+          carry_lb = lb31;
         }
-        rbase = __shfl_sync(kFull, rbase, leader) + __popc(peers & lanemask_lt());
+        // movers: groups of equal (bin, slot) keys
+        const int key = (write_ok && !stay) ? k : -1;
+        const unsigned peers = (ST_DBG & 1) ? dbg_peers(key) : __match_any_sync(kFull, key);
+        if (key >= 0) {
+          const int leader = __ffs(peers) - 1;
+          int rb0 = 0;
+          if (lane == leader) {
+            rb0 = run[key];
+            run[key] = rb0 + __popc(peers);
+          }
+          rbase = __shfl_sync(peers, rb0, leader) + __popc(peers & lt);
+        }
         __syncwarp();
         ox = c0;
         oy = c1;
@@ -239,30 +343,19 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(Ste
             up1 = un1;
             up2 = un2;
           }
-          if ((FEAT & 4) && a.p.two_way) {
+          if (two_way) {
+            // reaction into the sub-step start cell (Eq. 11); the bin cell's share is
+            // accumulated in registers, other cells take an individual red
             const int az = acc_z(g, c2);
             if (valid && az < 0) flags |= ERRF_WINDOW;
-            const bool dep = valid && az >= 0;
-            const int ckey = dep ? (az * g.n[1] + c1) * g.n[0] + c0 : -1;
             const float ja = -mw * du0, jb = -mw * du1, jc = -mw * du2;
-            // anchors: the bin cells of lanes 0 and 31 (the first and last bin of the
-            // batch) — their stayers, the bulk of a cell-sorted warp, are reduced in
-            // registers with one red per anchor; the other lanes red individually
-            const int bk = (acc_z(g, sz) * g.n[1] + sy) * g.n[0] + sx;
-            const int kA = __shfl_sync(kFull, bk, 0), kB = __shfl_sync(kFull, bk, 31);
-            const bool inA = dep && ckey == kA, inB = dep && kB != kA && ckey == kB;
-            const unsigned mA = __ballot_sync(kFull, inA), mB = __ballot_sync(kFull, inB);
-            if (mA) {
-              float ra = ja, rb = jb, rc = jc;
-              group_sum3(inA, ra, rb, rc);
-              if (lane == 0) red_add_v4(a.acc + kA, ra, rb, rc);
+            if (valid && c0 == sx && c1 == sy && c2 == sz) {
+              da0 += ja;
+              da1 += jb;
+              da2 += jc;
+            } else if (valid && az >= 0) {
+              red_add_v4(a.acc + ((int64_t)az * g.n[1] + c1) * g.n[0] + c0, ja, jb, jc);
             }
-            if (mB) {
-              float ra = ja, rb = jb, rc = jc;
-              group_sum3(inB, ra, rb, rc);
-              if (lane == 31) red_add_v4(a.acc + kB, ra, rb, rc);
-            }
-            if (dep && !inA && !inB) red_add_v4(a.acc + ckey, ja, jb, jc);
           }
           bool bad = false;
           bad |= apply_bc(periodic<BCM>(g, 0) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[0], g.hi[0], g.L[0], xp0, up0);
@@ -278,16 +371,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(Ste
         const bool here = write_ok && vside < 0;
         const int j2 = slot_of<BCM>(g, ox, oy, oz, e0, e1, e2);
         if (here && j2 < 0) farflag = 1;
-        const int hkey = (here && j2 >= 0) ? obin * kSlots + j2 : -1;
-        // anchors: (bin, stay) of lanes 0 and 31 — one atomic per anchor group; the
-        // remaining lanes (cell movers) add 1 each
-        const int hb = s * kSlots + kStay;
-        const int hA = __shfl_sync(kFull, hb, 0), hB = __shfl_sync(kFull, hb, 31);
-        const bool inA = hkey == hA, inB = hkey == hB && hB != hA;
-        const unsigned mA = __ballot_sync(kFull, inA), mB = __ballot_sync(kFull, inB);
-        if (lane == 0 && mA) atomicAdd(a.hist_next + (int64_t)kStay * nbins + hA / kSlots, __popc(mA));
-        if (lane == 31 && mB) atomicAdd(a.hist_next + (int64_t)kStay * nbins + hB / kSlots, __popc(mB));
-        if (hkey >= 0 && !inA && !inB) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, 1);
+        if (here && obin == s && j2 == kStay) ++hcnt;                       // flushed per (lane, bin)
+        else if (here && j2 >= 0) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, 1);
         const bool mover = write_ok && (((e0 >> SH) != (ox >> SH)) | ((e1 >> SH) != (oy >> SH)) | ((e2 >> SH) != (oz >> SH)));
         movers += mover ? 1u : 0u;
       }

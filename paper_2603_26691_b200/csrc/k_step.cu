@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
       fence_proxy_async();
       for (int k = 0; k < kStages && k < nbatch; ++k) stage_issue(stg + k, bar + k, a.A, cap, p0 + 32 * k, cap, SCATTER);
     }
+    __syncwarp();   // reconverge after the lane-0 issue (see k_pstep.cuh)
     int lb = 0;   // this lane's bin pointer (monotone over its particles)
     for (int bi = 0; bi < nbatch; ++bi) {
       const int base = bi << 5;
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
       const int s = b0 + lb;
       const int sx = cell_w[lb][0], sy = cell_w[lb][1], sz = cell_w[lb][2];
       mbar_wait(bar + sk, (phase >> sk) & 1u);
+      __syncwarp();
       phase ^= 1u << sk;
       const Stage& S = stg[sk];
       const int so = (int)((p0 + base) & 3) + lane;   // slot of this lane's particle in the segments
@@ -489,6 +491,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
         fence_proxy_async();
         stage_issue(stg + sk, bar + sk, a.A, cap, p0 + 32 * (bi + kStages), cap, SCATTER);
       }
+      __syncwarp();
     }
     __syncwarp();
   }
@@ -675,7 +678,7 @@ int launch_variant(const StepArgs& a, cudaStream_t s) {
 template <bool S, bool A, int BCM, int FEAT = 0xff>
 int launch_pvariant(const StepArgs& a, cudaStream_t s) {
   static int grid = 0;
-  const int smem = 8 * pwarp_smem_bytes(S);
+  const int smem = 8 * pwarp_smem_bytes(S) + kPSmemAlign;
   if (!grid) {
     int nsm = 148, dev = 0, per = 1;
     cudaGetDevice(&dev);

@@ -2,6 +2,8 @@
 // Owns the SoA particle store (ping-pong), the double-buffered fluid field and
 // source accumulators (asynchronous coupling buffer), the
 // compute and copy streams, and (nranks > 1) the NCCL communicator.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -40,6 +42,7 @@ struct st_ctx {
   int64_t cap = 0, n = 0;
   Store S[2];
   int cur = 0;
+  CUtensorMap tmap[4];        // [2 stores][float rows, ids] TMA descriptors (kernel parameters)
   int32_t* key[2] = {nullptr, nullptr};
   SortScratch sc;
   uint64_t next_id = 0;
@@ -314,6 +317,39 @@ static st_status alloc_store(st_ctx* c, Store& s, int64_t cap_in) {
   return ST_OK;
 }
 
+// TMA descriptors of the particle stores (k_pstep input): the 8 float rows of a
+// store are contiguous with stride cap (alloc_store), so one 2-D box {36, 8} stages
+// a 32-particle batch from the 16-B aligned index below it; ids are a 2-D box {34, 1}
+// of a {cap, 1} tensor.  Encoded through the driver entry
+// point (no libcuda link dependency); passed as __grid_constant__ kernel parameters.
+static st_status make_tensor_maps(st_ctx* c) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+      q != cudaDriverEntryPointSuccess)
+    return fail(c, ST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  auto encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  CUtensorMap* h = c->tmap;
+  memset(h, 0, sizeof(c->tmap));
+  for (int i = 0; i < 2; ++i) {
+    const cuuint64_t dimf[2] = {(cuuint64_t)c->cap, 8};
+    const cuuint64_t stridef[1] = {(cuuint64_t)c->cap * sizeof(float)};
+    const cuuint32_t boxf[2] = {36, 8}, es[2] = {1, 1};   // k_pstep.cuh kBoxF
+    CUresult r = encode(&h[2 * i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, c->S[i].x, dimf, stridef, boxf, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, ST_ERR_CUDA, "tensor map (float rows) encode failed: " + std::to_string((int)r));
+    const cuuint64_t dimi[2] = {(cuuint64_t)c->cap, 1};
+    const cuuint64_t stridei[1] = {(cuuint64_t)c->cap * sizeof(uint64_t)};
+    const cuuint32_t boxi[2] = {34, 1};                    // k_pstep.cuh kBoxI
+    r = encode(&h[2 * i + 1], CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, c->S[i].id, dimi, stridei, boxi, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, ST_ERR_CUDA, "tensor map (ids) encode failed: " + std::to_string((int)r));
+  }
+  return ST_OK;
+}
+
 static st_status init_impl(st_ctx* c) {
   ST_CUDA(c, cudaSetDevice(c->cfg.device));
   build_geometry(c);
@@ -348,6 +384,10 @@ static st_status init_impl(st_ctx* c) {
   ST_CUDA(c, cudaEventCreate(&c->t_adv1));
   ST_CUDA(c, cudaEventCreate(&c->t_reb0));
   ST_CUDA(c, cudaEventCreate(&c->t_reb1));
+  {
+    st_status ts = make_tensor_maps(c);
+    if (ts) return ts;
+  }
   ST_CUDA(c, cudaMalloc(&c->field_stage, (size_t)3 * c->ext_nz * g.n[1] * g.n[0] * sizeof(float)));
   ST_CUDA(c, cudaMalloc(&c->S_dev, (size_t)3 * (c->local_cells > 0 ? c->local_cells : 1) * sizeof(float)));
   ST_CUDA(c, cudaMalloc(&c->d_err, sizeof(int)));
@@ -587,6 +627,8 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.bg = c->bg;
   a.A = c->S[c->cur];
   a.B = c->S[1 - c->cur];
+  a.tm_f = c->tmap[2 * c->cur];
+  a.tm_id = c->tmap[2 * c->cur + 1];
   a.cap = c->cap;
   a.n = c->n;
   a.off = c->off[c->lay];

@@ -1,6 +1,7 @@
 // Binned particle step (k_step.cu): layout, arguments and launchers.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,6 +30,8 @@ struct StepArgs {
   Phys p;
   BinGeom bg;
   Store A, B;                 // input layout / output layout (scatter)
+  CUtensorMap tm_f;           // TMA tensor map of A's float rows (2-D {cap, 8}; k_pstep)
+  CUtensorMap tm_id;          // TMA tensor map of A's ids (2-D {cap, 1}; k_pstep)
   int64_t cap, n;
   const int64_t* off;         // [nbins+1] CSR of A
   const int64_t* off_new;     // [nbins+1] CSR of B (scatter)
