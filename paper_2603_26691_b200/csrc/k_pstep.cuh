@@ -34,6 +34,14 @@ __device__ __forceinline__ int dbg_sum(int v) {
   return v;
 }
 
+// one generic load of a cell (the window lives in smem, the rest of the field in
+// global); ptxas narrows it to 8 + 4 bytes since the 4th lane is unused
+__device__ __forceinline__ float4 ld4(const float4* p) {
+  float4 v;
+  asm("ld.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+
 constexpr int kRowBins = 8;
 constexpr int kPStages = 3;
 // A tensor-copy box must start 16-byte aligned along the inner dimension (a
@@ -48,10 +56,14 @@ struct alignas(128) TStage {
 constexpr int kTStageBytes = (int)sizeof(TStage);                   // 1536
 constexpr uint32_t kTxF = 8 * kBoxF * 4, kTxI = kBoxI * 8;
 constexpr int kScatterTable = (kRowBins * kSlots * 13 + 15) / 16 * 16;
-// per-warp slice: stages | mbarriers | [scatter: dbase i64, run i32, side i8] | rel[9]; 128-B multiple
+// fluid window of an item: ghosted cells x in [rx-1, rx+8], y in [ry-1, ry+1], z in [rz-1, rz+1]
+constexpr int kWinX = kRowBins + 2, kWinCells = kWinX * 9;
+// per-warp slice: stages | fluid window | mbarriers | [scatter: dbase i64, run i32, side i8] | rel[9]
+constexpr int kOffWin = kPStages * kTStageBytes;
+constexpr int kOffBar = kOffWin + kWinCells * 16;
+constexpr int kOffTail = kOffBar + 8 * kPStages;
 __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
-  return (kPStages * kTStageBytes + 8 * kPStages + (scatter ? kScatterTable : 0) + (kRowBins + 1) * 4 + 127) / 128 *
-         128;
+  return (kOffTail + (scatter ? kScatterTable : 0) + (kRowBins + 1) * 4 + 127) / 128 * 128;
 }
 constexpr int kPSmemAlign = 128;   // slack for aligning the dynamic smem base
 
@@ -76,8 +88,11 @@ __device__ __forceinline__ void tstage_issue(TStage* st, unsigned long long* bar
   if (with_id) tma_ids(st->id, tm_id, i0 & ~1, bar);
 }
 
+#ifndef ST_PMINB
+#define ST_PMINB 2
+#endif
 template <bool SCATTER, bool ADVANCE, int BCM, int FEAT = 0xff>
-__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(const __grid_constant__ StepArgs a) {
+__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_pstep(const __grid_constant__ StepArgs a) {
   constexpr int SH = 3;   // chunk_cells == 8
   extern __shared__ __align__(128) unsigned char psmem_raw[];
   const Geom& g = a.g;
@@ -86,8 +101,9 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(con
   unsigned char* sbase = psmem_raw + ((kPSmemAlign - (smem_u32(psmem_raw) & (kPSmemAlign - 1))) & (kPSmemAlign - 1));
   unsigned char* ws = sbase + (size_t)wib * pwarp_smem_bytes(SCATTER);
   TStage* stg = reinterpret_cast<TStage*>(ws);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kPStages * kTStageBytes);
-  unsigned char* tail = ws + kPStages * kTStageBytes + 8 * kPStages;
+  float4* win = reinterpret_cast<float4*>(ws + kOffWin);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kOffBar);
+  unsigned char* tail = ws + kOffTail;
   long long* dbase = reinterpret_cast<long long*>(tail);                                 // [8*27]
   int* run = reinterpret_cast<int*>(dbase + (SCATTER ? kRowBins * kSlots : 0));          // [8*27]
   signed char* dside = reinterpret_cast<signed char*>(run + (SCATTER ? kRowBins * kSlots : 0));
@@ -125,6 +141,19 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(con
     if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
     int rx, ry, rz;                               // cell of the row's first bin (row along +x)
     cell_of_bin(g, a.bg, b0, rx, ry, rz);
+    if (FEAT & 2) {
+      // the item's fluid window: every stencil of a particle whose cell lies in the row
+#pragma unroll
+      for (int it = 0; it < (kWinCells + 31) / 32; ++it) {
+        const int k = lane + 32 * it;
+        if (k < kWinCells) {
+          const int kx = k % kWinX, ky = (k / kWinX) % 3, kz = k / (3 * kWinX);
+          const int wz = window_z(g, rz - 1 + kz);
+          win[k] = wz >= 0 ? __ldg(a.field + ((int64_t)wz * pz + (ry + ky) * g.gx + (rx + kx)))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    }
     if (SCATTER) {
       // destination run bases of every (bin, slot) of the item
 #pragma unroll
@@ -295,11 +324,16 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_pstep(con
           }
           float4 uf = make_float4(0.1f, 0.0f, 0.0f, 0.0f);   // (ablation value)
           if (FEAT & 2) {
-            const float4* fb = a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
-            const float4 c000 = __ldg(fb), c100 = __ldg(fb + 1);
-            const float4 c010 = __ldg(fb + g.gx), c110 = __ldg(fb + g.gx + 1);
-            const float4 c001 = __ldg(fb + pz), c101 = __ldg(fb + pz + 1);
-            const float4 c011 = __ldg(fb + pz + g.gx), c111 = __ldg(fb + pz + g.gx + 1);
+            // corners from the smem window when the cell lies in the item's row, else
+            // from the global field: one generic-pointer load path for both
+            const bool inw = (unsigned)(c0 - rx) < (unsigned)kRowBins && c1 == ry && c2 == rz;
+            const float4* fb = inw ? win + ((iz - rz + 1) * 3 + (iy - ry + 1)) * kWinX + (ix - rx + 1)
+                                   : a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
+            const int oy = inw ? kWinX : g.gx, oz = inw ? 3 * kWinX : pz;
+            const float4 c000 = ld4(fb), c100 = ld4(fb + 1);
+            const float4 c010 = ld4(fb + oy), c110 = ld4(fb + oy + 1);
+            const float4 c001 = ld4(fb + oz), c101 = ld4(fb + oz + 1);
+            const float4 c011 = ld4(fb + oz + oy), c111 = ld4(fb + oz + oy + 1);
             uf = lerp4(lerp4(lerp4(c000, c100, fx), lerp4(c010, c110, fx), fy),
                        lerp4(lerp4(c001, c101, fx), lerp4(c011, c111, fx), fy), fz);
           }
