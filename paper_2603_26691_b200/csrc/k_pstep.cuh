@@ -16,24 +16,6 @@
 //  * movers: rank via MATCH.ANY over (bin, slot), individual red / atomic.
 #pragma once
 
-#ifndef ST_DBG
-#define ST_DBG 0
-#endif
-__device__ __forceinline__ unsigned dbg_peers(int key) {
-  unsigned todo = kFull, mine = 0;
-  while (todo) {
-    const int k = __shfl_sync(kFull, key, __ffs(todo) - 1);
-    const unsigned m = __ballot_sync(kFull, key == k);
-    mine = (key == k) ? m : mine;
-    todo &= ~m;
-  }
-  return mine;
-}
-__device__ __forceinline__ int dbg_sum(int v) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
-}
-
 // one generic load of a cell (the window lives in smem, the rest of the field in
 // global); ptxas narrows it to 8 + 4 bytes since the 4th lane is unused
 __device__ __forceinline__ float4 ld4(const float4* p) {
@@ -114,8 +96,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
   const int nbins = a.nbins;
   const int pz = g.gy * g.gx;
   const bool two_way = (FEAT & 4) && a.p.two_way;
-  int flags = 0, farflag = 0;
-  unsigned movers = 0;
+  int flags = 0;
   uint32_t phase = 0;
   if (lane == 0) {
     for (int k = 0; k < kPStages; ++k) mbar_init(bar + k, 1);
@@ -132,10 +113,10 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
     const int np = (int)(pe - p0);
     const int nbatch = (np + 31) >> 5;
     // prime the pipeline first: its latency overlaps the table set-up below
-    if (lane == 0 && !(ST_DBG & 16)) {
+    if (lane == 0) {
       fence_proxy_async();
       for (int k = 0; k < kPStages && k < nbatch; ++k)
-        tstage_issue(stg + k, bar + k, &a.tm_f, &a.tm_id, (int)(p0 + 32 * k), SCATTER && !(ST_DBG & 4));
+        tstage_issue(stg + k, bar + k, &a.tm_f, &a.tm_id, (int)(p0 + 32 * k), SCATTER);
     }
     __syncwarp();
     if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
@@ -183,8 +164,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
     __syncwarp();
     const int az_row = acc_z(g, rz);
     int lb = 0;
-    // per-lane stayer accumulators of bin st_lb: deposit (da*) and slot count (hcnt)
-    int st_lb = -1, hcnt = 0;
+    // per-lane stayer deposit accumulator (da*) of bin st_lb
+    int st_lb = -1;
     float da0 = 0.f, da1 = 0.f, da2 = 0.f;
     int carry_lb = -1, carry = 0;                 // stayers of bin carry_lb placed by earlier batches
     for (int bi = 0; bi <= nbatch; ++bi) {
@@ -195,25 +176,20 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
       if (!last)
         while (rel[lb + 1] <= r) ++lb;
       // flush the stayer accumulators of lanes whose bin changed (one group per bin)
-      {
-        const bool fl = !(ST_DBG & 8) && st_lb >= 0 && (last || lb != st_lb);
+      if (two_way) {
+        const bool fl = st_lb >= 0 && (last || lb != st_lb);
         unsigned todo = __ballot_sync(kFull, fl);
         while (todo) {
           const int ld = __ffs(todo) - 1;
           const int kb = __shfl_sync(kFull, st_lb, ld);
           const bool in = fl && st_lb == kb;
           todo &= ~__ballot_sync(kFull, in);
-          const int hc = (ST_DBG & 2) ? dbg_sum(in ? hcnt : 0) : (int)__reduce_add_sync(kFull, in ? (unsigned)hcnt : 0u);
-          if (two_way) {
-            float ra = da0, rb = da1, rc = da2;
-            group_sum3(in, ra, rb, rc);
-            if (lane == ld) red_add_v4(a.acc + ((int64_t)az_row * g.n[1] + ry) * g.n[0] + rx + kb, ra, rb, rc);
-          }
-          if ((FEAT & 8) && lane == ld && hc) atomicAdd(a.hist_next + (int64_t)kStay * nbins + b0 + kb, hc);
+          float ra = da0, rb = da1, rc = da2;
+          group_sum3(in, ra, rb, rc);
+          if (lane == ld) red_add_v4(a.acc + ((int64_t)az_row * g.n[1] + ry) * g.n[0] + rx + kb, ra, rb, rc);
         }
         if (fl || st_lb < 0) {
           st_lb = lb;
-          hcnt = 0;
           da0 = da1 = da2 = 0.f;
         }
       }
@@ -221,33 +197,27 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
       const int sk = bi % kPStages;
       const int s = b0 + lb;
       const int sx = rx + lb, sy = ry, sz = rz;             // bin cell (row along x)
-      if (!(ST_DBG & 16)) mbar_wait(bar + sk, (phase >> sk) & 1u);
+      mbar_wait(bar + sk, (phase >> sk) & 1u);
       __syncwarp();
       phase ^= 1u << sk;
       const TStage& S = stg[sk];
       const int so = (int)((p0 + base) & 3) + (r - base);   // slot in the aligned-down box
       float xp0 = S.f[0][so], xp1 = S.f[1][so], xp2 = S.f[2][so];
       float up0 = S.f[3][so], up1 = S.f[4][so], up2 = S.f[5][so];
-      float dp = S.f[6][so], wp = S.f[7][so];
-      if (ST_DBG & 16) {
-        const int64_t q = p0 + r;
-        xp0 = a.A.x[q]; xp1 = a.A.x[cap + q]; xp2 = a.A.x[2 * cap + q];
-        up0 = a.A.u[q]; up1 = a.A.u[cap + q]; up2 = a.A.u[2 * cap + q];
-        dp = a.A.d[q]; wp = a.A.w[q];
-      }
+      const float dp = S.f[6][so], wp = S.f[7][so];
       unsigned long long pid = 0;
-      if (SCATTER) pid = (ST_DBG & 4) ? a.A.id[p0 + r] : S.id[(int)((p0 + base) & 1) + (r - base)];
+      if (SCATTER) pid = S.id[(int)((p0 + base) & 1) + (r - base)];
       // the stage is consumed: refill it with the batch kPStages ahead
       __syncwarp();
-      if (lane == 0 && bi + kPStages < nbatch && !(ST_DBG & 16)) {
+      if (lane == 0 && bi + kPStages < nbatch) {
         fence_proxy_async();
-        tstage_issue(stg + sk, bar + sk, &a.tm_f, &a.tm_id, (int)(p0 + 32 * (bi + kPStages)), SCATTER && !(ST_DBG & 4));
+        tstage_issue(stg + sk, bar + sk, &a.tm_f, &a.tm_id, (int)(p0 + 32 * (bi + kPStages)), SCATTER);
       }
       __syncwarp();
       float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
             t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
       int c0 = cell_from_t(t0, g.n[0]), c1 = cell_from_t(t1, g.n[1]), c2 = cell_from_t(t2, g.n[2]);
-      int ox = sx, oy = sy, oz = sz, obin = s, vside = -1;
+      int vside = -1;
       int64_t dest = p0 + r;
       bool write_ok = valid;
       if (SCATTER) {
@@ -274,7 +244,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
         }
         // movers: groups of equal (bin, slot) keys
         const int key = (write_ok && !stay) ? k : -1;
-        const unsigned peers = (ST_DBG & 1) ? dbg_peers(key) : __match_any_sync(kFull, key);
+        const unsigned peers = __match_any_sync(kFull, key);
         if (key >= 0) {
           const int leader = __ffs(peers) - 1;
           int rb0 = 0;
@@ -285,12 +255,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           rbase = __shfl_sync(peers, rb0, leader) + __popc(peers & lt);
         }
         __syncwarp();
-        ox = c0;
-        oy = c1;
-        oz = c2;
         vside = dside[k];
         dest = db + rbase;
-        if (vside < 0) obin = bin_of_cell<SH>(g, a.bg, ox, oy, oz);
         if (write_ok && (dest < 0 || dest >= (vside < 0 ? a.n : a.scap))) {
           flags |= ERRF_SCATTER;
           write_ok = false;
@@ -398,18 +364,6 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           if (bad && valid) flags |= ERRF_CFL;
         }
       }
-      if (FEAT & 8) {   // slot histogram of the end position w.r.t. the output bin
-        const int e0 = cell_from_t(cell_coord(xp0, g.lo[0], g.ih[0]), g.n[0]);
-        const int e1 = cell_from_t(cell_coord(xp1, g.lo[1], g.ih[1]), g.n[1]);
-        const int e2 = cell_from_t(cell_coord(xp2, g.lo[2], g.ih[2]), g.n[2]);
-        const bool here = write_ok && vside < 0;
-        const int j2 = slot_of<BCM>(g, ox, oy, oz, e0, e1, e2);
-        if (here && j2 < 0) farflag = 1;
-        if (here && obin == s && j2 == kStay) ++hcnt;                       // flushed per (lane, bin)
-        else if (here && j2 >= 0) atomicAdd(a.hist_next + (int64_t)j2 * nbins + obin, 1);
-        const bool mover = write_ok && (((e0 >> SH) != (ox >> SH)) | ((e1 >> SH) != (oy >> SH)) | ((e2 >> SH) != (oz >> SH)));
-        movers += mover ? 1u : 0u;
-      }
       if ((FEAT & 16) && write_ok) {
         if (SCATTER) {
           const Store& o = vside < 0 ? a.B : a.sbuf[vside];
@@ -427,9 +381,5 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
     }
     __syncwarp();
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) movers += __shfl_xor_sync(kFull, movers, o);
-  if (lane == 0 && movers) atomicAdd(a.movers, (unsigned long long)movers);
   if (flags) atomicOr(a.err, flags);
-  if (farflag) *(volatile int*)a.far = 1;
 }

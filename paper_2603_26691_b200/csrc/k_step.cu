@@ -251,8 +251,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
   const int64_t cap = a.cap;
   const int nbins = a.nbins;
   const int cc = SH > 0 ? (1 << SH) : g.cc;
-  int flags = 0, farflag = 0;
-  unsigned movers = 0;
+  int flags = 0;
   uint32_t phase = 0;   // parity bit per stage
   if (lane == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(bar + k, 1);
@@ -451,22 +450,6 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
           if (bad && valid) flags |= ERRF_CFL;
         }
       }
-      // slot histogram of the end position w.r.t. the output bin (next rebin's input)
-      {
-        const int e0 = cell_from_t(cell_coord(xp0, g.lo[0], g.ih[0]), g.n[0]);
-        const int e1 = cell_from_t(cell_coord(xp1, g.lo[1], g.ih[1]), g.n[1]);
-        const int e2 = cell_from_t(cell_coord(xp2, g.lo[2], g.ih[2]), g.n[2]);
-        const bool here = write_ok && vside < 0;   // movers to a neighbour are counted by the receiver
-        const int j2 = here ? slot_of<BCM>(g, ox, oy, oz, e0, e1, e2) : -1;
-        if (here && j2 < 0) farflag = 1;
-        const long long hkey = (here && j2 >= 0) ? (long long)j2 * nbins + obin : -1 - lane;
-        const unsigned peers = __match_any_sync(kFull, hkey);
-        if (hkey >= 0 && (peers & lanemask_lt()) == 0) atomicAdd(a.hist_next + hkey, __popc(peers));
-        // chunk movers w.r.t. the output bins (the algorithmic rebin traffic)
-        const bool mover = write_ok && ((dcc<SH>(e0, cc) != dcc<SH>(ox, cc)) | (dcc<SH>(e1, cc) != dcc<SH>(oy, cc)) |
-                                        (dcc<SH>(e2, cc) != dcc<SH>(oz, cc)));
-        movers += mover ? 1u : 0u;
-      }
       if (write_ok) {
         if (SCATTER) {
           // the id is only carried: read it from the stage late, out of the live range
@@ -495,12 +478,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
     }
     __syncwarp();
   }
-  // warp totals -> one atomic per warp
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) movers += __shfl_xor_sync(kFull, movers, o);
-  if (lane == 0 && movers) atomicAdd(a.movers, (unsigned long long)movers);
   if (flags) atomicOr(a.err, flags);
-  if (farflag) *(volatile int*)a.far = 1;
 }
 
 #include "k_pstep.cuh"
@@ -593,34 +571,110 @@ __global__ void k_insert(InsertArgs a) {
   const int64_t dest = a.off_new[d] + a.kept[v] + (i - a.roff[v]);
   const Store& r = a.rbuf;
   const int64_t rc = a.rcap, cap = a.cap;
-  float xv[3];
   for (int ax = 0; ax < 3; ++ax) {
-    xv[ax] = r.x[ax * rc + i];
-    a.B.x[ax * cap + dest] = xv[ax];
+    a.B.x[ax * cap + dest] = r.x[ax * rc + i];
     a.B.u[ax * cap + dest] = r.u[ax * rc + i];
   }
   a.B.d[dest] = r.d[i];
   a.B.w[dest] = r.w[i];
   a.B.id[dest] = r.id[i];
-  int e[3];
-  for (int ax = 0; ax < 3; ++ax) e[ax] = cell_from_t(cell_coord(xv[ax], a.g.lo[ax], a.g.ih[ax]), a.g.n[ax]);
-  const int j = slot_of<-1>(a.g, x, y, a.plane, e[0], e[1], e[2]);
-  if (j < 0) *(volatile int*)a.far = 1;
-  else atomicAdd(a.hist_next + (int64_t)j * a.nbins + d, 1);
 }
 
-__global__ void k_hist_stay(const int64_t* __restrict__ off, int nbins, int* __restrict__ hist_row13) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < nbins) hist_row13[s] = (int)(off[s + 1] - off[s]);
+// Slot histogram of the current layout — the input of the next neighbour-slot
+// rebin (C-15): hist[j][s] = number of particles of bin s whose current cell lies at
+// slot j (0..26) relative to the bin's cell.  One warp per item: the item's bins are
+// owned, so counts gather in registers (stayers) and shared memory (the rest) and
+// reach HBM as plain stores (no memset, no global atomics).  Reads only x (12 B per
+// particle).  A particle more than one cell from its bin sets *far (the rebin must
+// then take the general sort); chunk movers are counted for the roofline.
+template <int BCM, int SH>
+__global__ void __launch_bounds__(256) k_count(CountArgs a) {
+  __shared__ int cnt_s[8][kMaxBins * kSlots];
+  __shared__ int rel_s[8][kMaxBins + 1];
+  const Geom& g = a.g;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int* wc = cnt_s[wib];
+  int* rel = rel_s[wib];
+  const int n_items = *a.n_items, nbins = a.nbins, cc = g.cc;
+  const int64_t cap = a.cap;
+  const int warps_total = gridDim.x * (blockDim.x >> 5);
+  unsigned movers = 0;
+  int farflag = 0;
+  for (int item = blockIdx.x * (blockDim.x >> 5) + wib; item < n_items; item += warps_total) {
+    const int b0 = a.item_bin0[item];
+    const int b1 = (item + 1 < n_items) ? a.item_bin0[item + 1] : nbins;
+    const int nb = b1 - b0;
+    const int64_t p0 = a.off[b0];
+    for (int k = lane; k <= nb; k += 32) rel[k] = (int)(a.off[b0 + k] - p0);
+    for (int k = lane; k < nb * kSlots; k += 32) wc[k] = 0;
+    int rx = 0, ry = 0, rz = 0;
+    if (SH == 3) cell_of_bin(g, a.bg, b0, rx, ry, rz);   // 8^3 chunks: the item is one row along +x
+    __syncwarp();
+    const int np = rel[nb];
+    int lb = -1, sx = 0, sy = 0, sz = 0, scnt = 0;
+    for (int base = 0; base < np; base += 128) {
+      float xv[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = base + 32 * u + lane;
+        const int64_t i = p0 + (r < np ? r : np - 1);
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) xv[u][ax] = __ldcs(a.x + ax * cap + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = base + 32 * u + lane;
+        if (r < np) {
+          int nl = lb < 0 ? 0 : lb;
+          while (rel[nl + 1] <= r) ++nl;
+          if (nl != lb) {
+            if (scnt) atomicAdd(&wc[lb * kSlots + kStay], scnt);
+            scnt = 0;
+            lb = nl;
+            if (SH == 3) {
+              sx = rx + lb;
+              sy = ry;
+              sz = rz;
+            } else {
+              cell_of_bin(g, a.bg, b0 + lb, sx, sy, sz);
+            }
+          }
+          const int c0 = cell_from_t(cell_coord(xv[u][0], g.lo[0], g.ih[0]), g.n[0]);
+          const int c1 = cell_from_t(cell_coord(xv[u][1], g.lo[1], g.ih[1]), g.n[1]);
+          const int c2 = cell_from_t(cell_coord(xv[u][2], g.lo[2], g.ih[2]), g.n[2]);
+          const int j = slot_of<BCM>(g, sx, sy, sz, c0, c1, c2);
+          if (j < 0) farflag = 1;
+          else if (j == kStay) ++scnt;
+          else atomicAdd(&wc[lb * kSlots + j], 1);
+          movers += ((dcc<SH>(c0, cc) != dcc<SH>(sx, cc)) | (dcc<SH>(c1, cc) != dcc<SH>(sy, cc)) |
+                     (dcc<SH>(c2, cc) != dcc<SH>(sz, cc)))
+                        ? 1u
+                        : 0u;
+        }
+      }
+    }
+    if (scnt) atomicAdd(&wc[lb * kSlots + kStay], scnt);
+    __syncwarp();
+    for (int k = lane; k < nb * kSlots; k += 32) {
+      const int l = k / kSlots, j = k - l * kSlots;
+      a.hist[(int64_t)j * nbins + b0 + l] = wc[k];
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) movers += __shfl_xor_sync(kFull, movers, o);
+  if (lane == 0 && movers) atomicAdd(a.movers, (unsigned long long)movers);
+  if (farflag) *(volatile int*)a.far = 1;
 }
 
-// item boundaries: bin s starts an item if s % kMaxBins == 0 or the kItemParticles
+// item boundaries: bin s starts an item if s % row == 0 or (ipart > 0) the ipart-particle
 // window of its first particle differs from that of bin s-1's first particle.
-__global__ void k_item_flags(const int64_t* __restrict__ off, int nbins, int row, uint32_t* __restrict__ flag) {
+__global__ void k_item_flags(const int64_t* __restrict__ off, int nbins, int row, int64_t ipart,
+                             uint32_t* __restrict__ flag) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nbins) return;
   uint32_t f = (s % row) == 0;
-  if (!f) f = (off[s] / kItemParticles) != (off[s - 1] / kItemParticles);
+  if (!f && ipart > 0) f = (off[s] / ipart) != (off[s - 1] / ipart);
   flag[s] = f;
 }
 
@@ -755,17 +809,41 @@ int launch_insert(const InsertArgs& a, cudaStream_t s) {
   return 1;
 }
 
-int launch_hist_all_stay(const int64_t* off, int nbins, int* hist, cudaStream_t s) {
-  cudaMemsetAsync(hist, 0, (size_t)nbins * kSlots * sizeof(int), s);
-  k_hist_stay<<<blocks_for(nbins), 256, 0, s>>>(off, nbins, hist + (int64_t)kStay * nbins);
+template <int BCM, int SH>
+int launch_count_v(const CountArgs& a, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    int nsm = 148, dev = 0, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_count<BCM, SH>, 256, 0);
+    grid = nsm * (per > 0 ? per : 1);
+  }
+  k_count<BCM, SH><<<grid, 256, 0, s>>>(a);
   return 1;
+}
+
+int launch_count(const CountArgs& a, cudaStream_t s) {
+  const int bcm = (a.g.bc[0] == ST_BC_PERIODIC ? 1 : 0) | (a.g.bc[1] == ST_BC_PERIODIC ? 2 : 0) |
+                  (a.g.bc[2] == ST_BC_PERIODIC ? 4 : 0);
+  if (a.g.cc == 8) {
+    switch (bcm) {
+      case 0: return launch_count_v<0, 3>(a, s);
+      case 7: return launch_count_v<7, 3>(a, s);
+      case 3: return launch_count_v<3, 3>(a, s);
+      default: return launch_count_v<-1, 3>(a, s);
+    }
+  }
+  return launch_count_v<-1, 0>(a, s);
 }
 
 int launch_items(const int64_t* off, int nbins, int cc, uint32_t* flag, int64_t* pos, int64_t* partial,
                  int* item_bin0, int* n_items, cudaStream_t s) {
-  // 8^3 chunks: one chunk row (<= 8 bins) per item for k_pstep; else <= kMaxBins bins
+  // 8^3 chunks: one whole chunk row (8 bins) per item for k_pstep, so its per-item
+  // set-up (destination table, fluid window) is amortised over the row; else
+  // <= kMaxBins bins and <= ~kItemParticles particles
   const int row = cc == 8 ? kRowBins : kMaxBins;
-  k_item_flags<<<blocks_for(nbins), 256, 0, s>>>(off, nbins, row, flag);
+  k_item_flags<<<blocks_for(nbins), 256, 0, s>>>(off, nbins, row, cc == 8 ? 0 : kItemParticles, flag);
   int nl = 1 + launch_exclusive_scan_u32(flag, nbins, pos, partial, s);
   k_item_fill<<<blocks_for(nbins), 256, 0, s>>>(flag, pos, nbins, item_bin0, n_items);
   return nl + 1;

@@ -52,17 +52,18 @@ struct st_ctx {
   bool binned = false;        // store sorted by bin key, off/items/hist valid
   bool rebin_due = false;     // contract rebin due (executed lazily, fused when possible)
   int lay = 0;                // index of the current layout in off/items
-  int hcur = 0;               // index of the current slot histogram
   int64_t* off[2] = {nullptr, nullptr};     // [nbins+1] current / next layout
   int* items[2] = {nullptr, nullptr};       // warp items (first bin of each)
   int* n_items[2] = {nullptr, nullptr};     // device counts
-  int* hist[2] = {nullptr, nullptr};        // [nbins*27] slot counts: current / being counted
+  int* hist = nullptr;                      // [27][nbins] slot counts of the current layout (k_count),
+                                            // turned into run bases by k_rebin_prep
   uint32_t* new_cnt = nullptr;              // [nbins]
   uint32_t* item_flag = nullptr;            // [nbins]
   int64_t* item_pos = nullptr;              // [nbins+1]
-  int* h_far = nullptr;                     // mapped pinned: next rebin needs the general sort
+  int* h_far = nullptr;                     // mapped pinned (1 rank): the rebin needs the general sort
   int* d_far = nullptr;
-  unsigned long long* d_movers = nullptr;   // chunk movers counted by the last step kernel
+  unsigned long long* d_movers = nullptr;   // chunk movers counted by the last k_count
+  cudaEvent_t ev_count = nullptr;           // k_count done (the far decision)
   // multi-GPU fused rebin (virtual neighbour planes)
   int64_t* voff[2] = {nullptr, nullptr};    // [nvb+1] offsets in the send buffers
   uint32_t* rcnt[2] = {nullptr, nullptr};   // [nvb] arrival counts (0: from below, 1: from above)
@@ -103,6 +104,7 @@ struct st_ctx {
   // timing
   cudaEvent_t t_adv0{}, t_adv1{}, t_reb0{}, t_reb1{};
   bool timed_adv = false, timed_reb = false;
+  bool reb_t0 = false;        // t_reb0 already recorded for the rebin in progress (k_count)
 
   // multi-GPU
   Comm* comm = nullptr;
@@ -397,8 +399,8 @@ static st_status init_impl(st_ctx* c) {
     ST_CUDA(c, cudaMalloc(&c->off[i], (nb + 1) * sizeof(int64_t)));
     ST_CUDA(c, cudaMalloc(&c->items[i], (nb + 1) * sizeof(int)));
     ST_CUDA(c, cudaMalloc(&c->n_items[i], sizeof(int)));
-    ST_CUDA(c, cudaMalloc(&c->hist[i], nb * 27 * sizeof(int)));
   }
+  ST_CUDA(c, cudaMalloc(&c->hist, nb * 27 * sizeof(int)));
   ST_CUDA(c, cudaMalloc(&c->new_cnt, (nb + 2 * (size_t)c->bg.nvb + 1) * sizeof(uint32_t)));
   if (c->bg.nvb > 0) {
     const size_t nv = (size_t)c->bg.nvb;
@@ -415,8 +417,6 @@ static st_status init_impl(st_ctx* c) {
       if (s2) return s2;
     }
     ST_CUDA(c, cudaHostAlloc(&c->h_tot, 4 * sizeof(int64_t), cudaHostAllocDefault));
-    ST_CUDA(c, cudaHostAlloc(&c->h_farg, sizeof(int), cudaHostAllocDefault));
-    ST_CUDA(c, cudaMalloc(&c->d_farg, sizeof(int)));
     ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_tot, cudaEventDisableTiming));
   }
   ST_CUDA(c, cudaMalloc(&c->item_flag, (nb + 1) * sizeof(uint32_t)));
@@ -425,6 +425,9 @@ static st_status init_impl(st_ctx* c) {
   *c->h_far = 0;
   ST_CUDA(c, cudaHostGetDevicePointer(&c->d_far, c->h_far, 0));
   ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_step_done, cudaEventDisableTiming));
+  ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming));
+  ST_CUDA(c, cudaHostAlloc(&c->h_farg, sizeof(int), cudaHostAllocDefault));
+  ST_CUDA(c, cudaMalloc(&c->d_farg, sizeof(int)));
   ST_CUDA(c, cudaMalloc(&c->d_movers, sizeof(unsigned long long)));
   ST_CUDA(c, cudaMemset(c->d_movers, 0, sizeof(unsigned long long)));
   // radix-sort scratch (also serves the scans over bins)
@@ -467,7 +470,6 @@ st_status st_destroy(st_ctx* c) {
     cudaFree(c->off[i]);
     cudaFree(c->items[i]);
     cudaFree(c->n_items[i]);
-    cudaFree(c->hist[i]);
   }
   cudaFree(c->new_cnt);
   cudaFree(c->item_flag);
@@ -487,6 +489,8 @@ st_status st_destroy(st_ctx* c) {
   cudaFree(c->d_farg);
   if (c->ev_tot) cudaEventDestroy(c->ev_tot);
   if (c->ev_step_done) cudaEventDestroy(c->ev_step_done);
+  if (c->ev_count) cudaEventDestroy(c->ev_count);
+  cudaFree(c->hist);
   cudaFree(c->sc.hist);
   cudaFree(c->sc.offs);
   cudaFree(c->sc.partial);
@@ -633,18 +637,15 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.n = c->n;
   a.off = c->off[c->lay];
   a.off_new = c->off[1 - c->lay];
-  a.slot_base = c->hist[c->hcur];
+  a.slot_base = c->hist;
   a.item_bin0 = c->items[c->lay];
   a.n_items = c->n_items[c->lay];
   a.nbins = c->bg.nbins;
   a.field = c->front >= 0 ? c->field[c->front] : nullptr;
   a.acc = c->acc[c->acc_cur];
-  a.hist_next = c->hist[1 - c->hcur];
   a.dt = dt;
   a.nsteps = nsteps;
   a.err = c->d_err;
-  a.far = c->d_far;
-  a.movers = c->d_movers;
   for (int k = 0; k < 2; ++k) {
     a.voff[k] = c->voff[k];
     a.sbuf[k] = c->sbuf[k];
@@ -655,7 +656,8 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
 
 static st_status general_rebin(st_ctx* c) {
   const Geom& g = c->g;
-  ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
+  if (!c->reb_t0) ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
+  c->reb_t0 = false;
   int in_b = 0, nl = 0;
   st_status s;
   if (c->comm) {
@@ -689,7 +691,6 @@ static st_status general_rebin(st_ctx* c) {
   if ((s = check_launch(c, nl + ns))) return s;
   if (in_b) c->cur = 1 - c->cur;
   nl = launch_bin_offsets(c->key[c->cur], c->n, c->bg.nbins, c->off[c->lay], c->cs);
-  nl += launch_hist_all_stay(c->off[c->lay], c->bg.nbins, c->hist[c->hcur], c->cs);
   nl += launch_items(c->off[c->lay], c->bg.nbins, g.cc, c->item_flag, c->item_pos, c->sc.partial, c->items[c->lay],
                      c->n_items[c->lay], c->cs);
   if ((s = check_launch(c, nl))) return s;
@@ -698,6 +699,48 @@ static st_status general_rebin(st_ctx* c) {
   c->binned = true;
   c->rebin_due = false;
   c->rebins += 1;
+  return ST_OK;
+}
+
+// Slot histogram of the current layout (k_count) before a neighbour-slot rebin.
+// *far: some particle is more than one cell from its bin, so the rebin must take
+// the general sort (1 rank: decided here, after the kernel; several ranks: the flag
+// stays on the device and is reduced over all ranks inside scatter_rebin).
+static st_status count_slots(st_ctx* c, bool* far) {
+  *far = true;
+  if (!c->binned) return ST_OK;
+  CountArgs ca;
+  memset(&ca, 0, sizeof(ca));
+  ca.g = c->g;
+  ca.bg = c->bg;
+  ca.x = c->S[c->cur].x;
+  ca.cap = c->cap;
+  ca.off = c->off[c->lay];
+  ca.item_bin0 = c->items[c->lay];
+  ca.n_items = c->n_items[c->lay];
+  ca.nbins = c->bg.nbins;
+  ca.hist = c->hist;
+  ca.movers = c->d_movers;
+  ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));   // the rebin's timing starts with the count
+  c->reb_t0 = true;
+  ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
+  if (c->comm) {
+    ST_CUDA(c, cudaMemsetAsync(c->d_farg, 0, sizeof(int), c->cs));
+    ca.far = c->d_farg;
+  } else {
+    ST_CUDA(c, cudaEventSynchronize(c->ev_count));   // the previous count has read nothing since
+    *c->h_far = 0;
+    ca.far = c->d_far;
+  }
+  st_status s = check_launch(c, launch_count(ca, c->cs));
+  if (s) return s;
+  if (c->comm) {
+    *far = false;
+    return ST_OK;
+  }
+  ST_CUDA(c, cudaEventRecord(c->ev_count, c->cs));
+  ST_CUDA(c, cudaEventSynchronize(c->ev_count));
+  *far = *(volatile int*)c->h_far != 0;
   return ST_OK;
 }
 
@@ -712,14 +755,13 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   const Geom& g = c->g;
   const int nlay = 1 - c->lay;
   const int nb = c->bg.nbins, nv = c->bg.nvb;
-  ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
-  int nl = launch_rebin_prep(g, c->bg, c->hist[c->hcur], c->new_cnt, c->cs);
+  if (!c->reb_t0) ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
+  c->reb_t0 = false;
+  int nl = launch_rebin_prep(g, c->bg, c->hist, c->new_cnt, c->cs);
   st_status s;
   if (c->comm) {
     if ((s = check_launch(c, nl))) return s;
     nl = 0;
-    int farv = (*c->h_far || !c->binned) ? 1 : 0;
-    ST_CUDA(c, cudaMemcpyAsync(c->d_farg, &farv, sizeof(int), cudaMemcpyHostToDevice, c->cs));
     std::string why;
     if (comm_rebin_counts(c->comm, c->new_cnt + nb, c->new_cnt + nb + nv, c->rcnt[0], c->rcnt[1], nv, c->d_farg,
                           g.bc[2] == ST_BC_PERIODIC, c->cs, why))
@@ -739,7 +781,6 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   nl += launch_exclusive_scan_u32(c->new_cnt, nb, c->off[nlay], c->sc.partial, c->cs);
   nl += launch_items(c->off[nlay], nb, g.cc, c->item_flag, c->item_pos, c->sc.partial, c->items[nlay], c->n_items[nlay],
                      c->cs);
-  ST_CUDA(c, cudaMemsetAsync(c->hist[1 - c->hcur], 0, (size_t)nb * 27 * sizeof(int), c->cs));
   ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));
   c->timed_reb = true;
   if ((s = check_launch(c, nl))) return s;
@@ -755,8 +796,6 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     n_new = c->n - c->h_tot[0] - c->h_tot[1] + c->h_tot[2] + c->h_tot[3];
     if (n_new > c->cfg.capacity) return fail(c, ST_ERR_CAPACITY, "migration would exceed the store capacity");
   }
-  *c->h_far = 0;
-  ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
   StepArgs a = step_args(c, dt, nsteps);
   a.n = n_new;
   if (advance) ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
@@ -782,8 +821,6 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
       ia.cap = c->cap;
       ia.off_new = c->off[nlay];
       ia.nbins = nb;
-      ia.hist_next = c->hist[1 - c->hcur];
-      ia.far = c->d_far;
       ia.err = c->d_err;
       nl += launch_insert(ia, c->cs);
     }
@@ -808,7 +845,6 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   ST_CUDA(c, cudaEventRecord(c->ev_step_done, c->cs));
   c->cur = 1 - c->cur;
   c->lay = nlay;
-  c->hcur = 1 - c->hcur;
   c->rebin_due = false;
   c->rebins += 1;
   if (advance) c->fused_rebins += 1;
@@ -819,8 +855,10 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
 // when nranks > 1).
 static st_status flush_rebin(st_ctx* c) {
   if (!c->rebin_due) return ST_OK;
-  ST_CUDA(c, cudaEventSynchronize(c->ev_step_done));
-  if (!c->binned || (!c->comm && *c->h_far)) return general_rebin(c);
+  bool far = true;
+  st_status s = count_slots(c, &far);
+  if (s) return s;
+  if (far) return general_rebin(c);
   bool fell_back = false;
   return scatter_rebin(c, false, 0.0f, 0, &fell_back);
 }
@@ -843,8 +881,9 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
   if (c->rebin_due) {
     // the rebin of the previous call (C-15), fused into this call when every
     // particle is still within one cell of its bin
-    ST_CUDA(c, cudaEventSynchronize(c->ev_step_done));
-    if (c->binned && (c->comm || !*c->h_far)) {
+    bool far = true;
+    if ((st = count_slots(c, &far))) return st;
+    if (!far) {
       bool fell_back = false;
       st = scatter_rebin(c, true, (float)dt, nsteps, &fell_back);
       if (st) return st;
@@ -857,13 +896,9 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
   if (!done) {
     ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
     if (c->binned) {
-      ST_CUDA(c, cudaMemsetAsync(c->hist[1 - c->hcur], 0, (size_t)c->bg.nbins * 27 * sizeof(int), c->cs));
-      ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
-      *c->h_far = 0;
       StepArgs a = step_args(c, (float)dt, nsteps);
       st = check_launch(c, launch_step(a, false, true, c->cs));
       if (st) return st;
-      c->hcur = 1 - c->hcur;
     } else {
       st = check_launch(c, launch_advance(c->g, c->p, c->field[c->front], c->acc[c->acc_cur], c->S[c->cur], c->cap,
                                           c->n, nullptr, 0, (float)dt, nsteps, nullptr, c->d_err, c->cs));

@@ -35,18 +35,15 @@ struct StepArgs {
   int64_t cap, n;
   const int64_t* off;         // [nbins+1] CSR of A
   const int64_t* off_new;     // [nbins+1] CSR of B (scatter)
-  const int* slot_base;       // [nbins*27] base[s][j] (scatter; rebin_prep output)
+  const int* slot_base;       // [27][nbins] base[j][s] (scatter; rebin_prep output)
   const int* item_bin0;       // warp items of A
   const int* n_items;
   int nbins;
   const float4* field;
   float4* acc;
-  int* hist_next;             // [nbins*27] slot counts of the output layout (zeroed before)
   float dt;
   int nsteps;
   int* err;                   // hard errors (ERRF_*)
-  int* far;                   // set when the next rebin cannot use the neighbour scatter
-  unsigned long long* movers; // particles whose end chunk differs from their output bin's chunk
   // multi-GPU scatter: movers into the neighbour planes go to send buffers
   const int64_t* voff[2];     // [nvb+1] offsets of the virtual bins in sbuf[side]
   Store sbuf[2];
@@ -68,15 +65,27 @@ struct InsertArgs {
   int64_t cap;
   const int64_t* off_new;
   int nbins;
-  int* hist_next;
-  int* far;
   int* err;
 };
 int launch_insert(const InsertArgs& a, cudaStream_t s);
 
 int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s);
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s);
-int launch_hist_all_stay(const int64_t* off, int nbins, int* hist, cudaStream_t s);
+// Slot histogram of the current layout (k_count): input of the next neighbour-slot rebin
+struct CountArgs {
+  Geom g;
+  BinGeom bg;
+  const float* x;             // [3][cap] positions of the current layout
+  int64_t cap;
+  const int64_t* off;         // [nbins+1] CSR of the current layout
+  const int* item_bin0;
+  const int* n_items;
+  int nbins;
+  int* hist;                  // [27][nbins] out: hist[j][s] (every entry written)
+  int* far;                   // set to 1 if a particle is more than one cell from its bin
+  unsigned long long* movers; // += particles whose current chunk differs from their bin's chunk
+};
+int launch_count(const CountArgs& a, cudaStream_t s);
 int launch_items(const int64_t* off, int nbins, int cc, uint32_t* flag, int64_t* pos, int64_t* partial,
                  int* item_bin0, int* n_items, cudaStream_t s);
 int launch_bin_offsets(const int32_t* key_sorted, int64_t n, int nbins, int64_t* off, cudaStream_t s);
