@@ -24,6 +24,11 @@ __device__ __forceinline__ float4 ld4(const float4* p) {
   return v;
 }
 
+__device__ __forceinline__ float4 trilerp(const float4 (&q)[8], float fx, float fy, float fz) {
+  return lerp4(lerp4(lerp4(q[0], q[1], fx), lerp4(q[2], q[3], fx), fy),
+               lerp4(lerp4(q[4], q[5], fx), lerp4(q[6], q[7], fx), fy), fz);
+}
+
 constexpr int kRowBins = 8;
 constexpr int kPStages = 3;
 // A tensor-copy box must start 16-byte aligned along the inner dimension (a
@@ -217,6 +222,31 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
       float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
             t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
       int c0 = cell_from_t(t0, g.n[0]), c1 = cell_from_t(t1, g.n[1]), c2 = cell_from_t(t2, g.n[2]);
+      // fluid corners of sub-step 0, issued before the warp-collective rank so that
+      // their latency overlaps it: from the smem window when the cell lies in the
+      // item's row, else from the global field (one generic-pointer load path)
+      float4 q[8];
+      float fx, fy, fz;
+      auto gather = [&](float s0, float s1, float s2, int k0, int k1, int k2) {
+        int ix, iy, iz;
+        stencil_from_cell(s0, k0, ix, fx);
+        stencil_from_cell(s1, k1, iy, fy);
+        stencil_from_cell(s2, k2, iz, fz);
+        int wz = window_z(g, iz);
+        if (wz < 0 || wz + 1 >= g.wnz) {
+          if (valid) flags |= ERRF_WINDOW;
+          wz = wz < 0 ? 0 : g.wnz - 2;
+        }
+        if (FEAT & 2) {
+          const bool inw = (unsigned)(k0 - rx) < (unsigned)kRowBins && k1 == ry && k2 == rz;
+          const float4* fb = inw ? win + ((iz - rz + 1) * 3 + (iy - ry + 1)) * kWinX + (ix - rx + 1)
+                                 : a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
+          const int oy = inw ? kWinX : g.gx, oz = inw ? 3 * kWinX : pz;
+          q[0] = ld4(fb); q[1] = ld4(fb + 1); q[2] = ld4(fb + oy); q[3] = ld4(fb + oy + 1);
+          q[4] = ld4(fb + oz); q[5] = ld4(fb + oz + 1); q[6] = ld4(fb + oz + oy); q[7] = ld4(fb + oz + oy + 1);
+        }
+      };
+      if (ADVANCE && (FEAT & 1)) gather(t0, t1, t2, c0, c1, c2);
       int vside = -1;
       int64_t dest = p0 + r;
       bool write_ok = valid;
@@ -277,32 +307,9 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
             c0 = cell_from_t(t0, g.n[0]);
             c1 = cell_from_t(t1, g.n[1]);
             c2 = cell_from_t(t2, g.n[2]);
+            gather(t0, t1, t2, c0, c1, c2);
           }
-          int ix, iy, iz;
-          float fx, fy, fz;
-          stencil_from_cell(t0, c0, ix, fx);
-          stencil_from_cell(t1, c1, iy, fy);
-          stencil_from_cell(t2, c2, iz, fz);
-          int wz = window_z(g, iz);
-          if (wz < 0 || wz + 1 >= g.wnz) {
-            if (valid) flags |= ERRF_WINDOW;
-            wz = wz < 0 ? 0 : g.wnz - 2;
-          }
-          float4 uf = make_float4(0.1f, 0.0f, 0.0f, 0.0f);   // (ablation value)
-          if (FEAT & 2) {
-            // corners from the smem window when the cell lies in the item's row, else
-            // from the global field: one generic-pointer load path for both
-            const bool inw = (unsigned)(c0 - rx) < (unsigned)kRowBins && c1 == ry && c2 == rz;
-            const float4* fb = inw ? win + ((iz - rz + 1) * 3 + (iy - ry + 1)) * kWinX + (ix - rx + 1)
-                                   : a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
-            const int oy = inw ? kWinX : g.gx, oz = inw ? 3 * kWinX : pz;
-            const float4 c000 = ld4(fb), c100 = ld4(fb + 1);
-            const float4 c010 = ld4(fb + oy), c110 = ld4(fb + oy + 1);
-            const float4 c001 = ld4(fb + oz), c101 = ld4(fb + oz + 1);
-            const float4 c011 = ld4(fb + oz + oy), c111 = ld4(fb + oz + oy + 1);
-            uf = lerp4(lerp4(lerp4(c000, c100, fx), lerp4(c010, c110, fx), fy),
-                       lerp4(lerp4(c001, c101, fx), lerp4(c011, c111, fx), fy), fz);
-          }
+          const float4 uf = (FEAT & 2) ? trilerp(q, fx, fy, fz) : make_float4(0.1f, 0.0f, 0.0f, 0.0f);
           const float sxv = uf.x - up0, syv = uf.y - up1, szv = uf.z - up2;
           const float Re = sqrt_approx(fmaf(sxv, sxv, fmaf(syv, syv, szv * szv))) * d * a.p.inv_nu;
           float f = 1.0f + 0.15f * exp2f(0.687f * __log2f(Re));
