@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
         __syncwarp();
         vside = dside[k];
         dest = db + rbase;
-        if (write_ok && (dest < 0 || dest >= (vside < 0 ? a.n : a.scap))) {
+        if (write_ok && (uint64_t)dest >= (uint64_t)(vside < 0 ? a.n : a.scap)) {
           flags |= ERRF_SCATTER;
           write_ok = false;
         }

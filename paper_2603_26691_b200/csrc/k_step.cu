@@ -587,6 +587,8 @@ __global__ void k_insert(InsertArgs a) {
 // reach HBM as plain stores (no memset, no global atomics).  Reads only x (12 B per
 // particle).  A particle more than one cell from its bin sets *far (the rebin must
 // then take the general sort); chunk movers are counted for the roofline.
+constexpr int kCountUnroll = 8;   // batches of x in flight per lane
+
 template <int BCM, int SH>
 __global__ void __launch_bounds__(256) k_count(CountArgs a) {
   __shared__ int cnt_s[8][kMaxBins * kSlots];
@@ -612,17 +614,17 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
     __syncwarp();
     const int np = rel[nb];
     int lb = -1, sx = 0, sy = 0, sz = 0, scnt = 0;
-    for (int base = 0; base < np; base += 128) {
-      float xv[4][3];
+    for (int base = 0; base < np; base += 32 * kCountUnroll) {
+      float xv[kCountUnroll][3];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kCountUnroll; ++u) {
         const int r = base + 32 * u + lane;
         const int64_t i = p0 + (r < np ? r : np - 1);
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) xv[u][ax] = __ldcs(a.x + ax * cap + i);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kCountUnroll; ++u) {
         const int r = base + 32 * u + lane;
         if (r < np) {
           int nl = lb < 0 ? 0 : lb;
