@@ -78,9 +78,13 @@ __device__ __forceinline__ void tstage_issue(TStage* st, unsigned long long* bar
 #ifndef ST_PMINB
 #define ST_PMINB 2
 #endif
-template <bool SCATTER, bool ADVANCE, int BCM, int FEAT = 0xff>
+constexpr int kSpecVP = 1;    // neighbour-rank planes (send buffers) may be destinations
+constexpr int kSpecSub = 2;   // more than one sub-step per call
+constexpr int kSpecAll = 3;
+template <bool SCATTER, bool ADVANCE, int BCM, int SPEC = kSpecAll, int FEAT = 0xff>
 __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_pstep(const __grid_constant__ StepArgs a) {
   constexpr int SH = 3;   // chunk_cells == 8
+  constexpr bool VP = (SPEC & kSpecVP) != 0;
   extern __shared__ __align__(128) unsigned char psmem_raw[];
   const Geom& g = a.g;
   const int lane = threadIdx.x & 31;
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           signed char side = -1;
           if (ok) {
             const int within = a.slot_base[(int64_t)j * nbins + b0 + lb];
-            side = (dz == a.bg.vz[0]) ? 0 : ((dz == a.bg.vz[1]) ? 1 : -1);
+            if (VP) side = (dz == a.bg.vz[0]) ? 0 : ((dz == a.bg.vz[1]) ? 1 : -1);
             if (side >= 0) db = a.voff[side][vbin_of_cell<SH>(g, dx, dy, 8)] + within;
             else if ((dz >> 3) >= a.bg.kz0 && (dz >> 3) < a.bg.kz0 + a.bg.nkz)
               db = a.off_new[bin_of_cell<SH>(g, a.bg, dx, dy, dz)] + within;
@@ -285,9 +289,9 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           rbase = __shfl_sync(peers, rb0, leader) + __popc(peers & lt);
         }
         __syncwarp();
-        vside = dside[k];
+        if (VP) vside = dside[k];
         dest = db + rbase;
-        if (write_ok && (uint64_t)dest >= (uint64_t)(vside < 0 ? a.n : a.scap)) {
+        if (write_ok && (uint64_t)dest >= (uint64_t)((VP && vside >= 0) ? a.scap : a.n)) {
           flags |= ERRF_SCATTER;
           write_ok = false;
         }
@@ -299,7 +303,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
         const float mw = a.p.mass_c * d * d * d * wp;
         const float dt = a.dt;
         const float gx = a.p.g[0], gy = a.p.g[1], gz = a.p.g[2];
-        for (int sub = 0; sub < a.nsteps; ++sub) {
+        const int nsub = (SPEC & kSpecSub) ? a.nsteps : 1;
+        for (int sub = 0; sub < nsub; ++sub) {
           if (sub > 0) {
             t0 = cell_coord(xp0, g.lo[0], g.ih[0]);
             t1 = cell_coord(xp1, g.lo[1], g.ih[1]);
@@ -373,8 +378,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
       }
       if ((FEAT & 16) && write_ok) {
         if (SCATTER) {
-          const Store& o = vside < 0 ? a.B : a.sbuf[vside];
-          const int64_t oc = vside < 0 ? cap : a.scap;
+          const Store& o = (VP && vside >= 0) ? a.sbuf[vside] : a.B;
+          const int64_t oc = (VP && vside >= 0) ? a.scap : cap;
           o.x[dest] = xp0; o.x[oc + dest] = xp1; o.x[2 * oc + dest] = xp2;
           o.u[dest] = up0; o.u[oc + dest] = up1; o.u[2 * oc + dest] = up2;
           o.d[dest] = dp;

@@ -731,7 +731,7 @@ int launch_variant(const StepArgs& a, cudaStream_t s) {
   return 1;
 }
 
-template <bool S, bool A, int BCM, int FEAT = 0xff>
+template <bool S, bool A, int BCM, int SPEC = kSpecAll, int FEAT = 0xff>
 int launch_pvariant(const StepArgs& a, cudaStream_t s) {
   static int grid = 0;
   const int smem = 8 * pwarp_smem_bytes(S) + kPSmemAlign;
@@ -739,16 +739,30 @@ int launch_pvariant(const StepArgs& a, cudaStream_t s) {
     int nsm = 148, dev = 0, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_pstep<S, A, BCM, FEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pstep<S, A, BCM, FEAT>, 256, smem);
+    cudaFuncSetAttribute(k_pstep<S, A, BCM, SPEC, FEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pstep<S, A, BCM, SPEC, FEAT>, 256, smem);
     grid = nsm * (per > 0 ? per : 1);
   }
-  k_pstep<S, A, BCM, FEAT><<<grid, 256, smem, s>>>(a);
+  k_pstep<S, A, BCM, SPEC, FEAT><<<grid, 256, smem, s>>>(a);
   return 1;
 }
 
+// compile-time specialisation of k_pstep: neighbour-rank planes present (kSpecVP),
+// more than one sub-step per call (kSpecSub)
+template <bool S, bool A, int BCM>
+int launch_pspec(const StepArgs& a, cudaStream_t s) {
+  const int spec = (a.bg.nvb > 0 ? kSpecVP : 0) | (a.nsteps > 1 ? kSpecSub : 0);
+  switch (spec) {
+    case 0: return launch_pvariant<S, A, BCM, 0>(a, s);
+    case kSpecVP: return launch_pvariant<S, A, BCM, kSpecVP>(a, s);
+    case kSpecSub: return launch_pvariant<S, A, BCM, kSpecSub>(a, s);
+    default: return launch_pvariant<S, A, BCM, kSpecAll>(a, s);
+  }
+}
+
 // Performance ablation (ST_ABLATE env var, benchmarking only; results are wrong):
-// FEAT bits 1 physics, 2 field gather, 4 deposit, 8 histogram, 16 stores.
+// FEAT bits 1 physics, 2 field gather, 4 deposit, 16 stores (only in the single-rank,
+// one-sub-step, reflecting-wall specialisation).
 int ablate_mask() {
   static int m = -2;
   if (m == -2) {
@@ -763,22 +777,21 @@ int launch_mode(const StepArgs& a, cudaStream_t s) {
   const int bcm = (a.g.bc[0] == ST_BC_PERIODIC ? 1 : 0) | (a.g.bc[1] == ST_BC_PERIODIC ? 2 : 0) |
                   (a.g.bc[2] == ST_BC_PERIODIC ? 4 : 0);
   if (a.g.cc == 8) {   // chunk-row items with the staged fluid box (k_pstep.cuh)
-    if (S && A && bcm == 0 && ablate_mask() >= 0) {
+    if (S && A && bcm == 0 && a.bg.nvb == 0 && a.nsteps == 1 && ablate_mask() >= 0) {
       switch (ablate_mask()) {
-        case 29: return launch_pvariant<S, A, 0, 29>(a, s);   // no field gather
-        case 27: return launch_pvariant<S, A, 0, 27>(a, s);   // no deposit
-        case 23: return launch_pvariant<S, A, 0, 23>(a, s);   // no histogram
-        case 15: return launch_pvariant<S, A, 0, 15>(a, s);   // no stores
-        case 30: return launch_pvariant<S, A, 0, 30>(a, s);   // no physics (no field, no deposit)
-        case 16: return launch_pvariant<S, A, 0, 16>(a, s);   // loads + scatter stores only
-        case 0: return launch_pvariant<S, A, 0, 0>(a, s);     // loads + rank only
+        case 29: return launch_pvariant<S, A, 0, 0, 29>(a, s);   // no field gather
+        case 27: return launch_pvariant<S, A, 0, 0, 27>(a, s);   // no deposit
+        case 15: return launch_pvariant<S, A, 0, 0, 15>(a, s);   // no stores
+        case 30: return launch_pvariant<S, A, 0, 0, 30>(a, s);   // no physics (no field, no deposit)
+        case 16: return launch_pvariant<S, A, 0, 0, 16>(a, s);   // loads + scatter stores only
+        case 0: return launch_pvariant<S, A, 0, 0, 0>(a, s);  // loads + rank only
         default: break;
       }
     }
     switch (bcm) {
-      case 0: return launch_pvariant<S, A, 0>(a, s);
-      case 7: return launch_pvariant<S, A, 7>(a, s);
-      case 3: return launch_pvariant<S, A, 3>(a, s);
+      case 0: return launch_pspec<S, A, 0>(a, s);
+      case 7: return launch_pspec<S, A, 7>(a, s);
+      case 3: return launch_pspec<S, A, 3>(a, s);
       default: return launch_pvariant<S, A, -1>(a, s);
     }
   }
