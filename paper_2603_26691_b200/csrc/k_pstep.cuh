@@ -29,6 +29,12 @@ __device__ __forceinline__ float4 trilerp(const float4 (&q)[8], float fx, float 
                lerp4(lerp4(q[4], q[5], fx), lerp4(q[6], q[7], fx), fy), fz);
 }
 
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
 constexpr int kRowBins = 8;
 constexpr int kPStages = 3;
 // A tensor-copy box must start 16-byte aligned along the inner dimension (a
@@ -42,15 +48,27 @@ struct alignas(128) TStage {
 };
 constexpr int kTStageBytes = (int)sizeof(TStage);                   // 1536
 constexpr uint32_t kTxF = 8 * kBoxF * 4, kTxI = kBoxI * 8;
-constexpr int kScatterTable = (kRowBins * kSlots * 13 + 15) / 16 * 16;
-// fluid window of an item: ghosted cells x in [rx-1, rx+8], y in [ry-1, ry+1], z in [rz-1, rz+1]
-constexpr int kWinX = kRowBins + 2, kWinCells = kWinX * 9;
-// per-warp slice: stages | fluid window | mbarriers | [scatter: dbase i64, run i32, side i8] | rel[9]
+// fluid window of an item, ghosted cells x in [rx-1-R, rx+8+R], y in [ry-1-R, ry+1+R],
+// z in [rz-1-R, rz+1+R]: every trilinear stencil of a particle whose cell is within R of
+// the row (R = 1 for the fused scatter: the whole neighbourhood a binned particle can
+// be in; R = 0 in place).  Staged by one 3-D TMA tensor copy (tm_win[R]).
+#ifndef ST_EARLY_GATHER
+#define ST_EARLY_GATHER 1   // sub-step-0 corners issued before the rank (A/B: ~1 % faster)
+#endif
+#ifndef ST_PWIN_R
+#define ST_PWIN_R 1   // window margin R of the fused scatter (A/B: R = 1 ~2.5 % faster than 0)
+#endif
+__host__ __device__ constexpr int win_x(bool scatter) { return kRowBins + 2 + (scatter ? 2 * ST_PWIN_R : 0); }
+__host__ __device__ constexpr int win_yz(bool scatter) { return 3 + (scatter ? 2 * ST_PWIN_R : 0); }
+__host__ __device__ constexpr int win_cells(bool scatter) { return win_x(scatter) * win_yz(scatter) * win_yz(scatter); }
+constexpr int kTable = kRowBins * kSlots;           // destination table entries of an item (i64)
+// per-warp slice: stages | fluid window | [scatter: table i64[216], run i32[216]] | rel[9] | mbarriers
 constexpr int kOffWin = kPStages * kTStageBytes;
-constexpr int kOffBar = kOffWin + kWinCells * 16;
-constexpr int kOffTail = kOffBar + 8 * kPStages;
+__host__ __device__ constexpr int off_tab(bool scatter) { return kOffWin + win_cells(scatter) * 16; }
+__host__ __device__ constexpr int off_rel(bool scatter) { return off_tab(scatter) + (scatter ? kTable * 12 : 0); }
+__host__ __device__ constexpr int off_bar(bool scatter) { return off_rel(scatter) + 48; }
 __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
-  return (kOffTail + (scatter ? kScatterTable : 0) + (kRowBins + 1) * 4 + 127) / 128 * 128;
+  return (off_bar(scatter) + 8 * (kPStages + 1) + 127) / 128 * 128;
 }
 constexpr int kPSmemAlign = 128;   // slack for aligning the dynamic smem base
 
@@ -66,6 +84,13 @@ __device__ __forceinline__ void tma_ids(void* dst, const void* tmap, int c0, uns
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           smem_u32(dst)),
       "l"(tmap), "r"(c0), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_win(void* dst, const void* tmap, int c0, int c1, int c2, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void tstage_issue(TStage* st, unsigned long long* bar, const void* tm_f, const void* tm_id,
@@ -93,12 +118,12 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
   unsigned char* ws = sbase + (size_t)wib * pwarp_smem_bytes(SCATTER);
   TStage* stg = reinterpret_cast<TStage*>(ws);
   float4* win = reinterpret_cast<float4*>(ws + kOffWin);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + kOffBar);
-  unsigned char* tail = ws + kOffTail;
-  long long* dbase = reinterpret_cast<long long*>(tail);                                 // [8*27]
-  int* run = reinterpret_cast<int*>(dbase + (SCATTER ? kRowBins * kSlots : 0));          // [8*27]
-  signed char* dside = reinterpret_cast<signed char*>(run + (SCATTER ? kRowBins * kSlots : 0));
-  int* rel = reinterpret_cast<int*>(tail + (SCATTER ? kScatterTable : 0));               // [kRowBins+1]
+  long long* dtab = reinterpret_cast<long long*>(ws + off_tab(SCATTER));                 // [8*27]
+  int* run = reinterpret_cast<int*>(ws + off_tab(SCATTER) + kTable * 8);                  // [8*27]
+  int* rel = reinterpret_cast<int*>(ws + off_rel(SCATTER));                               // [kRowBins+1]
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + off_bar(SCATTER));  // stages | item
+  unsigned long long* ibar = bar + kPStages;
+  constexpr int WX = win_x(SCATTER), WYZ = win_yz(SCATTER), WR = SCATTER ? ST_PWIN_R : 0;
   const int n_items = *a.n_items;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t cap = a.cap;
@@ -106,9 +131,9 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
   const int pz = g.gy * g.gx;
   const bool two_way = (FEAT & 4) && a.p.two_way;
   int flags = 0;
-  uint32_t phase = 0;
+  uint32_t phase = 0, iphase = 0;
   if (lane == 0) {
-    for (int k = 0; k < kPStages; ++k) mbar_init(bar + k, 1);
+    for (int k = 0; k <= kPStages; ++k) mbar_init(bar + k, 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -121,54 +146,28 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
     const int64_t pe = a.off[b1];
     const int np = (int)(pe - p0);
     const int nbatch = (np + 31) >> 5;
-    // prime the pipeline first: its latency overlaps the table set-up below
+    int rx, ry, rz;                               // cell of the row's first bin (row along +x)
+    cell_of_bin(g, a.bg, b0, rx, ry, rz);
+    // asynchronous item set-up: the destination table (one bulk copy of k_dbase's rows)
+    // and the fluid window (one 3-D tensor copy), then the first particle batches
     if (lane == 0) {
       fence_proxy_async();
+      const uint32_t tx = ((FEAT & 2) ? win_cells(SCATTER) * 16u : 0u) + (SCATTER ? kTable * 8u : 0u);
+      if (tx) {
+        mbar_expect_tx(ibar, tx);
+        if (FEAT & 2) tma_win(win, &a.tm_win[WR], 4 * (rx - WR), ry - WR, window_z(g, rz) - 1 - WR, ibar);
+        if (SCATTER) bulk_g2s(dtab, a.dtab + (int64_t)b0 * kSlots, kTable * 8u, ibar);
+      }
       for (int k = 0; k < kPStages && k < nbatch; ++k)
         tstage_issue(stg + k, bar + k, &a.tm_f, &a.tm_id, (int)(p0 + 32 * k), SCATTER);
     }
     __syncwarp();
     if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
-    int rx, ry, rz;                               // cell of the row's first bin (row along +x)
-    cell_of_bin(g, a.bg, b0, rx, ry, rz);
-    if (FEAT & 2) {
-      // the item's fluid window: every stencil of a particle whose cell lies in the row
-#pragma unroll
-      for (int it = 0; it < (kWinCells + 31) / 32; ++it) {
-        const int k = lane + 32 * it;
-        if (k < kWinCells) {
-          const int kx = k % kWinX, ky = (k / kWinX) % 3, kz = k / (3 * kWinX);
-          const int wz = window_z(g, rz - 1 + kz);
-          win[k] = wz >= 0 ? __ldg(a.field + ((int64_t)wz * pz + (ry + ky) * g.gx + (rx + kx)))
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-    }
-    if (SCATTER) {
-      // destination run bases of every (bin, slot) of the item
-#pragma unroll
-      for (int it = 0; it < (kRowBins * kSlots + 31) / 32; ++it) {
-        const int k = lane + 32 * it;
-        if (k < nb * kSlots) {
-          const int lb = k / kSlots, j = k - lb * kSlots;
-          bool ok = true;
-          const int dx = axis_step(rx + lb, j % 3 - 1, g.n[0], g.bc[0], ok);
-          const int dy = axis_step(ry, (j / 3) % 3 - 1, g.n[1], g.bc[1], ok);
-          const int dz = axis_step(rz, j / 9 - 1, g.n[2], g.bc[2], ok);
-          long long db = -1;
-          signed char side = -1;
-          if (ok) {
-            const int within = a.slot_base[(int64_t)j * nbins + b0 + lb];
-            if (VP) side = (dz == a.bg.vz[0]) ? 0 : ((dz == a.bg.vz[1]) ? 1 : -1);
-            if (side >= 0) db = a.voff[side][vbin_of_cell<SH>(g, dx, dy, 8)] + within;
-            else if ((dz >> 3) >= a.bg.kz0 && (dz >> 3) < a.bg.kz0 + a.bg.nkz)
-              db = a.off_new[bin_of_cell<SH>(g, a.bg, dx, dy, dz)] + within;
-          }
-          dbase[k] = db;
-          dside[k] = side;
-          run[k] = 0;
-        }
-      }
+    if (SCATTER)
+      for (int k = lane; k < kTable; k += 32) run[k] = 0;
+    if ((FEAT & 2) || SCATTER) {
+      mbar_wait(ibar, iphase);
+      iphase ^= 1u;
     }
     __syncwarp();
     const int az_row = acc_z(g, rz);
@@ -226,9 +225,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
       float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
             t2 = cell_coord(xp2, g.lo[2], g.ih[2]);
       int c0 = cell_from_t(t0, g.n[0]), c1 = cell_from_t(t1, g.n[1]), c2 = cell_from_t(t2, g.n[2]);
-      // fluid corners of sub-step 0, issued before the warp-collective rank so that
-      // their latency overlaps it: from the smem window when the cell lies in the
-      // item's row, else from the global field (one generic-pointer load path)
+      // fluid corners of a sub-step: from the smem window when the cell lies in the
+      // item's row (the whole warp: shared loads), else from the global field
       float4 q[8];
       float fx, fy, fz;
       auto gather = [&](float s0, float s1, float s2, int k0, int k1, int k2) {
@@ -242,22 +240,33 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           wz = wz < 0 ? 0 : g.wnz - 2;
         }
         if (FEAT & 2) {
-          const bool inw = (unsigned)(k0 - rx) < (unsigned)kRowBins && k1 == ry && k2 == rz;
-          const float4* fb = inw ? win + ((iz - rz + 1) * 3 + (iy - ry + 1)) * kWinX + (ix - rx + 1)
-                                 : a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
-          const int oy = inw ? kWinX : g.gx, oz = inw ? 3 * kWinX : pz;
-          q[0] = ld4(fb); q[1] = ld4(fb + 1); q[2] = ld4(fb + oy); q[3] = ld4(fb + oy + 1);
-          q[4] = ld4(fb + oz); q[5] = ld4(fb + oz + 1); q[6] = ld4(fb + oz + oy); q[7] = ld4(fb + oz + oy + 1);
+          const bool inw = (unsigned)(k0 - rx + WR) < (unsigned)(kRowBins + 2 * WR) &&
+                           (unsigned)(k1 - ry + WR) <= (unsigned)(2 * WR) && (unsigned)(k2 - rz + WR) <= (unsigned)(2 * WR);
+          if (__all_sync(kFull, inw)) {   // the binned case: shared-memory loads only
+            const uint32_t w0 = smem_u32(win + ((iz - rz + 1 + WR) * WYZ + (iy - ry + 1 + WR)) * WX + (ix - rx + 1 + WR));
+            constexpr uint32_t oy = WX * 16, oz = WYZ * WX * 16;
+            q[0] = lds4(w0); q[1] = lds4(w0 + 16); q[2] = lds4(w0 + oy); q[3] = lds4(w0 + oy + 16);
+            q[4] = lds4(w0 + oz); q[5] = lds4(w0 + oz + 16); q[6] = lds4(w0 + oz + oy); q[7] = lds4(w0 + oz + oy + 16);
+          } else {
+            const float4* fb = inw ? win + ((iz - rz + 1 + WR) * WYZ + (iy - ry + 1 + WR)) * WX + (ix - rx + 1 + WR)
+                                   : a.field + ((int64_t)wz * pz + (iy + 1) * g.gx + (ix + 1));
+            const int oy = inw ? WX : g.gx, oz = inw ? WYZ * WX : pz;
+            q[0] = ld4(fb); q[1] = ld4(fb + 1); q[2] = ld4(fb + oy); q[3] = ld4(fb + oy + 1);
+            q[4] = ld4(fb + oz); q[5] = ld4(fb + oz + 1); q[6] = ld4(fb + oz + oy); q[7] = ld4(fb + oz + oy + 1);
+          }
         }
       };
-      if (ADVANCE && (FEAT & 1)) gather(t0, t1, t2, c0, c1, c2);
+#if ST_EARLY_GATHER
+      if (ADVANCE && (FEAT & 1)) gather(t0, t1, t2, c0, c1, c2);   // latency overlaps the rank
+#endif
       int vside = -1;
       int64_t dest = p0 + r;
       bool write_ok = valid;
       if (SCATTER) {
         const int j = slot_of<BCM>(g, sx, sy, sz, c0, c1, c2);
         const int k = lb * kSlots + (j < 0 ? kStay : j);
-        const long long db = dbase[k];
+        const long long e = dtab[k];                  // -1: leaves the domain; bits 61-62: side + 1
+        const long long db = e < 0 ? -1 : (e & ((1LL << 61) - 1));
         if (valid && (j < 0 || db < 0)) {
           flags |= ERRF_SCATTER;
           write_ok = false;
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           rbase = __shfl_sync(peers, rb0, leader) + __popc(peers & lt);
         }
         __syncwarp();
-        if (VP) vside = dside[k];
+        if (VP) vside = e < 0 ? -1 : (int)(e >> 61) - 1;
         dest = db + rbase;
         if (write_ok && (uint64_t)dest >= (uint64_t)((VP && vside >= 0) ? a.scap : a.n)) {
           flags |= ERRF_SCATTER;
@@ -312,8 +321,11 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
             c0 = cell_from_t(t0, g.n[0]);
             c1 = cell_from_t(t1, g.n[1]);
             c2 = cell_from_t(t2, g.n[2]);
-            gather(t0, t1, t2, c0, c1, c2);
           }
+#if ST_EARLY_GATHER
+          if (sub > 0)
+#endif
+            gather(t0, t1, t2, c0, c1, c2);
           const float4 uf = (FEAT & 2) ? trilerp(q, fx, fy, fz) : make_float4(0.1f, 0.0f, 0.0f, 0.0f);
           const float sxv = uf.x - up0, syv = uf.y - up1, szv = uf.z - up2;
           const float Re = sqrt_approx(fmaf(sxv, sxv, fmaf(syv, syv, szv * szv))) * d * a.p.inv_nu;

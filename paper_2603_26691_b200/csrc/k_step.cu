@@ -536,6 +536,40 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
   new_cnt[d] = total;
 }
 
+// Destination table of the fused scatter (k_pstep): for every source bin s and slot j,
+// the store index where the run of s's particles at slot j starts in the new layout:
+// off_new[d] + base[j][s] for a local destination bin d, voff[side][v] + base[j][s] for
+// a neighbour rank's plane (the side is packed into bits 61-62), -1 if slot j leaves
+// the domain.  Row-major [nbins][27] so that one item (a chunk row of 8 bins) is one
+// contiguous 1728-byte bulk copy.
+__global__ void k_dbase(Geom g, BinGeom bg, int nbins, const int* __restrict__ base, const int64_t* __restrict__ off_new,
+                        const int64_t* __restrict__ voff0, const int64_t* __restrict__ voff1, long long* __restrict__ dtab) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nbins) return;
+  int sx, sy, sz;
+  cell_of_bin(g, bg, s, sx, sy, sz);
+  const bool cell_ok = sx < g.n[0] && sy < g.n[1] && sz < g.n[2];
+  for (int j = 0; j < kSlots; ++j) {
+    bool ok = cell_ok;
+    const int dx = axis_step(sx, j % 3 - 1, g.n[0], g.bc[0], ok);
+    const int dy = axis_step(sy, (j / 3) % 3 - 1, g.n[1], g.bc[1], ok);
+    const int dz = axis_step(sz, j / 9 - 1, g.n[2], g.bc[2], ok);
+    long long e = -1;
+    if (ok) {
+      const long long within = base[(int64_t)j * nbins + s];
+      if (bg.nvb > 0 && dz == bg.vz[0]) {
+        e = (voff0[vbin_of_cell<0>(g, dx, dy, g.cc)] + within) | (1LL << 61);
+      } else if (bg.nvb > 0 && dz == bg.vz[1]) {
+        e = (voff1[vbin_of_cell<0>(g, dx, dy, g.cc)] + within) | (2LL << 61);
+      } else {
+        const int kz = dz / g.cc;
+        if (kz >= bg.kz0 && kz < bg.kz0 + bg.nkz) e = off_new[bin_of_cell<0>(g, bg, dx, dy, dz)] + within;
+      }
+    }
+    dtab[(int64_t)s * kSlots + j] = e;
+  }
+}
+
 // Arrival counts from the neighbours land after the local particles of the
 // boundary-plane bins (C-16: kept first, then arrivals).
 __global__ void k_vcombine(Geom g, BinGeom bg, uint32_t* __restrict__ new_cnt, const uint32_t* __restrict__ rcnt_dn,
@@ -835,6 +869,12 @@ int launch_count_v(const CountArgs& a, cudaStream_t s) {
     grid = nsm * (per > 0 ? per : 1);
   }
   k_count<BCM, SH><<<grid, 256, 0, s>>>(a);
+  return 1;
+}
+
+int launch_dbase(const Geom& g, const BinGeom& bg, const int* base, const int64_t* off_new, const int64_t* voff0,
+                 const int64_t* voff1, long long* dtab, cudaStream_t s) {
+  k_dbase<<<blocks_for(bg.nbins), 256, 0, s>>>(g, bg, bg.nbins, base, off_new, voff0, voff1, dtab);
   return 1;
 }
 

@@ -43,6 +43,8 @@ struct st_ctx {
   Store S[2];
   int cur = 0;
   CUtensorMap tmap[4];        // [2 stores][float rows, ids] TMA descriptors (kernel parameters)
+  CUtensorMap tmap_win[2][2]; // [field buffer][window shape] TMA descriptors of the fluid field
+  long long* dtab = nullptr;  // [nbins][27] destination table of the fused scatter (k_dbase)
   int32_t* key[2] = {nullptr, nullptr};
   SortScratch sc;
   uint64_t next_id = 0;
@@ -349,6 +351,21 @@ static st_status make_tensor_maps(st_ctx* c) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(c, ST_ERR_CUDA, "tensor map (ids) encode failed: " + std::to_string((int)r));
   }
+  // fluid field float4 [wnz][gy][gx] seen as fp32 {4 gx, gy, wnz}: k_pstep's window boxes
+  // of (10 + 2R) x (3 + 2R) x (3 + 2R) cells, R = 0 (in place) / 1 (fused scatter);
+  // out-of-range planes/cells are zero-filled (never read by a lane inside the window)
+  const Geom& g = c->g;
+  for (int i = 0; i < 2; ++i)
+    for (int w = 0; w < 2; ++w) {
+      const cuuint64_t dimw[3] = {(cuuint64_t)g.gx * 4, (cuuint64_t)g.gy, (cuuint64_t)g.wnz};
+      const cuuint64_t stridew[2] = {(cuuint64_t)g.gx * 16, (cuuint64_t)g.gx * g.gy * 16};
+      const cuuint32_t boxw[3] = {(cuuint32_t)(4 * (10 + 2 * w)), (cuuint32_t)(3 + 2 * w), (cuuint32_t)(3 + 2 * w)};
+      const cuuint32_t es3[3] = {1, 1, 1};
+      CUresult r = encode(&c->tmap_win[i][w], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->field[i], dimw, stridew, boxw, es3,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(c, ST_ERR_CUDA, "tensor map (field window) encode failed: " + std::to_string((int)r));
+    }
   return ST_OK;
 }
 
@@ -401,6 +418,7 @@ static st_status init_impl(st_ctx* c) {
     ST_CUDA(c, cudaMalloc(&c->n_items[i], sizeof(int)));
   }
   ST_CUDA(c, cudaMalloc(&c->hist, nb * 27 * sizeof(int)));
+  if (c->g.cc == 8) ST_CUDA(c, cudaMalloc(&c->dtab, nb * 27 * sizeof(long long)));
   ST_CUDA(c, cudaMalloc(&c->new_cnt, (nb + 2 * (size_t)c->bg.nvb + 1) * sizeof(uint32_t)));
   if (c->bg.nvb > 0) {
     const size_t nv = (size_t)c->bg.nvb;
@@ -491,6 +509,7 @@ st_status st_destroy(st_ctx* c) {
   if (c->ev_step_done) cudaEventDestroy(c->ev_step_done);
   if (c->ev_count) cudaEventDestroy(c->ev_count);
   cudaFree(c->hist);
+  cudaFree(c->dtab);
   cudaFree(c->sc.hist);
   cudaFree(c->sc.offs);
   cudaFree(c->sc.partial);
@@ -633,6 +652,9 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.B = c->S[1 - c->cur];
   a.tm_f = c->tmap[2 * c->cur];
   a.tm_id = c->tmap[2 * c->cur + 1];
+  a.tm_win[0] = c->tmap_win[c->front < 0 ? 0 : c->front][0];
+  a.tm_win[1] = c->tmap_win[c->front < 0 ? 0 : c->front][1];
+  a.dtab = c->dtab;
   a.cap = c->cap;
   a.n = c->n;
   a.off = c->off[c->lay];
@@ -779,6 +801,9 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     ST_CUDA(c, cudaEventRecord(c->ev_tot, c->cs));
   }
   nl += launch_exclusive_scan_u32(c->new_cnt, nb, c->off[nlay], c->sc.partial, c->cs);
+  if (c->dtab)
+    nl += launch_dbase(g, c->bg, c->hist, c->off[nlay], nv > 0 ? c->voff[0] : nullptr, nv > 0 ? c->voff[1] : nullptr,
+                       c->dtab, c->cs);
   nl += launch_items(c->off[nlay], nb, g.cc, c->item_flag, c->item_pos, c->sc.partial, c->items[nlay], c->n_items[nlay],
                      c->cs);
   ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));

@@ -32,10 +32,13 @@ struct StepArgs {
   Store A, B;                 // input layout / output layout (scatter)
   CUtensorMap tm_f;           // TMA tensor map of A's float rows (2-D {cap, 8}; k_pstep)
   CUtensorMap tm_id;          // TMA tensor map of A's ids (2-D {cap, 1}; k_pstep)
+  CUtensorMap tm_win[2];      // TMA maps of the front fluid field, window boxes of k_pstep:
+                              // [0] 10x3x3 cells (in place), [1] 12x5x5 cells (fused scatter)
   int64_t cap, n;
   const int64_t* off;         // [nbins+1] CSR of A
   const int64_t* off_new;     // [nbins+1] CSR of B (scatter)
-  const int* slot_base;       // [27][nbins] base[j][s] (scatter; rebin_prep output)
+  const int* slot_base;       // [27][nbins] base[j][s] (scatter; rebin_prep output; k_step)
+  const long long* dtab;      // [nbins][27] destination table (scatter; k_dbase output; k_pstep)
   const int* item_bin0;       // warp items of A
   const int* n_items;
   int nbins;
@@ -86,6 +89,9 @@ struct CountArgs {
   unsigned long long* movers; // += particles whose current chunk differs from their bin's chunk
 };
 int launch_count(const CountArgs& a, cudaStream_t s);
+// destination table [nbins][27] of k_pstep from the prep bases and the new offsets
+int launch_dbase(const Geom& g, const BinGeom& bg, const int* base, const int64_t* off_new, const int64_t* voff0,
+                 const int64_t* voff1, long long* dtab, cudaStream_t s);
 int launch_items(const int64_t* off, int nbins, int cc, uint32_t* flag, int64_t* pos, int64_t* partial,
                  int* item_bin0, int* n_items, cudaStream_t s);
 int launch_bin_offsets(const int32_t* key_sorted, int64_t n, int nbins, int64_t* off, cudaStream_t s);

@@ -2,7 +2,7 @@
 # Step-kernel ablation on C5 (K=1 fused): which stage costs what.
 NP=${1:-1e9}
 for M in ${MODES:--1 29 27 30 16}; do
-  ST_ABLATE=$M timeout 600 python bench.py --particles $NP --steps 4 --warmup 2 --no-cpu-baseline --no-e2e \
+  ST_ABLATE=$M timeout 600 python bench.py --particles $NP --steps 4 --warmup 2 --no-cpu-baseline --no-e2e --rebin-interval 1 \
     > gpurun_out/ablate_$M.log 2>&1
   python - "$M" <<'PY'
 import json, sys

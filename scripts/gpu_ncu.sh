@@ -3,7 +3,7 @@
 # usage: bash scripts/gpu_ncu.sh <tag> [particles]
 TAG=${1:-r}
 NP=${2:-2e7}
-CMD="python bench.py --particles $NP --steps 3 --warmup 2 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --particles $NP --steps 3 --warmup 2 --no-cpu-baseline --no-e2e ${EXTRA}"
 $CMD > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > /dev/null 2>&1
 echo "launch list rc=$?"
