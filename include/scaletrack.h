@@ -222,6 +222,59 @@ int32_t st_abi_version(void);
  * the bytes to the other ranks before st_init).  ST_ERR_NCCL on failure. */
 st_status st_nccl_unique_id(void* out);
 
+/* ---------------------------------------------------------------------------------
+ * Extrapolator-corrector for the asynchronously coupled Eulerian solve (SURVEY
+ * §8(f1); §2.4 "Extrapolator-corrector method", Eq. 14-16).
+ *
+ * When the Eulerian step n starts before the true Lagrangian sources of the previous
+ * step(s) are available, it uses the estimate
+ *     S^n_est = ΔS^n_corr + dt_ratio · S^n_ext                         (Eq. 15)
+ *     ΔS^n_corr = Σ_{newly received steps m} (S^m − S^m_est)          (Eq. 14 + P:228)
+ *     S^n_ext = 0 | S^{n-1} | 2 S^{n-1} − S^{n-2}   (zero / constant / linear, Eq. 16)
+ * with S^{n-1}, S^{n-2} the last two true sources received.  S^m_est is the estimate of
+ * step m's own source: what step m emitted beyond its correction (C-25), so
+ * the sequence is conservative: Σ emitted − Σ received = Σ estimates still pending.
+ * Cell-wise over a whole field of n values (e.g. the 3 × cells of st_get_sources);
+ * fp64 state on the device, fp32 emitted values.  Test oracle: oracle/extrapolator.py.
+ * ------------------------------------------------------------------------------- */
+typedef struct st_ec st_ec;
+enum { ST_EC_ZERO = 0, ST_EC_CONSTANT = 1, ST_EC_LINEAR = 2 };
+
+typedef struct {
+  int32_t abi_version;   /* ST_ABI_VERSION */
+  int32_t mode;          /* ST_EC_ZERO | ST_EC_CONSTANT | ST_EC_LINEAR */
+  int64_t n;             /* values per source field, >= 1 */
+  int32_t max_backlog;   /* steps whose truth may be outstanding, 1..64 */
+  int32_t device;        /* CUDA device ordinal */
+  void* stream;          /* cudaStream_t to run on, or NULL for a private stream */
+} st_ec_config;
+
+/* Create / destroy.  ST_ERR_INVALID_ARG on a bad config, ST_ERR_CUDA / ST_ERR_OOM on
+ * device failures (message via st_ec_last_error(NULL)). */
+st_status st_ec_init(const st_ec_config* cfg, st_ec** out);
+st_status st_ec_destroy(st_ec* ec);
+
+/* One Eulerian step.  received: k true source fields, oldest first, k*n floats
+ * (host or device memory, caller-owned, read before return for host pointers; may be
+ * NULL iff k == 0); they are the truths of the k oldest steps still pending.
+ * dt_ratio > 0 scales the extrapolated term (C-27; 1 for rates or constant steps).
+ * est: n floats (host or device) receive S^n_est.  Blocking: on return est is final.
+ * Errors: ST_ERR_INVALID_ARG (k < 0, dt_ratio <= 0, NULL pointers),
+ * ST_ERR_STATE (k > pending steps: a truth for a step never estimated — the protocol
+ * violation; or the backlog would exceed max_backlog), ST_ERR_CUDA. */
+st_status st_ec_step(st_ec* ec, int32_t k, const float* received, double dt_ratio, float* est);
+
+/* Conservation ledger, fp64: per value (each array n doubles, host, NULL to skip)
+ * Σ received truths, Σ emitted estimates, Σ estimates still pending; totals[3] (host,
+ * NULL to skip) = the same three summed over the n values. */
+st_status st_ec_ledger(st_ec* ec, double* cum_true, double* cum_est, double* pending, double* totals);
+
+/* Number of emitted steps whose truth has not been received. */
+st_status st_ec_backlog(st_ec* ec, int32_t* steps);
+
+/* Message of the last error on ec ("" if none); NULL ec: last init error. */
+const char* st_ec_last_error(const st_ec* ec);
+
 #ifdef __cplusplus
 }
 #endif

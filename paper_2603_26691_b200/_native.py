@@ -73,6 +73,20 @@ class StStats(ctypes.Structure):
 
 # every symbol include/scaletrack.h declares: name -> (restype, argtypes)
 _vp, _i32, _i64, _f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+EC_ZERO, EC_CONSTANT, EC_LINEAR = 0, 1, 2
+
+
+class StEcConfig(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("mode", ctypes.c_int32),
+        ("n", ctypes.c_int64),
+        ("max_backlog", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("stream", ctypes.c_void_p),
+    ]
+
+
 SIGNATURES = {
     "st_config_default": (None, [ctypes.POINTER(StConfig)]),
     "st_init": (_i32, [ctypes.POINTER(StConfig), ctypes.POINTER(_vp)]),
@@ -95,6 +109,12 @@ SIGNATURES = {
     "st_last_error": (ctypes.c_char_p, [_vp]),
     "st_abi_version": (_i32, []),
     "st_nccl_unique_id": (_i32, [_vp]),
+    "st_ec_init": (_i32, [ctypes.POINTER(StEcConfig), ctypes.POINTER(_vp)]),
+    "st_ec_destroy": (_i32, [_vp]),
+    "st_ec_step": (_i32, [_vp, _i32, _vp, _f64, _vp]),
+    "st_ec_ledger": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "st_ec_backlog": (_i32, [_vp, ctypes.POINTER(_i32)]),
+    "st_ec_last_error": (ctypes.c_char_p, [_vp]),
 }
 
 _lib = None

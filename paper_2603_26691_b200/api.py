@@ -225,3 +225,69 @@ class ScaleTrack:
         a, r = ctypes.c_float(), ctypes.c_float()
         self._check(self.lib.st_last_timings(self.h, ctypes.byref(a), ctypes.byref(r)))
         return a.value, r.value
+
+
+class Extrapolator:
+    """st_ec_*: the extrapolator-corrector of the asynchronous coupling (SURVEY §8(f1),
+    PAPER.md §2.4 Eq. 14-16) over source fields of `n` values.  Marshalling only: the
+    estimator runs in libscaletrack.so (csrc/st_ec.cu)."""
+
+    MODES = {"zero": N.EC_ZERO, "constant": N.EC_CONSTANT, "linear": N.EC_LINEAR}
+
+    def __init__(self, mode: str, n: int, max_backlog: int = 8, device: int = 0, stream=None):
+        self.lib = N.load()
+        c = N.StEcConfig()
+        c.abi_version = N.ST_ABI_VERSION
+        c.mode = self.MODES[mode]
+        c.n = int(n)
+        c.max_backlog = int(max_backlog)
+        c.device = int(device)
+        c.stream = stream
+        h = ctypes.c_void_p()
+        rc = self.lib.st_ec_init(ctypes.byref(c), ctypes.byref(h))
+        if rc:
+            raise N.StError(rc, self.lib.st_ec_last_error(None).decode())
+        self.h = h
+        self.n = int(n)
+
+    def _check(self, rc: int):
+        if rc:
+            raise N.StError(rc, self.lib.st_ec_last_error(self.h).decode())
+
+    def step(self, received=None, dt_ratio: float = 1.0, out=None):
+        """received: None, or k true fields stacked as [k, n] (numpy or torch, host or
+        CUDA), oldest first.  Returns S^n_est as float32 [n] (numpy unless `out`)."""
+        k = 0
+        if received is not None:
+            received = _as_f32(received)
+            k = int(received.shape[0]) if received.ndim > 1 else 1
+            numel = received.size if isinstance(received, np.ndarray) else received.numel()
+            if numel != k * self.n:
+                raise ValueError(f"received must hold k*n = {k}*{self.n} values")
+        if out is None:
+            out = np.empty(self.n, dtype=np.float32)
+        self._check(self.lib.st_ec_step(self.h, k, _ptr(received) if k else None, float(dt_ratio), _ptr(out)))
+        return out
+
+    def ledger(self):
+        """(Σ true received, Σ emitted, Σ pending) per value (fp64) and their totals."""
+        ct, ce, pe = (np.empty(self.n, dtype=np.float64) for _ in range(3))
+        tot = np.empty(3, dtype=np.float64)
+        self._check(self.lib.st_ec_ledger(self.h, _ptr(ct), _ptr(ce), _ptr(pe), _ptr(tot)))
+        return ct, ce, pe, tot
+
+    def backlog(self) -> int:
+        b = ctypes.c_int32()
+        self._check(self.lib.st_ec_backlog(self.h, ctypes.byref(b)))
+        return b.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.st_ec_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
