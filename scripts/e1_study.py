@@ -1,0 +1,180 @@
+#!/usr/bin/env python
+"""E1 (§3.1): a particle cloud moving at 1 m/s in a
+quiescent 0-D fluid box, two-way coupled; momentum errors of the conventional
+(sequential) coupling and of the asynchronous coupling with the zero / constant /
+linear extrapolators, against the analytical solution.
+
+The particle side is the library (st_advance + st_get_sources on the GPU, or the oracle
+with --backend oracle); the asynchronous schemes use the GPU extrapolator-corrector
+(st_ec_*) or the oracle estimator.  The fluid is the paper's box0d: one uniform velocity
+u_f with m_f du_f/dt = V <S>  (S: the momentum source rate per volume of st_get_sources).
+
+Analytical solution (Stokes drag, no gravity, r = m_p/m_f, λ = (1 + r)/τ):
+  u_p(t) = U + (u_p0 - u_f0) e^{-λt}/(1 + r),   u_f(t) = U - r (u_p0 - u_f0) e^{-λt}/(1 + r),
+  U = (m_p u_p0 + m_f u_f0)/(m_p + m_f).
+Choices the paper omits (SPEC's design decision): dt/τ = 0.1, m_p/m_f = 0.5.
+
+  python scripts/e1_study.py [--backend gpu|oracle] [--steps 60] [--out profiles/r1_e1_study.csv]
+"""
+from __future__ import annotations
+
+import argparse
+import math
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+RHO_F, NU_F, RHO_P = 1.2, 1.5e-5, 1000.0
+DIMS, H = (8, 8, 8), 1.0 / 64
+D = 20e-6
+TAU = RHO_P * D * D / (18 * RHO_F * NU_F)
+DT = 0.1 * TAU
+N = 4096
+V = (DIMS[0] * H) * (DIMS[1] * H) * (DIMS[2] * H)
+M_F = RHO_F * V
+M_ONE = math.pi / 6 * RHO_P * D ** 3
+W = 0.5 * M_F / (N * M_ONE)            # parcel weight: m_p/m_f = 0.5
+M_P = N * W * M_ONE
+SCHEMES = ("conventional", "zero", "constant", "linear")
+
+
+def exact(t):
+    r = M_P / M_F
+    lam = (1 + r) / TAU
+    U = M_P * 1.0 / (M_P + M_F)
+    up = U + math.exp(-lam * t) / (1 + r)
+    uf = U - r * math.exp(-lam * t) / (1 + r)
+    return up, uf
+
+
+class _GpuParticles:
+    def __init__(self, x, u, d, w):
+        from paper_2603_26691_b200 import BC_PERIODIC, DRAG_STOKES, TWO_WAY, Config, ScaleTrack
+        self.st = ScaleTrack(Config(dims=DIMS, cell_size=(H,) * 3, chunk_cells=8, bc=(BC_PERIODIC,) * 3,
+                                    rho_f=RHO_F, nu_f=NU_F, rho_p=RHO_P, gravity=(0.0, 0.0, 0.0),
+                                    drag_law=DRAG_STOKES, coupling=TWO_WAY, capacity=N))
+        self.st.inject(x, u, d, w)
+
+    def step(self, uf):
+        F = np.zeros((3,) + DIMS[::-1], np.float32)
+        F[0] = uf
+        self.st.set_fluid_field(F)
+        self.st.advance(DT, 1)
+        S, T = self.st.get_sources()
+        return np.asarray(S, np.float64).reshape(3, -1)
+
+    def momentum(self):
+        p = self.st.get_particles()
+        return float(np.sum(p["w"].astype(np.float64) * (math.pi / 6 * RHO_P * p["d"].astype(np.float64) ** 3) *
+                            p["u"][0].astype(np.float64)))
+
+
+class _OracleParticles:
+    def __init__(self, x, u, d, w):
+        import oracle
+        mesh = oracle.Mesh(DIMS, (0.0, 0.0, 0.0), (H,) * 3, 8, (oracle.BC_PERIODIC,) * 3)
+        phys = oracle.Physics(RHO_F, NU_F, RHO_P, (0.0, 0.0, 0.0), oracle.DRAG_STOKES, oracle.INT_EXPONENTIAL,
+                              oracle.TWO_WAY)
+        self.sim = oracle.Sim(mesh, phys, rebin_interval=1, precision="f32")
+        self.sim.inject(x, u, d, w)
+
+    def step(self, uf):
+        F = np.zeros((3,) + DIMS[::-1], np.float32)
+        F[0] = uf
+        self.sim.set_fluid_field(F)
+        self.sim.advance(DT, 1)
+        S, T = self.sim.get_sources()
+        return np.asarray(S, np.float64).reshape(3, -1)
+
+    def momentum(self):
+        p = self.sim.particles()
+        return float(np.sum(p["w"].astype(np.float64) * (math.pi / 6 * RHO_P * p["d"].astype(np.float64) ** 3) *
+                            p["u"][0].astype(np.float64)))
+
+
+def _estimator(mode, n, backend):
+    if backend == "gpu":
+        from paper_2603_26691_b200 import Extrapolator
+        e = Extrapolator(mode, n, max_backlog=4)
+        return lambda rec: e.step(None if rec is None else rec.astype(np.float32)[None, :]).astype(np.float64)
+    from oracle.extrapolator import Estimator
+    e = Estimator(mode, (n,), emit_dtype=np.float32, max_backlog=4)
+    return lambda rec: e.step([] if rec is None else [rec.astype(np.float32)]).astype(np.float64)
+
+
+def run(scheme: str, steps: int = 60, backend: str = "gpu", seed: int = 1):
+    """Momentum series of one scheme: dict(t, Pp, Pf, Pp_exact, Pf_exact, e_p, e_f)."""
+    rng = np.random.default_rng(seed)
+    L = DIMS[0] * H
+    x = rng.uniform(0, L, (3, N)).astype(np.float32)
+    u = np.zeros((3, N), np.float32)
+    u[0] = 1.0
+    d = np.full(N, D, np.float32)
+    w = np.full(N, W, np.float32)
+    parts = (_GpuParticles if backend == "gpu" else _OracleParticles)(x, u, d, w)
+    ncell = DIMS[0] * DIMS[1] * DIMS[2]
+    est = None if scheme == "conventional" else _estimator(scheme, ncell, backend)
+    uf = 0.0
+    S_prev = None                                     # truth of the previous Lagrangian step
+    given = 0.0                                       # momentum handed to the fluid so far
+    out = {k: [] for k in ("t", "Pp", "Pf", "Pp_exact", "Pf_exact", "P_lagr_out", "P_fluid_in")}
+    P_lagr = 0.0                                      # momentum the particles gave away (truths)
+    for n in range(1, steps + 1):
+        if scheme == "conventional":
+            # Euler step n with the sources of Lagrangian step n-1, then particles with u_f^n
+            if S_prev is not None:
+                uf += DT * S_prev[0].mean() / RHO_F
+                given += DT * S_prev[0].mean() * V
+            S_prev = parts.step(uf)
+            P_lagr += DT * S_prev[0].mean() * V
+        else:
+            # Euler step n and Lagrangian step n run concurrently: the fluid uses the
+            # estimate of S^n (truth of step n-1 just arrived), the particles u_f^{n-1}
+            uf_old = uf
+            S_est = est(S_prev[0] if S_prev is not None else None)
+            uf += DT * S_est.mean() / RHO_F
+            given += DT * S_est.mean() * V
+            S_prev = parts.step(uf_old)
+            P_lagr += DT * S_prev[0].mean() * V
+        t = n * DT
+        up_e, uf_e = exact(t)
+        out["t"].append(t)
+        out["Pp"].append(parts.momentum())
+        out["Pf"].append(M_F * uf)
+        out["Pp_exact"].append(M_P * up_e)
+        out["Pf_exact"].append(M_F * uf_e)
+        out["P_lagr_out"].append(P_lagr)
+        out["P_fluid_in"].append(given)
+    res = {k: np.array(v) for k, v in out.items()}
+    P0 = M_P * 1.0
+    res["e_p"] = (res["Pp"] - res["Pp_exact"]) / P0       # P:268 e_rel
+    res["e_f"] = (res["Pf"] - res["Pf_exact"]) / P0
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--backend", choices=["gpu", "oracle"], default="gpu")
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    cols, names = [], []
+    for s in SCHEMES:
+        r = run(s, a.steps, a.backend)
+        if not cols:
+            cols.append(r["t"]); names.append("t")
+        cols += [r["e_f"], r["e_p"]]
+        names += [f"{s}_e_fluid", f"{s}_e_particles"]
+        print(f"{s:12s} max|e_f| {np.abs(r['e_f']).max():.3e} (first 10 steps {np.abs(r['e_f'][:10]).max():.3e})  "
+              f"tail|e_f| {np.abs(r['e_f'][-10:]).max():.3e}  max|e_p| {np.abs(r['e_p']).max():.3e}")
+    if a.out:
+        np.savetxt(a.out, np.stack(cols, 1), delimiter=",", header=",".join(names), comments="")
+
+
+if __name__ == "__main__":
+    main()
