@@ -344,6 +344,7 @@ def run_ours(args):
                          "alg_bytes_per_launch": alg, "kernel_ms": kms},
             "step_kernel_ms": adv_ms, "rebin_prep_ms": reb_ms, "rebins_in_timed_region": len(reb_list),
             "f_move_chunk": f_move, "fused_rebins": st_stats["fused_rebins"],
+            "general_rebins": st_stats["general_rebins"], "far_last_rebin": st_stats["last_far"],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

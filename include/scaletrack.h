@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 1
+#define ST_ABI_VERSION 2
 
 typedef struct st_ctx st_ctx;   /* opaque; owns the particle store, fields, sources */
 typedef int32_t st_status;
@@ -121,6 +121,9 @@ typedef struct {
   int64_t last_recv_total;   /* particles received in the last rebin                  */
   int64_t fused_rebins;      /* rebins fused into the advance kernel                  */
   int64_t kernel_launches;   /* kernels launched by the library so far                */
+  int64_t general_rebins;    /* rebins that took the general radix sort               */
+  int64_t last_far;          /* particles > 1 cell from their bin placed in bin tails
+                                by the last neighbour-slot rebin (C-15b)              */
 } st_stats;
 
 /* Fill *cfg with defaults: 1 GPU, 16^3 unit box, periodic, chunk 8, air/water

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libscaletrack.so")
 
-ST_ABI_VERSION = 1
+ST_ABI_VERSION = 2
 
 ST_OK = 0
 STATUS_NAMES = {
@@ -67,7 +67,8 @@ class StStats(ctypes.Structure):
         ("n_particles", ctypes.c_int64), ("calls", ctypes.c_int64), ("rebins", ctypes.c_int64),
         ("last_movers", ctypes.c_int64), ("last_sent_total", ctypes.c_int64),
         ("last_recv_total", ctypes.c_int64), ("fused_rebins", ctypes.c_int64),
-        ("kernel_launches", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64), ("general_rebins", ctypes.c_int64),
+        ("last_far", ctypes.c_int64),
     ]
 
 

@@ -267,9 +267,21 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
         const int k = lb * kSlots + (j < 0 ? kStay : j);
         const long long e = dtab[k];                  // -1: leaves the domain; bits 61-62: side + 1
         const long long db = e < 0 ? -1 : (e & ((1LL << 61) - 1));
-        if (valid && (j < 0 || db < 0)) {
+        const bool farp = j < 0;                      // more than one cell from its bin
+        if (valid && !farp && db < 0) {
           flags |= ERRF_SCATTER;
           write_ok = false;
+        }
+        long long fdest = -1;
+        if (valid && farp) {
+          // C-15b: a far particle takes the next slot of its destination bin's tail
+          const int kz = c2 >> SH;
+          if (a.far_cur && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
+            fdest = (long long)atomicAdd(a.far_cur + bin_of_cell<SH>(g, a.bg, c0, c1, c2), 1ULL);
+          } else {
+            flags |= ERRF_SCATTER;
+            write_ok = false;
+          }
         }
         const bool stay = write_ok && j == kStay;
         // stayers: rank inside the lane's bin segment (lanes of one bin are contiguous)
@@ -286,7 +298,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           carry_lb = lb31;
         }
         // movers: groups of equal (bin, slot) keys
-        const int key = (write_ok && !stay) ? k : -1;
+        const int key = (write_ok && !stay && !farp) ? k : -1;
         const unsigned peers = __match_any_sync(kFull, key);
         if (key >= 0) {
           const int leader = __ffs(peers) - 1;
@@ -298,8 +310,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           rbase = __shfl_sync(peers, rb0, leader) + __popc(peers & lt);
         }
         __syncwarp();
-        if (VP) vside = e < 0 ? -1 : (int)(e >> 61) - 1;
-        dest = db + rbase;
+        if (VP) vside = (farp || e < 0) ? -1 : (int)(e >> 61) - 1;
+        dest = farp ? fdest : db + rbase;
         if (write_ok && (uint64_t)dest >= (uint64_t)((VP && vside >= 0) ? a.scap : a.n)) {
           flags |= ERRF_SCATTER;
           write_ok = false;

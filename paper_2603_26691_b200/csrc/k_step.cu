@@ -489,7 +489,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
 // The slot-major layout makes consecutive threads touch consecutive words.
 // Destinations d >= nbins are the virtual bins of the neighbour planes (multi-GPU):
 // d = nbins + side * nvb + v.
-__global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cnt_base, uint32_t* __restrict__ new_cnt) {
+__global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cnt_base, uint32_t* __restrict__ new_cnt,
+                             const int* __restrict__ far_cnt) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nbins + 2 * bg.nvb) return;
   int dx, dy, dz;
@@ -533,6 +534,8 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
     if (key[q] != 0x7fffffff) cnt_base[(int64_t)q * nbins + key[q]] = (int)base;
     total += (uint32_t)cnt[q];
   }
+  // far particles of this destination (C-15b) take the slots after its 27 runs
+  if (far_cnt && d < nbins) total += (uint32_t)far_cnt[d];
   new_cnt[d] = total;
 }
 
@@ -543,9 +546,11 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
 // the domain.  Row-major [nbins][27] so that one item (a chunk row of 8 bins) is one
 // contiguous 1728-byte bulk copy.
 __global__ void k_dbase(Geom g, BinGeom bg, int nbins, const int* __restrict__ base, const int64_t* __restrict__ off_new,
-                        const int64_t* __restrict__ voff0, const int64_t* __restrict__ voff1, long long* __restrict__ dtab) {
+                        const int64_t* __restrict__ voff0, const int64_t* __restrict__ voff1, long long* __restrict__ dtab,
+                        const int* __restrict__ far_cnt, unsigned long long* __restrict__ far_cur) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nbins) return;
+  if (far_cur) far_cur[s] = (unsigned long long)(off_new[s + 1] - far_cnt[s]);   // start of bin s's far tail
   int sx, sy, sz;
   cell_of_bin(g, bg, s, sx, sy, sz);
   const bool cell_ok = sx < g.n[0] && sy < g.n[1] && sz < g.n[2];
@@ -679,7 +684,16 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
           const int c1 = cell_from_t(cell_coord(xv[u][1], g.lo[1], g.ih[1]), g.n[1]);
           const int c2 = cell_from_t(cell_coord(xv[u][2], g.lo[2], g.ih[2]), g.n[2]);
           const int j = slot_of<BCM>(g, sx, sy, sz, c0, c1, c2);
-          if (j < 0) farflag = 1;
+          if (j < 0) {
+            // C-15b: a far particle whose cell is on this rank goes to its bin's tail
+            const int kz = dcc<SH>(c2, cc);
+            if (a.far_cnt && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
+              atomicAdd(a.far_cnt + bin_of_cell<SH>(a.g, a.bg, c0, c1, c2), 1);
+              atomicAdd(a.far_n, 1ULL);
+            }
+            else
+              farflag = 1;
+          }
           else if (j == kStay) ++scnt;
           else atomicAdd(&wc[lb * kSlots + j], 1);
           movers += ((dcc<SH>(c0, cc) != dcc<SH>(sx, cc)) | (dcc<SH>(c1, cc) != dcc<SH>(sy, cc)) |
@@ -840,8 +854,10 @@ int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s) {
   return launch_mode<false, true>(a, s);
 }
 
-int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s) {
-  k_rebin_prep<<<blocks_for((int64_t)bg.nbins + 2 * bg.nvb, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt);
+int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, const int* far_cnt,
+                      cudaStream_t s) {
+  k_rebin_prep<<<blocks_for((int64_t)bg.nbins + 2 * bg.nvb, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt,
+                                                                               far_cnt);
   return 1;
 }
 
@@ -873,8 +889,8 @@ int launch_count_v(const CountArgs& a, cudaStream_t s) {
 }
 
 int launch_dbase(const Geom& g, const BinGeom& bg, const int* base, const int64_t* off_new, const int64_t* voff0,
-                 const int64_t* voff1, long long* dtab, cudaStream_t s) {
-  k_dbase<<<blocks_for(bg.nbins), 256, 0, s>>>(g, bg, bg.nbins, base, off_new, voff0, voff1, dtab);
+                 const int64_t* voff1, long long* dtab, const int* far_cnt, unsigned long long* far_cur, cudaStream_t s) {
+  k_dbase<<<blocks_for(bg.nbins), 256, 0, s>>>(g, bg, bg.nbins, base, off_new, voff0, voff1, dtab, far_cnt, far_cur);
   return 1;
 }
 

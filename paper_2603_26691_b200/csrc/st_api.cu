@@ -45,6 +45,10 @@ struct st_ctx {
   CUtensorMap tmap[4];        // [2 stores][float rows, ids] TMA descriptors (kernel parameters)
   CUtensorMap tmap_win[2][2]; // [field buffer][window shape] TMA descriptors of the fluid field
   long long* dtab = nullptr;  // [nbins][27] destination table of the fused scatter (k_dbase)
+  int* far_cnt = nullptr;     // [nbins] far particles per destination bin (C-15b; k_count)
+  unsigned long long* far_cur = nullptr;  // [nbins] far-tail cursors of the new layout (k_dbase)
+  unsigned long long* d_far_n = nullptr;  // far particles placed by the last count (C-15b)
+  int64_t general_rebins = 0;
   int32_t* key[2] = {nullptr, nullptr};
   SortScratch sc;
   uint64_t next_id = 0;
@@ -418,7 +422,11 @@ static st_status init_impl(st_ctx* c) {
     ST_CUDA(c, cudaMalloc(&c->n_items[i], sizeof(int)));
   }
   ST_CUDA(c, cudaMalloc(&c->hist, nb * 27 * sizeof(int)));
-  if (c->g.cc == 8) ST_CUDA(c, cudaMalloc(&c->dtab, nb * 27 * sizeof(long long)));
+  if (c->g.cc == 8) {
+    ST_CUDA(c, cudaMalloc(&c->dtab, nb * 27 * sizeof(long long)));
+    ST_CUDA(c, cudaMalloc(&c->far_cnt, nb * sizeof(int)));
+    ST_CUDA(c, cudaMalloc(&c->far_cur, nb * sizeof(unsigned long long)));
+  }
   ST_CUDA(c, cudaMalloc(&c->new_cnt, (nb + 2 * (size_t)c->bg.nvb + 1) * sizeof(uint32_t)));
   if (c->bg.nvb > 0) {
     const size_t nv = (size_t)c->bg.nvb;
@@ -447,6 +455,8 @@ static st_status init_impl(st_ctx* c) {
   ST_CUDA(c, cudaHostAlloc(&c->h_farg, sizeof(int), cudaHostAllocDefault));
   ST_CUDA(c, cudaMalloc(&c->d_farg, sizeof(int)));
   ST_CUDA(c, cudaMalloc(&c->d_movers, sizeof(unsigned long long)));
+  ST_CUDA(c, cudaMalloc(&c->d_far_n, sizeof(unsigned long long)));
+  ST_CUDA(c, cudaMemset(c->d_far_n, 0, sizeof(unsigned long long)));
   ST_CUDA(c, cudaMemset(c->d_movers, 0, sizeof(unsigned long long)));
   // radix-sort scratch (also serves the scans over bins)
   c->sc.max_blocks = (c->cap + 4095) / 4096 + 1;
@@ -510,6 +520,9 @@ st_status st_destroy(st_ctx* c) {
   if (c->ev_count) cudaEventDestroy(c->ev_count);
   cudaFree(c->hist);
   cudaFree(c->dtab);
+  cudaFree(c->far_cnt);
+  cudaFree(c->far_cur);
+  cudaFree(c->d_far_n);
   cudaFree(c->sc.hist);
   cudaFree(c->sc.offs);
   cudaFree(c->sc.partial);
@@ -655,6 +668,7 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.tm_win[0] = c->tmap_win[c->front < 0 ? 0 : c->front][0];
   a.tm_win[1] = c->tmap_win[c->front < 0 ? 0 : c->front][1];
   a.dtab = c->dtab;
+  a.far_cur = c->far_cur;
   a.cap = c->cap;
   a.n = c->n;
   a.off = c->off[c->lay];
@@ -721,6 +735,7 @@ static st_status general_rebin(st_ctx* c) {
   c->binned = true;
   c->rebin_due = false;
   c->rebins += 1;
+  c->general_rebins += 1;
   return ST_OK;
 }
 
@@ -743,6 +758,10 @@ static st_status count_slots(st_ctx* c, bool* far) {
   ca.nbins = c->bg.nbins;
   ca.hist = c->hist;
   ca.movers = c->d_movers;
+  ca.far_n = c->d_far_n;
+  ST_CUDA(c, cudaMemsetAsync(c->d_far_n, 0, sizeof(unsigned long long), c->cs));
+  ca.far_cnt = c->far_cnt;   // NULL unless 8^3 chunks (k_pstep): then far particles stay on the fused path
+  if (c->far_cnt) ST_CUDA(c, cudaMemsetAsync(c->far_cnt, 0, (size_t)c->bg.nbins * sizeof(int), c->cs));
   ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));   // the rebin's timing starts with the count
   c->reb_t0 = true;
   ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
@@ -779,7 +798,7 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   const int nb = c->bg.nbins, nv = c->bg.nvb;
   if (!c->reb_t0) ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
   c->reb_t0 = false;
-  int nl = launch_rebin_prep(g, c->bg, c->hist, c->new_cnt, c->cs);
+  int nl = launch_rebin_prep(g, c->bg, c->hist, c->new_cnt, c->far_cnt, c->cs);
   st_status s;
   if (c->comm) {
     if ((s = check_launch(c, nl))) return s;
@@ -803,7 +822,7 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   nl += launch_exclusive_scan_u32(c->new_cnt, nb, c->off[nlay], c->sc.partial, c->cs);
   if (c->dtab)
     nl += launch_dbase(g, c->bg, c->hist, c->off[nlay], nv > 0 ? c->voff[0] : nullptr, nv > 0 ? c->voff[1] : nullptr,
-                       c->dtab, c->cs);
+                       c->dtab, c->far_cnt, c->far_cur, c->cs);
   nl += launch_items(c->off[nlay], nb, g.cc, c->item_flag, c->item_pos, c->sc.partial, c->items[nlay], c->n_items[nlay],
                      c->cs);
   ST_CUDA(c, cudaEventRecord(c->t_reb1, c->cs));
@@ -1129,6 +1148,10 @@ st_status st_get_stats(st_ctx* c, st_stats* o) {
   o->last_recv_total = c->last_recv;
   o->fused_rebins = c->fused_rebins;
   o->kernel_launches = c->launches;
+  unsigned long long fn = 0;
+  ST_CUDA(c, cudaMemcpy(&fn, c->d_far_n, sizeof(fn), cudaMemcpyDeviceToHost));
+  o->general_rebins = c->general_rebins;
+  o->last_far = (int64_t)fn;
   return ST_OK;
 }
 

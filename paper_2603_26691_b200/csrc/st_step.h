@@ -39,6 +39,7 @@ struct StepArgs {
   const int64_t* off_new;     // [nbins+1] CSR of B (scatter)
   const int* slot_base;       // [27][nbins] base[j][s] (scatter; rebin_prep output; k_step)
   const long long* dtab;      // [nbins][27] destination table (scatter; k_dbase output; k_pstep)
+  unsigned long long* far_cur;// [nbins] next free slot of each bin's far tail (C-15b), or NULL
   const int* item_bin0;       // warp items of A
   const int* n_items;
   int nbins;
@@ -73,7 +74,8 @@ struct InsertArgs {
 int launch_insert(const InsertArgs& a, cudaStream_t s);
 
 int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s);
-int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, cudaStream_t s);
+int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, const int* far_cnt,
+                      cudaStream_t s);
 // Slot histogram of the current layout (k_count): input of the next neighbour-slot rebin
 struct CountArgs {
   Geom g;
@@ -85,13 +87,17 @@ struct CountArgs {
   const int* n_items;
   int nbins;
   int* hist;                  // [27][nbins] out: hist[j][s] (every entry written)
-  int* far;                   // set to 1 if a particle is more than one cell from its bin
+  int* far;                   // set to 1 if a far particle cannot be placed by the fused rebin
+  int* far_cnt;               // [nbins] far particles per destination bin (C-15b), or NULL:
+                              // any particle more than one cell from its bin sets *far
   unsigned long long* movers; // += particles whose current chunk differs from their bin's chunk
+  unsigned long long* far_n;  // += far particles placed in bin tails
 };
 int launch_count(const CountArgs& a, cudaStream_t s);
 // destination table [nbins][27] of k_pstep from the prep bases and the new offsets
 int launch_dbase(const Geom& g, const BinGeom& bg, const int* base, const int64_t* off_new, const int64_t* voff0,
-                 const int64_t* voff1, long long* dtab, cudaStream_t s);
+                 const int64_t* voff1, long long* dtab, const int* far_cnt, unsigned long long* far_cur,
+                 cudaStream_t s);
 int launch_items(const int64_t* off, int nbins, int cc, uint32_t* flag, int64_t* pos, int64_t* partial,
                  int* item_bin0, int* n_items, cudaStream_t s);
 int launch_bin_offsets(const int32_t* key_sorted, int64_t n, int nbins, int64_t* off, cudaStream_t s);

@@ -127,19 +127,54 @@ def test_fused_rebin_then_observe():
     _check_rebin_given_gpu_positions(o, before, after)
 
 
-def test_far_movers_fall_back_to_general_sort():
-    """Particles moving more than one cell between rebins (K = 8, fast flow) take the
-    general radix path; the order is still the contract's."""
+def _check_rebin_c15b(o, P0, after):
+    """C-15 / C-15b: P0 is the layout of the previous rebin (every particle in its own
+    cell's bin), `after` the layout of this one.  Every particle sits in the bin of its
+    cell, bins ascending; within a bin the particles within one cell (per axis,
+    periodic) of their previous bin come first, in their previous store order (the
+    stable counting sort), then the far ones (any order)."""
+    nx, ny, nz = o.mesh.dims
+    key = o.bin_key(after["x"]).astype(np.int64)
+    assert np.all(np.diff(key) >= 0)
+    pos = {int(i): k for k, i in enumerate(P0["id"])}
+    src = np.array([pos[int(i)] for i in after["id"]])
+    c_old, _ = o.locate(P0["x"][:, src])
+    c_new, _ = o.locate(after["x"])
+    far = np.zeros(len(src), bool)
+    for a, n, div in ((0, nx, 1), (1, ny, nx), (2, nz, nx * ny)):
+        d = (c_new // div) % n - (c_old // div) % n
+        if o.mesh.bc[a] == oracle.BC_PERIODIC:
+            d = (d + n // 2) % n - n // 2 if n > 2 else d
+        far |= np.abs(d) > 1
+    starts = np.flatnonzero(np.r_[True, np.diff(key) != 0])
+    ends = np.r_[starts[1:], len(key)]
+    for b0, b1 in zip(starts, ends):
+        f = far[b0:b1]
+        nf = int((~f).sum())
+        assert not f[:nf].any(), "far particles before near ones in a bin"
+        assert np.all(np.diff(src[b0:b0 + nf]) > 0), "near particles out of stable order"
+    return int(far.sum())
+
+
+def test_far_movers_placed_in_bin_tails():
+    """Particles moving more than one cell between rebins (K = 8, fast flow) stay on the
+    fused neighbour-slot path: placed at the tail of their destination bin (C-15b) — no
+    general sort."""
     wl = synth.workload("C2", n_particles=100_000)
     g, o, _, F = _setup(wl, rebin_interval=8)
-    F2 = (F * 20.0).astype(np.float32)       # up to 20 m/s: several cells per 8 calls
+    F2 = (F * 20.0).astype(np.float32)        # up to 20 m/s: several cells per 8 calls
     g.set_fluid_field(F2)
-    for _ in range(15):
-        g.advance(wl.dt, 1)
-    before = g.get_particles()
-    g.advance(wl.dt, 1)                       # call 16 ends with a rebin
+    for _ in range(8):
+        g.advance(wl.dt, 1)                    # call 8 leaves a rebin due
+    P8 = g.get_particles()                     # flushed: every particle in its cell's bin
+    gen0 = g.stats()["general_rebins"]
+    for _ in range(8):
+        g.advance(wl.dt, 1)                    # call 16 leaves the next one due
     after = g.get_particles()
-    _check_rebin_given_gpu_positions(o, before, after)
+    st = g.stats()
+    nfar = _check_rebin_c15b(o, P8, after)
+    assert nfar > 100 and st["last_far"] == nfar, (nfar, st["last_far"])
+    assert st["general_rebins"] == gen0
 
 
 # ------------------------------------------------------------------ closed form through the GPU
