@@ -38,9 +38,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C5", choices=["C3", "C4", "C5"])
     ap.add_argument("--particles", type=float, default=None, help="particles per GPU (default: the workload's)")
-    ap.add_argument("--rebin-interval", type=int, default=1,
-                    help="K: rebin (fused neighbour scatter) every K-th step; the scatter needs K * |u|max dt / h < 1, "
-                         "else the rebin falls back to the general sort (DESIGN.md section 9)")
+    ap.add_argument("--rebin-interval", type=int, default=2,
+                    help="K: rebin (fused neighbour scatter) every K-th step; particles that moved more than one "
+                         "cell in between go to their bin's far tail (C-15b, DESIGN.md section 9)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target oracle CPU time for cpu_baseline")
