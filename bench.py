@@ -237,9 +237,10 @@ def run_ours(args):
         st.advance(wl.dt, 1)
         st.get_sources(Sdst)
 
-    # setup (untimed): K calls so the first rebin after injection (a full sort of the
-    # randomly injected store) happens before the warm-up; then W warm-up steps
-    for s in range(K + args.warmup):
+    # setup (untimed): 2K + 1 calls — the first rebin after injection (a full sort of the
+    # randomly injected store) at call K, then one whole K-cycle including a fused
+    # neighbour-slot rebin, so every kernel has run once — then W warm-up steps
+    for s in range(2 * K + 1 + args.warmup):
         step(s, fields, S)
     torch.cuda.synchronize()
     if G > 1:

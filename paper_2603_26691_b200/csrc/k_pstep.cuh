@@ -65,7 +65,7 @@ constexpr int kTable = kRowBins * kSlots;           // destination table entries
 // per-warp slice: stages | fluid window | [scatter: table i64[216], run i32[216]] | rel[9] | mbarriers
 constexpr int kOffWin = kPStages * kTStageBytes;
 __host__ __device__ constexpr int off_tab(bool scatter) { return kOffWin + win_cells(scatter) * 16; }
-__host__ __device__ constexpr int off_rel(bool scatter) { return off_tab(scatter) + (scatter ? kTable * 12 : 0); }
+__host__ __device__ constexpr int off_rel(bool scatter) { return off_tab(scatter) + (scatter ? kTable * 12 : kTable * 4); }
 __host__ __device__ constexpr int off_bar(bool scatter) { return off_rel(scatter) + 48; }
 __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
   return (off_bar(scatter) + 8 * (kPStages + 1) + 127) / 128 * 128;
@@ -101,13 +101,16 @@ __device__ __forceinline__ void tstage_issue(TStage* st, unsigned long long* bar
 }
 
 #ifndef ST_PMINB
-#define ST_PMINB 2
+#define ST_PMINB 2      // CTAs per SM of the fused scatter
+#endif
+#ifndef ST_PMINB_IP
+#define ST_PMINB_IP 3   // CTAs per SM of the in-place step (4: 64 registers, spills)
 #endif
 constexpr int kSpecVP = 1;    // neighbour-rank planes (send buffers) may be destinations
 constexpr int kSpecSub = 2;   // more than one sub-step per call
 constexpr int kSpecAll = 3;
 template <bool SCATTER, bool ADVANCE, int BCM, int SPEC = kSpecAll, int FEAT = 0xff>
-__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_pstep(const __grid_constant__ StepArgs a) {
+__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMINB_IP) k_pstep(const __grid_constant__ StepArgs a) {
   constexpr int SH = 3;   // chunk_cells == 8
   constexpr bool VP = (SPEC & kSpecVP) != 0;
   extern __shared__ __align__(128) unsigned char psmem_raw[];
@@ -120,6 +123,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
   float4* win = reinterpret_cast<float4*>(ws + kOffWin);
   long long* dtab = reinterpret_cast<long long*>(ws + off_tab(SCATTER));                 // [8*27]
   int* run = reinterpret_cast<int*>(ws + off_tab(SCATTER) + kTable * 8);                  // [8*27]
+  int* cnt_s = reinterpret_cast<int*>(ws + off_tab(SCATTER));      // [8*27] slot counts (in place, counting)
   int* rel = reinterpret_cast<int*>(ws + off_rel(SCATTER));                               // [kRowBins+1]
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + off_bar(SCATTER));  // stages | item
   unsigned long long* ibar = bar + kPStages;
@@ -130,6 +134,11 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
   const int nbins = a.nbins;
   const int pz = g.gy * g.gx;
   const bool two_way = (FEAT & 4) && a.p.two_way;
+  // in place, when this call makes a rebin due: count the slot histogram of the item's
+  // bins here (the warp owns them) instead of a later k_count pass over x
+  const bool counting = !SCATTER && ADVANCE && a.cnt_hist != nullptr;
+  unsigned cmov = 0;
+  int cfar = 0;
   int flags = 0;
   uint32_t phase = 0, iphase = 0;
   if (lane == 0) {
@@ -165,6 +174,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
     if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
     if (SCATTER)
       for (int k = lane; k < kTable; k += 32) run[k] = 0;
+    if (counting)
+      for (int k = lane; k < kTable; k += 32) cnt_s[k] = 0;
     if ((FEAT & 2) || SCATTER) {
       mbar_wait(ibar, iphase);
       iphase ^= 1u;
@@ -172,8 +183,8 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
     __syncwarp();
     const int az_row = acc_z(g, rz);
     int lb = 0;
-    // per-lane stayer deposit accumulator (da*) of bin st_lb
-    int st_lb = -1;
+    // per-lane stayer accumulators of bin st_lb: deposit (da*), slot count (hcnt)
+    int st_lb = -1, hcnt = 0;
     float da0 = 0.f, da1 = 0.f, da2 = 0.f;
     int carry_lb = -1, carry = 0;                 // stayers of bin carry_lb placed by earlier batches
     for (int bi = 0; bi <= nbatch; ++bi) {
@@ -184,7 +195,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
       if (!last)
         while (rel[lb + 1] <= r) ++lb;
       // flush the stayer accumulators of lanes whose bin changed (one group per bin)
-      if (two_way) {
+      if (two_way || counting) {
         const bool fl = st_lb >= 0 && (last || lb != st_lb);
         unsigned todo = __ballot_sync(kFull, fl);
         while (todo) {
@@ -192,12 +203,19 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           const int kb = __shfl_sync(kFull, st_lb, ld);
           const bool in = fl && st_lb == kb;
           todo &= ~__ballot_sync(kFull, in);
-          float ra = da0, rb = da1, rc = da2;
-          group_sum3(in, ra, rb, rc);
-          if (lane == ld) red_add_v4(a.acc + ((int64_t)az_row * g.n[1] + ry) * g.n[0] + rx + kb, ra, rb, rc);
+          if (two_way) {
+            float ra = da0, rb = da1, rc = da2;
+            group_sum3(in, ra, rb, rc);
+            if (lane == ld) red_add_v4(a.acc + ((int64_t)az_row * g.n[1] + ry) * g.n[0] + rx + kb, ra, rb, rc);
+          }
+          if (counting) {
+            const int hc = (int)__reduce_add_sync(kFull, in ? (unsigned)hcnt : 0u);
+            if (lane == ld && hc) cnt_s[kb * kSlots + kStay] += hc;
+          }
         }
         if (fl || st_lb < 0) {
           st_lb = lb;
+          hcnt = 0;
           da0 = da1 = da2 = 0.f;
         }
       }
@@ -400,6 +418,27 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
           if (bad && valid) flags |= ERRF_CFL;
         }
       }
+      if (counting && valid) {
+        // slot of the end cell relative to the bin (the next rebin's input)
+        const int e0 = cell_from_t(cell_coord(xp0, g.lo[0], g.ih[0]), g.n[0]);
+        const int e1 = cell_from_t(cell_coord(xp1, g.lo[1], g.ih[1]), g.n[1]);
+        const int e2 = cell_from_t(cell_coord(xp2, g.lo[2], g.ih[2]), g.n[2]);
+        const int j2 = slot_of<BCM>(g, sx, sy, sz, e0, e1, e2);
+        if (j2 == kStay) {
+          ++hcnt;
+        } else if (j2 >= 0) {
+          atomicAdd(&cnt_s[lb * kSlots + j2], 1);
+        } else {   // far (C-15b): counted for the bin of its cell when that is on this rank
+          const int kz = e2 >> SH;
+          if (a.cnt_far_cnt && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
+            atomicAdd(a.cnt_far_cnt + bin_of_cell<SH>(g, a.bg, e0, e1, e2), 1);
+            atomicAdd(a.cnt_far_n, 1ULL);
+          } else {
+            cfar = 1;
+          }
+        }
+        cmov += ((e0 >> SH) != (sx >> SH)) | ((e1 >> SH) != (sy >> SH)) | ((e2 >> SH) != (sz >> SH));
+      }
       if ((FEAT & 16) && write_ok) {
         if (SCATTER) {
           const Store& o = (VP && vside >= 0) ? a.sbuf[vside] : a.B;
@@ -416,6 +455,19 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : 4) k_ps
       }
     }
     __syncwarp();
+    if (counting) {   // the item's bins are this warp's: plain stores, every entry
+      for (int k = lane; k < nb * kSlots; k += 32) {
+        const int l = k / kSlots, j = k - l * kSlots;
+        a.cnt_hist[(int64_t)j * nbins + b0 + l] = cnt_s[k];
+      }
+      __syncwarp();
+    }
+  }
+  if (counting) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cmov += __shfl_xor_sync(kFull, cmov, o);
+    if (lane == 0 && cmov) atomicAdd(a.cnt_movers, (unsigned long long)cmov);
+    if (cfar) *(volatile int*)a.cnt_far = 1;
   }
   if (flags) atomicOr(a.err, flags);
 }

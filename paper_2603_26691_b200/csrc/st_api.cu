@@ -49,6 +49,7 @@ struct st_ctx {
   unsigned long long* far_cur = nullptr;  // [nbins] far-tail cursors of the new layout (k_dbase)
   unsigned long long* d_far_n = nullptr;  // far particles placed by the last count (C-15b)
   int64_t general_rebins = 0;
+  bool hist_ready = false;    // the last in-place step produced the next rebin's counts
   int32_t* key[2] = {nullptr, nullptr};
   SortScratch sc;
   uint64_t next_id = 0;
@@ -613,7 +614,7 @@ st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const 
     if (fr) return fr;
   }
   if (n == 0) {
-    if (c->comm) c->binned = false;   // collective: every rank leaves the binned state together
+    if (c->comm) c->binned = c->hist_ready = false;   // collective: every rank leaves the binned state together
     return ST_OK;
   }
   if (!x || !u || !d) return fail(c, ST_ERR_INVALID_ARG, "x, u and d are required");
@@ -646,6 +647,7 @@ st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const 
   if (!id) c->next_id += (uint64_t)n;
   c->n += n;
   c->binned = false;
+  c->hist_ready = false;
   return ST_OK;
 }
 
@@ -736,6 +738,7 @@ static st_status general_rebin(st_ctx* c) {
   c->rebin_due = false;
   c->rebins += 1;
   c->general_rebins += 1;
+  c->hist_ready = false;
   return ST_OK;
 }
 
@@ -746,6 +749,18 @@ static st_status general_rebin(st_ctx* c) {
 static st_status count_slots(st_ctx* c, bool* far) {
   *far = true;
   if (!c->binned) return ST_OK;
+  if (c->hist_ready) {   // counted by the in-place step that made this rebin due
+    c->hist_ready = false;
+    ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
+    c->reb_t0 = true;
+    if (c->comm) {
+      *far = false;
+      return ST_OK;
+    }
+    ST_CUDA(c, cudaEventSynchronize(c->ev_step_done));
+    *far = *(volatile int*)c->h_far != 0;
+    return ST_OK;
+  }
   CountArgs ca;
   memset(&ca, 0, sizeof(ca));
   ca.g = c->g;
@@ -941,6 +956,26 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
     ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
     if (c->binned) {
       StepArgs a = step_args(c, (float)dt, nsteps);
+      // this call makes a rebin due: let the in-place kernel count its bins' slots
+      // (8^3 chunks: k_pstep) so the rebin needs no k_count pass
+      if (c->dtab && (c->calls + 1) % c->cfg.rebin_interval == 0) {
+        ST_CUDA(c, cudaMemsetAsync(c->d_movers, 0, sizeof(unsigned long long), c->cs));
+        ST_CUDA(c, cudaMemsetAsync(c->d_far_n, 0, sizeof(unsigned long long), c->cs));
+        ST_CUDA(c, cudaMemsetAsync(c->far_cnt, 0, (size_t)c->bg.nbins * sizeof(int), c->cs));
+        if (c->comm) {
+          ST_CUDA(c, cudaMemsetAsync(c->d_farg, 0, sizeof(int), c->cs));
+          a.cnt_far = c->d_farg;
+        } else {
+          ST_CUDA(c, cudaEventSynchronize(c->ev_count));   // no kernel still writes the flag
+          *c->h_far = 0;
+          a.cnt_far = c->d_far;
+        }
+        a.cnt_hist = c->hist;
+        a.cnt_far_cnt = c->far_cnt;
+        a.cnt_movers = c->d_movers;
+        a.cnt_far_n = c->d_far_n;
+        c->hist_ready = true;
+      }
       st = check_launch(c, launch_step(a, false, true, c->cs));
       if (st) return st;
     } else {

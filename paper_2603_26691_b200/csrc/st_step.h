@@ -40,6 +40,13 @@ struct StepArgs {
   const int* slot_base;       // [27][nbins] base[j][s] (scatter; rebin_prep output; k_step)
   const long long* dtab;      // [nbins][27] destination table (scatter; k_dbase output; k_pstep)
   unsigned long long* far_cur;// [nbins] next free slot of each bin's far tail (C-15b), or NULL
+  // slot histogram produced by an in-place step whose call makes a rebin due (k_count's
+  // outputs, same meaning; cnt_hist == NULL: not produced by this launch)
+  int* cnt_hist;
+  int* cnt_far;
+  int* cnt_far_cnt;
+  unsigned long long* cnt_movers;
+  unsigned long long* cnt_far_n;
   const int* item_bin0;       // warp items of A
   const int* n_items;
   int nbins;

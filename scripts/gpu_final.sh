@@ -9,5 +9,5 @@ timeout 900 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?"
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launch list rc=$?"
 timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
-  -k regex:"k_pstep|k_count" -s 4 -c 4 --log-file gpurun_out/traffic_$TAG.csv \
+  -k regex:"k_pstep|k_count" -s 6 -c 6 --log-file gpurun_out/traffic_$TAG.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_traffic_$TAG.log 2>&1; echo "ncu traffic rc=$?"
