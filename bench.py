@@ -37,6 +37,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C5", choices=["C3", "C4", "C5"])
+    ap.add_argument("--decomp", default="slab", choices=["slab", "sharded"],
+                    help="slab: z-slabs with migration (north star); sharded: every GPU holds the whole "
+                         "domain, particles stay, sources all-reduced (PAPER Fig. 1c, SURVEY f2)")
     ap.add_argument("--particles", type=float, default=None, help="particles per GPU (default: the workload's)")
     ap.add_argument("--rebin-interval", type=int, default=2,
                     help="K: rebin (fused neighbour scatter) every K-th step; particles that moved more than one "
@@ -212,7 +215,8 @@ def run_ours(args):
     cap = n_per if G == 1 else int(n_per * 1.05) + 1_000_000
     cfg = Config(dims=wl.dims, origin=wl.origin, cell_size=wl.cell_size, chunk_cells=wl.chunk_cells, bc=wl.bc,
                  rho_f=synth.RHO_F, nu_f=synth.NU_F, rho_p=synth.RHO_P, gravity=wl.gravity, drag_law=wl.drag_law,
-                 coupling=wl.coupling, rebin_interval=K, capacity=cap, device=local, rank=rank, nranks=G)
+                 coupling=wl.coupling, rebin_interval=K, capacity=cap, device=local, rank=rank, nranks=G,
+                 decomposition=1 if args.decomp == "sharded" else 0)
     st = ScaleTrack(cfg, stream=stream.cuda_stream, unique_id=uid)
     lay = st.layout
     z_range = (lay.z0, lay.z1)
@@ -339,7 +343,7 @@ def run_ours(args):
                        "particles_per_gpu": n_per, "grid": list(wl.dims), "chunk_cells": wl.chunk_cells,
                        "rebin_interval": K, "substeps_per_step": 1,
                        "l2": "inputs larger than L2 (40 B x N resident particle state)",
-                       "parallelism": f"z-slab x{G}"},
+                       "parallelism": f"z-slab x{G}" if args.decomp == "slab" else f"particle-sharded x{G}"},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg, "kernel_ms": kms},

@@ -82,6 +82,13 @@ enum { ST_ONE_WAY = 0, ST_TWO_WAY = 1 };                        /* P:69 */
  *   device                  : CUDA ordinal; stream: cudaStream_t (NULL = library's own).
  *   rank, nranks            : position in the one-box job (nranks == 1: single GPU).
  *   nccl_unique_id          : 128-byte ncclUniqueId broadcast by the caller (nranks > 1).
+ *   decomposition           : ST_DECOMP_SLAB (default): z-slabs of chunk planes, particles
+ *                             migrate to the rank owning their chunk (north star).
+ *                             ST_DECOMP_SHARDED: the paper's own scheme (Fig. 1c, P:181-185;
+ *                             SURVEY §8(f2)): every rank holds the whole domain and the whole
+ *                             fluid field, particles stay on the rank that injected them (no
+ *                             migration), st_get_sources returns the sources of the whole
+ *                             domain summed over all ranks (one NCCL all-reduce, collective).
  */
 typedef struct {
   int32_t abi_version;
@@ -99,7 +106,10 @@ typedef struct {
   void* stream;
   int32_t rank, nranks;
   const void* nccl_unique_id;
+  int32_t decomposition;
 } st_config;
+
+enum { ST_DECOMP_SLAB = 0, ST_DECOMP_SHARDED = 1 };
 
 /* Geometry of this rank's share of the mesh (filled by st_get_layout). */
 typedef struct {

@@ -2,12 +2,13 @@
 Lagrangian particle step as sm_100a CUDA kernels behind a C ABI
 (include/scaletrack.h).  This package is the thin Python binding; see DESIGN.md.
 """
-from ._native import (BC_PERIODIC, BC_REFLECT, DRAG_SCHILLER_NAUMANN, DRAG_STOKES, INT_EXPONENTIAL,
+from ._native import (BC_PERIODIC, BC_REFLECT, DECOMP_SHARDED, DECOMP_SLAB, DRAG_SCHILLER_NAUMANN, DRAG_STOKES,
+                      INT_EXPONENTIAL,
                       INT_SEMI_IMPLICIT, ONE_WAY, TWO_WAY, StError)
 from .api import Config, Extrapolator, ScaleTrack, nccl_unique_id, plan_layout
 
 __all__ = [
     "Config", "Extrapolator", "ScaleTrack", "StError", "nccl_unique_id", "plan_layout",
     "BC_PERIODIC", "BC_REFLECT", "DRAG_STOKES", "DRAG_SCHILLER_NAUMANN",
-    "INT_EXPONENTIAL", "INT_SEMI_IMPLICIT", "ONE_WAY", "TWO_WAY",
+    "INT_EXPONENTIAL", "INT_SEMI_IMPLICIT", "ONE_WAY", "TWO_WAY", "DECOMP_SLAB", "DECOMP_SHARDED",
 ]

@@ -21,6 +21,7 @@ STATUS_NAMES = {
     8: "ST_ERR_OOM", 9: "ST_ERR_UNSUPPORTED",
 }
 BC_PERIODIC, BC_REFLECT = 0, 1
+DECOMP_SLAB, DECOMP_SHARDED = 0, 1
 DRAG_STOKES, DRAG_SCHILLER_NAUMANN = 0, 1
 INT_EXPONENTIAL, INT_SEMI_IMPLICIT = 0, 1
 ONE_WAY, TWO_WAY = 0, 1
@@ -48,6 +49,7 @@ class StConfig(ctypes.Structure):
         ("rank", ctypes.c_int32),
         ("nranks", ctypes.c_int32),
         ("nccl_unique_id", ctypes.c_void_p),
+        ("decomposition", ctypes.c_int32),
     ]
 
 

@@ -59,6 +59,7 @@ class Config:
     device: int = 0
     rank: int = 0
     nranks: int = 1
+    decomposition: int = 0       # N.DECOMP_SLAB | N.DECOMP_SHARDED
 
     def to_c(self, stream=None, unique_id: bytes | None = None) -> N.StConfig:
         c = N.StConfig()
@@ -77,6 +78,7 @@ class Config:
         c.device = int(self.device)
         c.stream = stream
         c.rank, c.nranks = int(self.rank), int(self.nranks)
+        c.decomposition = int(self.decomposition)
         c.nccl_unique_id = None
         return c
 

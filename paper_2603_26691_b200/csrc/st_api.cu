@@ -50,6 +50,8 @@ struct st_ctx {
   unsigned long long* d_far_n = nullptr;  // far particles placed by the last count (C-15b)
   int64_t general_rebins = 0;
   bool hist_ready = false;    // the last in-place step produced the next rebin's counts
+  Comm* shard = nullptr;      // ST_DECOMP_SHARDED: communicator of the source all-reduce
+  int shard_rank = 0, shard_nranks = 1;
   int32_t* key[2] = {nullptr, nullptr};
   SortScratch sc;
   uint64_t next_id = 0;
@@ -206,12 +208,35 @@ void st_config_default(st_config* c) {
   c->rank = 0;
   c->nranks = 1;
   c->nccl_unique_id = nullptr;
+  c->decomposition = ST_DECOMP_SLAB;
+}
+
+// The geometry a rank sees: its own slab (ST_DECOMP_SLAB), or the whole domain as if
+// alone (ST_DECOMP_SHARDED: the paper's Fig. 1c scheme, particles stay where injected).
+static st_config geometry_view(const st_config* c) {
+  st_config v = *c;
+  if (c->decomposition == ST_DECOMP_SHARDED) {
+    v.rank = 0;
+    v.nranks = 1;
+    v.decomposition = ST_DECOMP_SLAB;   // one rank's slab = the whole domain
+  }
+  return v;
 }
 
 const char* st_last_error(const st_ctx* c) { return c ? c->err.c_str() : g_init_error.c_str(); }
 
 static st_status validate(const st_config* c, std::string& why) {
   if (c->abi_version != ST_ABI_VERSION) { why = "abi_version mismatch"; return ST_ERR_INVALID_ARG; }
+  if (c->decomposition != ST_DECOMP_SLAB && c->decomposition != ST_DECOMP_SHARDED) {
+    why = "decomposition must be ST_DECOMP_SLAB or ST_DECOMP_SHARDED";
+    return ST_ERR_INVALID_ARG;
+  }
+  if (c->decomposition == ST_DECOMP_SHARDED) {
+    if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) { why = "bad rank/nranks"; return ST_ERR_INVALID_ARG; }
+    if (c->nranks > 1 && !c->nccl_unique_id) { why = "nccl_unique_id required when nranks > 1"; return ST_ERR_INVALID_ARG; }
+    const st_config v = geometry_view(c);
+    return validate(&v, why);
+  }
   for (int a = 0; a < 3; ++a) {
     if (c->dims[a] < 1) { why = "dims must be >= 1"; return ST_ERR_INVALID_ARG; }
     if (!(c->cell_size[a] > 0.0)) { why = "cell_size must be > 0"; return ST_ERR_INVALID_ARG; }
@@ -473,6 +498,12 @@ static st_status init_impl(st_ctx* c) {
     c->comm = comm_create(c->cfg.nccl_unique_id, c->cfg.rank, c->cfg.nranks, c->cs, why);
     if (!c->comm) return fail(c, ST_ERR_NCCL, why);
   }
+  if (c->shard_nranks > 1) {   // particle-sharded: one communicator for the source sum
+    std::string why;
+    c->next_id = (uint64_t)c->shard_rank << 40;
+    c->shard = comm_create(c->cfg.nccl_unique_id, c->shard_rank, c->shard_nranks, c->cs, why);
+    if (!c->shard) return fail(c, ST_ERR_NCCL, why);
+  }
   ST_CUDA(c, cudaStreamSynchronize(c->cs));
   return ST_OK;
 }
@@ -482,6 +513,7 @@ st_status st_destroy(st_ctx* c) {
   if (c->cs) cudaStreamSynchronize(c->cs);
   if (c->xs) cudaStreamSynchronize(c->xs);
   if (c->comm) comm_destroy(c->comm);
+  if (c->shard) comm_destroy(c->shard);
   for (int i = 0; i < 2; ++i) {
     cudaFree(c->S[i].base);
     cudaFree(c->key[i]);
@@ -550,7 +582,11 @@ st_status st_init(const st_config* cfg, st_ctx** out) {
     return s;
   }
   st_ctx* c = new st_ctx();
-  c->cfg = *cfg;
+  c->cfg = geometry_view(cfg);
+  if (cfg->decomposition == ST_DECOMP_SHARDED) {
+    c->shard_rank = cfg->rank;
+    c->shard_nranks = cfg->nranks;
+  }
   s = init_impl(c);
   if (s) {
     g_init_error = c->err;
@@ -1016,6 +1052,12 @@ st_status st_request_sources(st_ctx* c) {
     std::string why;
     if (comm_source_halo(c->comm, c->acc[old], g, c->z0, c->z1, c->H, c->xs, why)) return fail(c, ST_ERR_NCCL, why);
   }
+  if (c->shard) {   // particle-sharded: every rank deposited into the whole domain
+    std::string why;
+    if (comm_allreduce_sum(c->shard, reinterpret_cast<float*>(c->acc[old]), (size_t)g.anz * g.n[1] * g.n[0] * 4, c->xs,
+                           why))
+      return fail(c, ST_ERR_NCCL, why);
+  }
   const double V = c->cfg.cell_size[0] * c->cfg.cell_size[1] * c->cfg.cell_size[2];
   const float scale = c->readout_T > 0.0 ? (float)(1.0 / (V * c->readout_T)) : 0.0f;
   st_status s = check_launch(c, launch_source_readout(g, c->acc[old], c->z0, c->z1, scale, c->S_dev, c->xs));
@@ -1155,7 +1197,7 @@ st_status st_plan_layout(const st_config* cfg, st_layout* o) {
     return s;
   }
   st_ctx tmp;
-  tmp.cfg = *cfg;
+  tmp.cfg = geometry_view(cfg);
   build_geometry(&tmp);
   o->z0 = tmp.z0;
   o->z1 = tmp.z1;

@@ -181,6 +181,12 @@ int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H,
   return join_out(c, s, why);
 }
 
+int comm_allreduce_sum(Comm* c, float* buf, size_t n, cudaStream_t s, std::string& why) {
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclAllReduce(buf, buf, n, ncclFloat, ncclSum, c->nc, c->ns), why);
+  return join_out(c, s, why);
+}
+
 int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int64_t cap, int64_t n, int32_t chunk_lo,
                  int32_t n_local_chunks, int key_bits, SortScratch& sc, int64_t* row, int64_t* n_new, int* launches,
                  cudaStream_t s, std::string& why) {

@@ -27,6 +27,10 @@ int comm_field_halo(Comm* c, float* stage, int64_t comp_stride, int64_t plane, i
 // whole window afterwards is the caller's job.
 int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H, cudaStream_t s, std::string& why);
 
+// Particle-sharded decomposition (ST_DECOMP_SHARDED): sum the whole-domain source
+// accumulator over all ranks in place (one all-reduce).  Returns 0 on success.
+int comm_allreduce_sum(Comm* c, float* buf, size_t n, cudaStream_t s, std::string& why);
+
 // Migration after the local stable sort (store S[*cur] sorted by key[*cur]):
 // send each owner segment to its rank, build kept ++ arrivals (ascending source
 // rank) in the other buffer, and stable-sort it by chunk (C-16).  row[dst] gets

@@ -36,3 +36,21 @@ def test_multigpu_matches_emulation(K, bcz):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "MR_REPORT" in out
+
+
+@pytest.mark.parametrize("K", [1, 2])
+def test_sharded_decomposition_matches_one_oracle(K):
+    """ST_DECOMP_SHARDED: whole domain per rank, particles stay where
+    injected, sources all-reduced — equal to one oracle run holding all particles."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    env = dict(os.environ, MR_K=str(K), MR_STEPS="6")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + K),
+           os.path.join(ROOT, "tests", "mr_shard_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "MR_REPORT" in out
