@@ -164,11 +164,22 @@ def cpu_baseline(wl, target_s, K):
                       f"fp32 oracle, single-threaded, {t:.1f} s"}
 
 
+def bench_config(wl, n_per, K, G, decomp):
+    """The `config` of the JSON line, identical for both arms."""
+    return {"workload": f"{wl.name}: {n_per:.3g} particles/GPU, grid {list(wl.dims)}, "
+                        f"{'reflect' if wl.bc[0] else 'periodic'}, random-Fourier field "
+                        f"u_rms={wl.field_args.get('u_rms')}, two-way, S-N drag + gravity, dt={wl.dt}",
+            "particles_per_gpu": n_per, "grid": list(wl.dims), "chunk_cells": wl.chunk_cells,
+            "rebin_interval": K, "substeps_per_step": 1,
+            "l2": "inputs larger than L2 (40 B x N resident particle state)",
+            "parallelism": f"z-slab x{G}" if decomp == "slab" else f"particle-sharded x{G}"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    wl, _ = make_workload(args.workload, args.gpus, args.particles)
+    wl, n_per = make_workload(args.workload, args.gpus, args.particles)
     n = 100_000
     t_w = run_oracle_sample(wl, n, max(args.warmup, 0), K=args.rebin_interval) if args.warmup else 0.0
     t = run_oracle_sample(wl, n, args.steps, K=args.rebin_interval)
@@ -176,10 +187,10 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{wl.name} sample: {n} particles on the {wl.dims} grid (oracle, 1 core)",
-                       "rebin_interval": args.rebin_interval},
+            "config": bench_config(wl, n_per, args.rebin_interval, args.gpus, args.decomp),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{n} particles x {args.steps} steps of {wl.name}, fp32 oracle, 1 thread"},
+                             "sample": f"{n} particles x {args.steps} steps of {wl.name} (full {wl.dims} grid, same "
+                                       f"field recipe), fp32 oracle, 1 thread, per step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -337,13 +348,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{wl.name}: {n_per:.3g} particles/GPU, grid {list(wl.dims)}, "
-                                   f"{'reflect' if wl.bc[0] else 'periodic'}, random-Fourier field "
-                                   f"u_rms={wl.field_args.get('u_rms')}, two-way, S-N drag + gravity, dt={wl.dt}",
-                       "particles_per_gpu": n_per, "grid": list(wl.dims), "chunk_cells": wl.chunk_cells,
-                       "rebin_interval": K, "substeps_per_step": 1,
-                       "l2": "inputs larger than L2 (40 B x N resident particle state)",
-                       "parallelism": f"z-slab x{G}" if args.decomp == "slab" else f"particle-sharded x{G}"},
+            "config": bench_config(wl, n_per, K, G, args.decomp),
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg, "kernel_ms": kms},
