@@ -58,13 +58,19 @@ constexpr uint32_t kTxF = 8 * kBoxF * 4, kTxI = kBoxI * 8;
 #ifndef ST_PWIN_R
 #define ST_PWIN_R 1   // window margin R of the fused scatter (A/B: R = 1 ~2.5 % faster than 0)
 #endif
-__host__ __device__ constexpr int win_x(bool scatter) { return kRowBins + 2 + (scatter ? 2 * ST_PWIN_R : 0); }
-__host__ __device__ constexpr int win_yz(bool scatter) { return 3 + (scatter ? 2 * ST_PWIN_R : 0); }
+#ifndef ST_PWIN_R_IP
+#define ST_PWIN_R_IP 1   // window margin of the in-place step (binned particles are within one cell)
+#endif
+__host__ __device__ constexpr int win_r(bool scatter) { return scatter ? ST_PWIN_R : ST_PWIN_R_IP; }
+__host__ __device__ constexpr int win_x(bool scatter) { return kRowBins + 2 + 2 * win_r(scatter); }
+__host__ __device__ constexpr int win_yz(bool scatter) { return 3 + 2 * win_r(scatter); }
 __host__ __device__ constexpr int win_cells(bool scatter) { return win_x(scatter) * win_yz(scatter) * win_yz(scatter); }
 constexpr int kTable = kRowBins * kSlots;           // destination table entries of an item (i64)
 // per-warp slice: stages | fluid window | [scatter: table i64[216], run i32[216]] | rel[9] | mbarriers
-constexpr int kOffWin = kPStages * kTStageBytes;
-__host__ __device__ constexpr int off_tab(bool scatter) { return kOffWin + win_cells(scatter) * 16; }
+// stage stride: the in-place step stages no ids (the float box only, 1152 B)
+__host__ __device__ constexpr int stage_bytes(bool scatter) { return scatter ? kTStageBytes : 8 * kBoxF * 4; }
+__host__ __device__ constexpr int off_win(bool scatter) { return kPStages * stage_bytes(scatter); }
+__host__ __device__ constexpr int off_tab(bool scatter) { return off_win(scatter) + win_cells(scatter) * 16; }
 __host__ __device__ constexpr int off_rel(bool scatter) { return off_tab(scatter) + (scatter ? kTable * 12 : kTable * 4); }
 __host__ __device__ constexpr int off_bar(bool scatter) { return off_rel(scatter) + 48; }
 __host__ __device__ constexpr int pwarp_smem_bytes(bool scatter) {
@@ -119,15 +125,15 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMIN
   const int wib = threadIdx.x >> 5;
   unsigned char* sbase = psmem_raw + ((kPSmemAlign - (smem_u32(psmem_raw) & (kPSmemAlign - 1))) & (kPSmemAlign - 1));
   unsigned char* ws = sbase + (size_t)wib * pwarp_smem_bytes(SCATTER);
-  TStage* stg = reinterpret_cast<TStage*>(ws);
-  float4* win = reinterpret_cast<float4*>(ws + kOffWin);
+  auto stg = [&](int k) { return reinterpret_cast<TStage*>(ws + k * stage_bytes(SCATTER)); };
+  float4* win = reinterpret_cast<float4*>(ws + off_win(SCATTER));
   long long* dtab = reinterpret_cast<long long*>(ws + off_tab(SCATTER));                 // [8*27]
   int* run = reinterpret_cast<int*>(ws + off_tab(SCATTER) + kTable * 8);                  // [8*27]
   int* cnt_s = reinterpret_cast<int*>(ws + off_tab(SCATTER));      // [8*27] slot counts (in place, counting)
   int* rel = reinterpret_cast<int*>(ws + off_rel(SCATTER));                               // [kRowBins+1]
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(ws + off_bar(SCATTER));  // stages | item
   unsigned long long* ibar = bar + kPStages;
-  constexpr int WX = win_x(SCATTER), WYZ = win_yz(SCATTER), WR = SCATTER ? ST_PWIN_R : 0;
+  constexpr int WX = win_x(SCATTER), WYZ = win_yz(SCATTER), WR = win_r(SCATTER);
   const int n_items = *a.n_items;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t cap = a.cap;
@@ -168,7 +174,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMIN
         if (SCATTER) bulk_g2s(dtab, a.dtab + (int64_t)b0 * kSlots, kTable * 8u, ibar);
       }
       for (int k = 0; k < kPStages && k < nbatch; ++k)
-        tstage_issue(stg + k, bar + k, &a.tm_f, &a.tm_id, (int)(p0 + 32 * k), SCATTER);
+        tstage_issue(stg(k), bar + k, &a.tm_f, &a.tm_id, (int)(p0 + 32 * k), SCATTER);
     }
     __syncwarp();
     if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMIN
       mbar_wait(bar + sk, (phase >> sk) & 1u);
       __syncwarp();
       phase ^= 1u << sk;
-      const TStage& S = stg[sk];
+      const TStage& S = *stg(sk);
       const int so = (int)((p0 + base) & 3) + (r - base);   // slot in the aligned-down box
       float xp0 = S.f[0][so], xp1 = S.f[1][so], xp2 = S.f[2][so];
       float up0 = S.f[3][so], up1 = S.f[4][so], up2 = S.f[5][so];
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMIN
       __syncwarp();
       if (lane == 0 && bi + kPStages < nbatch) {
         fence_proxy_async();
-        tstage_issue(stg + sk, bar + sk, &a.tm_f, &a.tm_id, (int)(p0 + 32 * (bi + kPStages)), SCATTER);
+        tstage_issue(stg(sk), bar + sk, &a.tm_f, &a.tm_id, (int)(p0 + 32 * (bi + kPStages)), SCATTER);
       }
       __syncwarp();
       float t0 = cell_coord(xp0, g.lo[0], g.ih[0]), t1 = cell_coord(xp1, g.lo[1], g.ih[1]),
