@@ -35,6 +35,15 @@ __device__ __forceinline__ float4 lds4(uint32_t a) {
   return v;
 }
 
+// trilinear stencil base and weight from the cell coordinate t = (x - lo)/h:
+// i0 = floor(t - 1/2), f = t - 1/2 - i0 — exact in fp32 (t < 2^22), identical to
+// deriving them from the cell (C-6) including the f = 1/2 tie and the clamped top cell
+__device__ __forceinline__ void stencil_lo(float t, int& i0, float& f) {
+  const float sh = t - 0.5f;
+  i0 = __float2int_rd(sh);
+  f = sh - (float)i0;
+}
+
 constexpr int kRowBins = 8;
 constexpr int kPStages = 3;
 // A tensor-copy box must start 16-byte aligned along the inner dimension (a
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMIN
           if (two_way) {
             float ra = da0, rb = da1, rc = da2;
             group_sum3(in, ra, rb, rc);
-            if (lane == ld) red_add_v4(a.acc + ((int64_t)az_row * g.n[1] + ry) * g.n[0] + rx + kb, ra, rb, rc);
+            if (lane == ld) red_add_v4(a.acc + (uint32_t)((az_row * g.n[1] + ry) * g.n[0] + rx + kb), ra, rb, rc);
           }
           if (counting) {
             const int hc = (int)__reduce_add_sync(kFull, in ? (unsigned)hcnt : 0u);
@@ -255,9 +264,9 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMIN
       float fx, fy, fz;
       auto gather = [&](float s0, float s1, float s2, int k0, int k1, int k2) {
         int ix, iy, iz;
-        stencil_from_cell(s0, k0, ix, fx);
-        stencil_from_cell(s1, k1, iy, fy);
-        stencil_from_cell(s2, k2, iz, fz);
+        stencil_lo(s0, ix, fx);
+        stencil_lo(s1, iy, fy);
+        stencil_lo(s2, iz, fz);
         int wz = window_z(g, iz);
         if (wz < 0 || wz + 1 >= g.wnz) {
           if (valid) flags |= ERRF_WINDOW;
@@ -414,14 +423,20 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMIN
               da1 += jb;
               da2 += jc;
             } else if (valid && az >= 0) {
-              red_add_v4(a.acc + ((int64_t)az * g.n[1] + c1) * g.n[0] + c0, ja, jb, jc);
+              red_add_v4(a.acc + (uint32_t)((az * g.n[1] + c1) * g.n[0] + c0), ja, jb, jc);
             }
           }
-          bool bad = false;
-          bad |= apply_bc(periodic<BCM>(g, 0) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[0], g.hi[0], g.L[0], xp0, up0);
-          bad |= apply_bc(periodic<BCM>(g, 1) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[1], g.hi[1], g.L[1], xp1, up1);
-          bad |= apply_bc(periodic<BCM>(g, 2) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[2], g.hi[2], g.L[2], xp2, up2);
-          if (bad && valid) flags |= ERRF_CFL;
+          // walls / wrap (C-11, C-12): one warp vote skips the three axes when no lane
+          // left the box (the common case)
+          const bool out = (xp0 < g.lo[0]) | (xp0 >= g.hi[0]) | (xp1 < g.lo[1]) | (xp1 >= g.hi[1]) |
+                           (xp2 < g.lo[2]) | (xp2 >= g.hi[2]);
+          if (__any_sync(kFull, out)) {
+            bool bad = false;
+            bad |= apply_bc(periodic<BCM>(g, 0) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[0], g.hi[0], g.L[0], xp0, up0);
+            bad |= apply_bc(periodic<BCM>(g, 1) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[1], g.hi[1], g.L[1], xp1, up1);
+            bad |= apply_bc(periodic<BCM>(g, 2) ? ST_BC_PERIODIC : ST_BC_REFLECT, g.lo[2], g.hi[2], g.L[2], xp2, up2);
+            if (bad && valid) flags |= ERRF_CFL;
+          }
         }
       }
       if (counting && valid) {
