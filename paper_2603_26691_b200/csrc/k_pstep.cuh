@@ -124,8 +124,13 @@ __device__ __forceinline__ void tstage_issue(TStage* st, unsigned long long* bar
 constexpr int kSpecVP = 1;    // neighbour-rank planes (send buffers) may be destinations
 constexpr int kSpecSub = 2;   // more than one sub-step per call
 constexpr int kSpecAll = 3;
+#ifndef ST_PWARPS
+#define ST_PWARPS 8     // warps per CTA of the fused scatter
+#endif
+__host__ __device__ constexpr int pwarps(bool scatter_advance) { return scatter_advance ? ST_PWARPS : 8; }
 template <bool SCATTER, bool ADVANCE, int BCM, int SPEC = kSpecAll, int FEAT = 0xff>
-__global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? ST_PMINB : ST_PMINB_IP) k_pstep(const __grid_constant__ StepArgs a) {
+__global__ void __launch_bounds__(32 * pwarps(SCATTER && ADVANCE), (SCATTER && ADVANCE) ? ST_PMINB : ST_PMINB_IP)
+    k_pstep(const __grid_constant__ StepArgs a) {
   constexpr int SH = 3;   // chunk_cells == 8
   constexpr bool VP = (SPEC & kSpecVP) != 0;
   extern __shared__ __align__(128) unsigned char psmem_raw[];

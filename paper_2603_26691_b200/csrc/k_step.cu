@@ -782,16 +782,17 @@ int launch_variant(const StepArgs& a, cudaStream_t s) {
 template <bool S, bool A, int BCM, int SPEC = kSpecAll, int FEAT = 0xff>
 int launch_pvariant(const StepArgs& a, cudaStream_t s) {
   static int grid = 0;
-  const int smem = 8 * pwarp_smem_bytes(S) + kPSmemAlign;
+  constexpr int W = pwarps(S && A);
+  const int smem = W * pwarp_smem_bytes(S) + kPSmemAlign;
   if (!grid) {
     int nsm = 148, dev = 0, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_pstep<S, A, BCM, SPEC, FEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pstep<S, A, BCM, SPEC, FEAT>, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pstep<S, A, BCM, SPEC, FEAT>, 32 * W, smem);
     grid = nsm * (per > 0 ? per : 1);
   }
-  k_pstep<S, A, BCM, SPEC, FEAT><<<grid, 256, smem, s>>>(a);
+  k_pstep<S, A, BCM, SPEC, FEAT><<<grid, 32 * W, smem, s>>>(a);
   return 1;
 }
 
