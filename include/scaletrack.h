@@ -89,6 +89,12 @@ enum { ST_ONE_WAY = 0, ST_TWO_WAY = 1 };                        /* P:69 */
  *                             fluid field, particles stay on the rank that injected them (no
  *                             migration), st_get_sources returns the sources of the whole
  *                             domain summed over all ranks (one NCCL all-reduce, collective).
+ *   slab_planes             : ST_DECOMP_SLAB only: NULL = equal split of the chunk planes;
+ *                             else nranks+1 ascending chunk-plane boundaries (slab of rank r =
+ *                             planes [slab_planes[r], slab_planes[r+1]), [0] = 0, [nranks] =
+ *                             ceil(dims[2]/chunk_cells)), e.g. from st_plan_partition: the
+ *                             count-balanced owner ranges of SURVEY §8(f4)
+ *                             along z.  Read during st_init only.
  */
 typedef struct {
   int32_t abi_version;
@@ -107,6 +113,7 @@ typedef struct {
   int32_t rank, nranks;
   const void* nccl_unique_id;
   int32_t decomposition;
+  const int32_t* slab_planes;
 } st_config;
 
 enum { ST_DECOMP_SLAB = 0, ST_DECOMP_SHARDED = 1 };
@@ -227,6 +234,14 @@ st_status st_last_timings(st_ctx* ctx, float* advance_ms, float* rebin_ms);
 
 /* Message of the last error on ctx ("" if none).  NULL ctx: last init error. */
 const char* st_last_error(const st_ctx* ctx);
+
+/* Count-balanced slab boundaries (the paper balances owner ranges by
+ * particle count): given plane_counts[k] = particles in chunk plane k
+ * (k < ceil(dims[2]/chunk_cells)), write the cfg->nranks+1 boundaries minimising the
+ * largest slab count, every slab holding >= chunk_cells+1 cell planes (the halo the
+ * neighbour needs); ties -> the lexicographically smallest boundaries.  Host-only.
+ * ST_ERR_INVALID_ARG if cfg is invalid or no feasible split exists. */
+st_status st_plan_partition(const st_config* cfg, const int64_t* plane_counts, int32_t* slab_planes);
 
 /* ABI version the library was built with (== ST_ABI_VERSION). */
 int32_t st_abi_version(void);

@@ -213,6 +213,7 @@ class Sim:
     rebin_interval: int = 1
     precision: str = "f32"
     nranks: int = 1
+    plane_split: tuple | None = None   # C-16b: nranks+1 chunk-plane boundaries (None: equal split)
 
     def __post_init__(self):
         if self.precision not in ("f32", "f64"):
@@ -233,6 +234,8 @@ class Sim:
 
     # ---- geometry (C-6, C-14, C-16) ----
     def plane_range(self, r: int) -> tuple:
+        if self.plane_split is not None:
+            return int(self.plane_split[r]), int(self.plane_split[r + 1])
         ncz = self.mesh.nchunk[2]
         return (r * ncz) // self.nranks, ((r + 1) * ncz) // self.nranks
 

@@ -50,6 +50,7 @@ class StConfig(ctypes.Structure):
         ("nranks", ctypes.c_int32),
         ("nccl_unique_id", ctypes.c_void_p),
         ("decomposition", ctypes.c_int32),
+        ("slab_planes", ctypes.POINTER(ctypes.c_int32)),
     ]
 
 
@@ -106,6 +107,7 @@ SIGNATURES = {
     "st_get_migration_counts": (_i32, [_vp, _vp]),
     "st_get_layout": (_i32, [_vp, ctypes.POINTER(StLayout)]),
     "st_plan_layout": (_i32, [ctypes.POINTER(StConfig), ctypes.POINTER(StLayout)]),
+    "st_plan_partition": (_i32, [ctypes.POINTER(StConfig), _vp, _vp]),
     "st_get_stats": (_i32, [_vp, ctypes.POINTER(StStats)]),
     "st_sync": (_i32, [_vp]),
     "st_last_timings": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),

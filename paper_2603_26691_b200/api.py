@@ -60,6 +60,7 @@ class Config:
     rank: int = 0
     nranks: int = 1
     decomposition: int = 0       # N.DECOMP_SLAB | N.DECOMP_SHARDED
+    slab_planes: tuple | None = None   # nranks+1 chunk-plane boundaries (plan_partition), None = equal
 
     def to_c(self, stream=None, unique_id: bytes | None = None) -> N.StConfig:
         c = N.StConfig()
@@ -80,6 +81,10 @@ class Config:
         c.rank, c.nranks = int(self.rank), int(self.nranks)
         c.decomposition = int(self.decomposition)
         c.nccl_unique_id = None
+        if self.slab_planes is not None:
+            arr = (ctypes.c_int32 * len(self.slab_planes))(*[int(v) for v in self.slab_planes])
+            c._keep_slab_planes = arr   # alive as long as the struct
+            c.slab_planes = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32))
         return c
 
     @property
@@ -98,6 +103,19 @@ def plan_layout(cfg: Config) -> N.StLayout:
     if rc:
         raise N.StError(rc, lib.st_last_error(None).decode())
     return o
+
+
+def plan_partition(cfg: Config, plane_counts) -> tuple:
+    """st_plan_partition: count-balanced slab boundaries (chunk planes) for cfg.nranks
+    ranks from the particle count of every chunk plane.  Host-only."""
+    lib = N.load()
+    c = cfg.to_c()
+    counts = np.ascontiguousarray(plane_counts, dtype=np.int64)
+    out = np.empty(int(cfg.nranks) + 1, np.int32)
+    rc = lib.st_plan_partition(ctypes.byref(c), counts.ctypes.data, out.ctypes.data)
+    if rc:
+        raise N.StError(rc, lib.st_last_error(None).decode())
+    return tuple(int(v) for v in out)
 
 
 def nccl_unique_id() -> bytes:

@@ -209,6 +209,18 @@ void st_config_default(st_config* c) {
   c->nranks = 1;
   c->nccl_unique_id = nullptr;
   c->decomposition = ST_DECOMP_SLAB;
+  c->slab_planes = nullptr;
+}
+
+// chunk planes [k0, k1) of rank r: equal split, or cfg->slab_planes
+static void slab_range(const st_config* c, int ncz, int r, int* k0, int* k1) {
+  if (c->slab_planes) {
+    *k0 = c->slab_planes[r];
+    *k1 = c->slab_planes[r + 1];
+  } else {
+    *k0 = (int)(((int64_t)r * ncz) / c->nranks);
+    *k1 = (int)(((int64_t)(r + 1) * ncz) / c->nranks);
+  }
 }
 
 // The geometry a rank sees: its own slab (ST_DECOMP_SLAB), or the whole domain as if
@@ -258,10 +270,16 @@ static st_status validate(const st_config* c, std::string& why) {
   const int ncz = (c->dims[2] + c->chunk_cells - 1) / c->chunk_cells;
   if (c->nranks > ncz) { why = "need at least one chunk plane per rank"; return ST_ERR_INVALID_ARG; }
   if (c->nranks > 1 && !c->nccl_unique_id) { why = "nccl_unique_id required when nranks > 1"; return ST_ERR_INVALID_ARG; }
+  if (c->slab_planes) {
+    if (c->slab_planes[0] != 0 || c->slab_planes[c->nranks] != ncz) { why = "slab_planes must span [0, ncz]"; return ST_ERR_INVALID_ARG; }
+    for (int r = 0; r < c->nranks; ++r)
+      if (c->slab_planes[r + 1] <= c->slab_planes[r]) { why = "slab_planes must be strictly ascending"; return ST_ERR_INVALID_ARG; }
+  }
   if (c->nranks > 1) {
     // every slab must hold the (chunk_cells + 1)-plane field halo its neighbour needs
     for (int r = 0; r < c->nranks; ++r) {
-      const int k0 = (int)(((int64_t)r * ncz) / c->nranks), k1 = (int)(((int64_t)(r + 1) * ncz) / c->nranks);
+      int k0, k1;
+      slab_range(c, ncz, r, &k0, &k1);
       const int zz1 = k1 * c->chunk_cells < c->dims[2] ? k1 * c->chunk_cells : c->dims[2];
       if (zz1 - k0 * c->chunk_cells < c->chunk_cells + 1) { why = "each rank needs >= chunk_cells+1 z planes"; return ST_ERR_INVALID_ARG; }
     }
@@ -284,8 +302,7 @@ static void build_geometry(st_ctx* c) {
   }
   g.cc = f.chunk_cells;
   const int G = f.nranks, r = f.rank;
-  c->kz0 = (int)(((int64_t)r * g.NC[2]) / G);
-  c->kz1 = (int)(((int64_t)(r + 1) * g.NC[2]) / G);
+  slab_range(&f, g.NC[2], r, &c->kz0, &c->kz1);
   c->z0 = c->kz0 * g.cc;
   c->z1 = c->kz1 * g.cc < g.n[2] ? c->kz1 * g.cc : g.n[2];
   c->H = G > 1 ? g.cc : 0;
@@ -1185,6 +1202,52 @@ st_status st_get_layout(st_ctx* c, st_layout* o) {
   for (int a = 0; a < 3; ++a) o->nchunk[a] = c->g.NC[a];
   o->local_cells = c->local_cells;
   o->halo_cells = c->H;
+  return ST_OK;
+}
+
+st_status st_plan_partition(const st_config* cfg, const int64_t* counts, int32_t* out) {
+  if (!cfg || !counts || !out) return ST_ERR_INVALID_ARG;
+  st_config v = *cfg;
+  v.slab_planes = nullptr;
+  v.nccl_unique_id = (const void*)1;   // planning only
+  std::string why;
+  st_status s = validate(&v, why);
+  if (s) {
+    g_init_error = why;
+    return s;
+  }
+  const int G = v.nranks, cc = v.chunk_cells, nz = v.dims[2];
+  const int ncz = (nz + cc - 1) / cc;
+  auto ok_slab = [&](int k0, int k1) {   // >= cc+1 cell planes (ragged top plane counted exactly)
+    const int z1 = k1 * cc < nz ? k1 * cc : nz;
+    return G == 1 || z1 - k0 * cc >= cc + 1;
+  };
+  std::vector<int64_t> pre(ncz + 1, 0);
+  for (int k = 0; k < ncz; ++k) pre[k + 1] = pre[k] + (counts[k] > 0 ? counts[k] : 0);
+  const int64_t INF = INT64_MAX;
+  // best[g][k]: minimal largest slab count splitting planes [0, k) into g slabs
+  std::vector<std::vector<int64_t>> best(G + 1, std::vector<int64_t>(ncz + 1, INF));
+  std::vector<std::vector<int>> cut(G + 1, std::vector<int>(ncz + 1, -1));
+  best[0][0] = 0;
+  for (int gi = 1; gi <= G; ++gi)
+    for (int k = 1; k <= ncz; ++k)
+      for (int j = 0; j < k; ++j) {   // last slab [j, k); smallest j wins ties
+        if (best[gi - 1][j] == INF || !ok_slab(j, k)) continue;
+        const int64_t m = std::max(best[gi - 1][j], pre[k] - pre[j]);
+        if (m < best[gi][k]) {
+          best[gi][k] = m;
+          cut[gi][k] = j;
+        }
+      }
+  if (best[G][ncz] == INF) {
+    g_init_error = "no split with >= chunk_cells+1 planes per rank";
+    return ST_ERR_INVALID_ARG;
+  }
+  out[G] = ncz;
+  for (int gi = G, k = ncz; gi > 0; --gi) {
+    k = cut[gi][k];
+    out[gi - 1] = k;
+  }
   return ST_OK;
 }
 
