@@ -51,6 +51,7 @@ struct st_ctx {
   int64_t general_rebins = 0;
   bool hist_ready = false;    // the last in-place step produced the next rebin's counts
   Comm* shard = nullptr;      // ST_DECOMP_SHARDED: communicator of the source all-reduce
+  std::vector<int32_t> slab_copy;   // cfg.slab_planes, owned (the caller's array is read at init only)
   int shard_rank = 0, shard_nranks = 1;
   int32_t* key[2] = {nullptr, nullptr};
   SortScratch sc;
@@ -512,13 +513,13 @@ static st_status init_impl(st_ctx* c) {
   c->next_id = (uint64_t)c->cfg.rank << 40;
   if (c->cfg.nranks > 1) {
     std::string why;
-    c->comm = comm_create(c->cfg.nccl_unique_id, c->cfg.rank, c->cfg.nranks, c->cs, why);
+    c->comm = comm_create(c->cfg.nccl_unique_id, c->cfg.rank, c->cfg.nranks, c->cfg.slab_planes, c->cs, why);
     if (!c->comm) return fail(c, ST_ERR_NCCL, why);
   }
   if (c->shard_nranks > 1) {   // particle-sharded: one communicator for the source sum
     std::string why;
     c->next_id = (uint64_t)c->shard_rank << 40;
-    c->shard = comm_create(c->cfg.nccl_unique_id, c->shard_rank, c->shard_nranks, c->cs, why);
+    c->shard = comm_create(c->cfg.nccl_unique_id, c->shard_rank, c->shard_nranks, nullptr, c->cs, why);
     if (!c->shard) return fail(c, ST_ERR_NCCL, why);
   }
   ST_CUDA(c, cudaStreamSynchronize(c->cs));
@@ -600,6 +601,10 @@ st_status st_init(const st_config* cfg, st_ctx** out) {
   }
   st_ctx* c = new st_ctx();
   c->cfg = geometry_view(cfg);
+  if (c->cfg.slab_planes) {
+    c->slab_copy.assign(c->cfg.slab_planes, c->cfg.slab_planes + c->cfg.nranks + 1);
+    c->cfg.slab_planes = c->slab_copy.data();
+  }
   if (cfg->decomposition == ST_DECOMP_SHARDED) {
     c->shard_rank = cfg->rank;
     c->shard_nranks = cfg->nranks;

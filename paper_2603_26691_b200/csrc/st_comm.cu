@@ -16,6 +16,7 @@ namespace st {
 struct Comm {
   ncclComm_t nc = nullptr;
   int rank = 0, nranks = 1;
+  std::vector<int32_t> planes;  // slab boundaries (chunk planes, nranks+1), empty = equal split
   cudaStream_t ns = nullptr;
   cudaEvent_t e_in = nullptr, e_out = nullptr;
   float4* halo_recv = nullptr;  // 2 * H * plane float4 (source halo receive)
@@ -53,7 +54,11 @@ __global__ void k_halo_add(float4* __restrict__ acc, const float4* __restrict__ 
   }
 }
 
-inline int plane_owner_lo(int r, int ncz, int G) { return (int)(((int64_t)r * ncz) / G); }
+// first chunk plane of rank r: the configured slab boundaries, else the equal split
+inline int plane_owner_lo(const Comm* c, int r, int ncz) {
+  if (!c->planes.empty()) return c->planes[r];
+  return (int)(((int64_t)r * ncz) / c->nranks);
+}
 
 #define NCCK(call, why)                                                    \
   do {                                                                     \
@@ -85,11 +90,13 @@ int join_out(Comm* c, cudaStream_t s, std::string& why) {
 
 }  // namespace
 
-Comm* comm_create(const void* unique_id, int rank, int nranks, cudaStream_t s, std::string& why) {
+Comm* comm_create(const void* unique_id, int rank, int nranks, const int32_t* slab_planes, cudaStream_t s,
+                  std::string& why) {
   (void)s;
   Comm* c = new Comm();
   c->rank = rank;
   c->nranks = nranks;
+  if (slab_planes) c->planes.assign(slab_planes, slab_planes + nranks + 1);
   ncclUniqueId id;
   memcpy(&id, unique_id, sizeof(id));
   ncclResult_t r = ncclCommInitRank(&c->nc, nranks, id, rank);
@@ -195,7 +202,7 @@ int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int6
   const int G = c->nranks, r = c->rank;
   const int ncxy = g.NC[0] * g.NC[1];
   std::vector<int32_t> bases(G + 1);
-  for (int q = 0; q <= G; ++q) bases[q] = plane_owner_lo(q, g.NC[2], G) * ncxy;
+  for (int q = 0; q <= G; ++q) bases[q] = plane_owner_lo(c, q, g.NC[2]) * ncxy;
   CUCK(cudaMemcpyAsync(c->d_bases, bases.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, s), why);
   k_rank_bounds<<<1, 64, 0, s>>>(key[*cur], n, c->d_bases, G + 1, c->d_bounds);
   *launches += 1;

@@ -14,7 +14,10 @@ namespace st {
 
 struct Comm;
 
-Comm* comm_create(const void* unique_id, int rank, int nranks, cudaStream_t s, std::string& why);
+// slab_planes: the nranks+1 chunk-plane boundaries of the slab decomposition (copied),
+// NULL = equal split
+Comm* comm_create(const void* unique_id, int rank, int nranks, const int32_t* slab_planes, cudaStream_t s,
+                  std::string& why);
 void comm_destroy(Comm* c);
 
 // Fill the halo planes of the field staging buffer [3][ext_nz][ny][nx] (owned

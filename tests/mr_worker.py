@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 def main():
     import oracle
     import synth
-    from paper_2603_26691_b200 import Config, ScaleTrack, nccl_unique_id
+    from paper_2603_26691_b200 import Config, ScaleTrack, nccl_unique_id, plan_partition
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -38,11 +38,17 @@ def main():
     wl = synth.workload("C4", n_particles=0)
     cfg = Config(dims=dims, cell_size=(h, h, h), chunk_cells=8, bc=(1, 1, bcz), gravity=(0, 0, -9.81),
                  rebin_interval=K, capacity=200_000, device=local, rank=rank, nranks=world)
+    split = None
+    if os.environ.get("MR_SPLIT") == "weighted":   # count-balanced slabs for a bottom-heavy load (f4)
+        split = plan_partition(cfg, np.exp(-np.arange(dims[2] // 8) / 2.0) * 1e5)
+        cfg.slab_planes = split
     st = ScaleTrack(cfg, unique_id=uid[0])
     lay = st.layout
     # inputs: every rank injects particles drawn over its own slab, seed per rank
     L = [d * h for d in dims]
     slabs = [(r * (dims[2] // 8) // world * 8, (r + 1) * (dims[2] // 8) // world * 8) for r in range(world)]
+    if split is not None:
+        slabs = [(split[r] * 8, split[r + 1] * 8) for r in range(world)]
     parts = [synth.particles_np(20_000 + 1000 * r, (0, 0, slabs[r][0] * h), (L[0], L[1], slabs[r][1] * h),
                                 (5e-6, 40e-6), seed=100 + r) for r in range(world)]
     assert (lay.z0, lay.z1) == slabs[rank]
@@ -66,7 +72,8 @@ def main():
     report = {}
     if rank == 0:
         mesh = oracle.Mesh(dims=dims, cell_size=(h, h, h), chunk_cells=8, bc=(1, 1, bcz))
-        emu = oracle.Sim(mesh, oracle.Physics(gravity=(0, 0, -9.81)), rebin_interval=K, precision="f32", nranks=world)
+        emu = oracle.Sim(mesh, oracle.Physics(gravity=(0, 0, -9.81)), rebin_interval=K, precision="f32", nranks=world,
+                         plane_split=split)
         for r in range(world):
             xr, ur, dr, wr = parts[r]
             emu.inject(xr, ur, dr, wr, rank=r)

@@ -54,3 +54,19 @@ def test_sharded_decomposition_matches_one_oracle(K):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "MR_REPORT" in out
+
+
+def test_multigpu_weighted_slabs_match_emulation():
+    """Count-balanced slab boundaries (st_plan_partition, f4): unequal slabs through the
+    fused rebin, migration and halos match the oracle's emulation with the same split."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    env = dict(os.environ, MR_K="2", MR_BCZ="1", MR_STEPS="6", MR_SPLIT="weighted")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", "29750", os.path.join(ROOT, "tests", "mr_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "MR_REPORT" in out
