@@ -37,6 +37,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C5", choices=["C3", "C4", "C5"])
+    ap.add_argument("--cluster", type=float, default=0.0,
+                    help="clustered load: particle density ~ exp(-z / (c Lz)) over the whole job (0 = uniform)")
+    ap.add_argument("--partition", default="equal", choices=["equal", "weighted"],
+                    help="slab boundaries: equal chunk planes, or count-balanced (st_plan_partition, SURVEY f4)")
     ap.add_argument("--decomp", default="slab", choices=["slab", "sharded"],
                     help="slab: z-slabs with migration (north star); sharded: every GPU holds the whole "
                          "domain, particles stay, sources all-reduced (PAPER Fig. 1c, SURVEY f2)")
@@ -228,16 +232,44 @@ def run_ours(args):
                  rho_f=synth.RHO_F, nu_f=synth.NU_F, rho_p=synth.RHO_P, gravity=wl.gravity, drag_law=wl.drag_law,
                  coupling=wl.coupling, rebin_interval=K, capacity=cap, device=local, rank=rank, nranks=G,
                  decomposition=1 if args.decomp == "sharded" else 0)
+    n_mine = n_per
+    if args.cluster > 0:
+        # clustered job: G * n_per particles with density ~ exp(-z / (c Lz)); rank r holds
+        # those of its slab (equal planes, or count-balanced boundaries from the planes' counts)
+        from paper_2603_26691_b200 import plan_partition
+        Lz = wl.dims[2] * wl.cell_size[2]
+        lam = args.cluster * Lz
+        cc_h = wl.chunk_cells * wl.cell_size[2]
+        ncz = (wl.dims[2] + wl.chunk_cells - 1) // wl.chunk_cells
+        edges = [min(k * cc_h, Lz) for k in range(ncz + 1)]
+        mass = [math.exp(-a / lam) - math.exp(-b / lam) for a, b in zip(edges[:-1], edges[1:])]
+        tot_m = sum(mass)
+        counts = [G * n_per * m / tot_m for m in mass]
+        if args.partition == "weighted" and G > 1:
+            cfg.slab_planes = plan_partition(cfg, counts)
+        lay0 = __import__("paper_2603_26691_b200").plan_layout(cfg)
+        n_mine = int(round(sum(counts[lay0.kz0:lay0.kz1])))
+        cfg.capacity = cap = int(n_mine * 1.1) + 1_000_000
     st = ScaleTrack(cfg, stream=stream.cuda_stream, unique_id=uid)
     lay = st.layout
     z_range = (lay.z0, lay.z1)
-    # particles: uniform in this rank's slab, drawn on the device in batches (seed 8 + rank)
+    # particles: uniform in this rank's slab, drawn on the device in batches (seed 8 + rank);
+    # clustered: z redrawn from the exponential restricted to the slab (inverse CDF)
     lo, hi = synth.domain_box(wl, z_range)
     batch = 100_000_000
-    for b0 in range(0, n_per, batch):
-        nb = min(batch, n_per - b0)
+    for b0 in range(0, n_mine, batch):
+        nb = min(batch, n_mine - b0)
         x, u, d, w = synth.particles_torch(nb, lo, hi, wl.d_range, wl.d_dist, wl.w,
                                            seed=wl.seed_particles * 1000 + rank * 100 + b0 // batch, device=dev)
+        if args.cluster > 0:
+            qz = torch.rand(nb, device=dev, dtype=torch.float64,
+                            generator=torch.Generator(device=dev).manual_seed(77 + rank * 1000 + b0 // batch))
+            ea, eb = math.exp(-lo[2] / lam), math.exp(-hi[2] / lam)
+            z = -lam * torch.log(ea - qz * (ea - eb))
+            z32 = z.to(torch.float32)   # clamp in fp32: the cast must not round onto the slab's top face
+            lo32 = torch.tensor(lo[2], dtype=torch.float32, device=dev)
+            hi32 = torch.tensor(hi[2], dtype=torch.float32, device=dev)
+            x[2] = torch.minimum(torch.maximum(z32, lo32), torch.nextafter(hi32, lo32))
         st.inject(x, u, d, w)
         del x, u, d, w
     torch.cuda.synchronize()
@@ -359,7 +391,10 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": bench_config(wl, n_per, K, G, args.decomp),
+            "config": dict(bench_config(wl, n_per, K, G, args.decomp),
+                           **({"cluster": args.cluster, "partition": args.partition,
+                               "slab_planes": list(cfg.slab_planes) if cfg.slab_planes else None}
+                              if args.cluster > 0 else {})),
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg, "kernel_ms": kms},
