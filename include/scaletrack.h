@@ -169,7 +169,9 @@ st_status st_set_fluid_field(st_ctx* ctx, const float* u);
  * Positions must satisfy lo <= x <= hi per axis, else ST_ERR_OUT_OF_DOMAIN and
  * nothing is appended.  With nranks > 1 the call is collective (every rank calls
  * it, n may be 0) and a rank injects only particles whose cell lies in its own
- * z-slab (st_get_layout z0..z1), else ST_ERR_OUT_OF_DOMAIN.  st_get_particles
+ * z-slab (st_get_layout z0..z1), else ST_ERR_OUT_OF_DOMAIN; the outcome is agreed
+ * over ranks: if any rank fails, nothing is appended on any rank and the others
+ * return ST_ERR_STATE (no rank is left alone in the next exchange).  st_get_particles
  * and st_get_count are collective too when nranks > 1 (they may execute a due
  * rebin, which exchanges movers). */
 st_status st_inject(st_ctx* ctx, int64_t n, const float* x, const float* u,

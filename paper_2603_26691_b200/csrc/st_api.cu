@@ -663,7 +663,7 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
 }
 
 // ---------------------------------------------------------------- inject
-st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const float* d, const float* w,
+static st_status inject_local(st_ctx* c, int64_t n, const float* x, const float* u, const float* d, const float* w,
                     const uint64_t* id) {
   ST_ALIVE(c);
   if (n < 0) return fail(c, ST_ERR_INVALID_ARG, "n < 0");
@@ -706,6 +706,31 @@ st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const 
   c->n += n;
   c->binned = false;
   c->hist_ready = false;
+  return ST_OK;
+}
+
+st_status st_inject(st_ctx* c, int64_t n, const float* x, const float* u, const float* d, const float* w,
+                    const uint64_t* id) {
+  ST_ALIVE(c);
+  const int64_t n0 = c->n;
+  const uint64_t id0 = c->next_id;
+  st_status st = inject_local(c, n, x, u, d, w, id);
+  if (!c->comm) return st;
+  // collective: every rank learns whether any rank failed (else the others would run
+  // into the next NCCL exchange alone and hang); ranks that appended roll back
+  int flag = st != ST_OK ? 1 : 0;
+  std::string why;
+  ST_CUDA(c, cudaMemcpyAsync(c->d_farg, &flag, sizeof(int), cudaMemcpyHostToDevice, c->cs));
+  if (comm_allreduce_max_i32(c->comm, c->d_farg, 1, c->cs, why)) return fail(c, ST_ERR_NCCL, why);
+  ST_CUDA(c, cudaMemcpyAsync(&flag, c->d_farg, sizeof(int), cudaMemcpyDeviceToHost, c->cs));
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  if (flag) {   // every rank: nothing appended, leave the binned state together
+    c->n = n0;
+    c->next_id = id0;
+    c->binned = c->hist_ready = false;
+  }
+  if (st != ST_OK) return st;
+  if (flag) return fail(c, ST_ERR_STATE, "st_inject failed on another rank (nothing appended on any rank)");
   return ST_OK;
 }
 

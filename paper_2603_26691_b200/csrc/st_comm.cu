@@ -188,6 +188,12 @@ int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H,
   return join_out(c, s, why);
 }
 
+int comm_allreduce_max_i32(Comm* c, int* buf, size_t n, cudaStream_t s, std::string& why) {
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclAllReduce(buf, buf, n, ncclInt32, ncclMax, c->nc, c->ns), why);
+  return join_out(c, s, why);
+}
+
 int comm_allreduce_sum(Comm* c, float* buf, size_t n, cudaStream_t s, std::string& why) {
   if (join_in(c, s, why)) return 1;
   NCCK(ncclAllReduce(buf, buf, n, ncclFloat, ncclSum, c->nc, c->ns), why);

@@ -33,6 +33,8 @@ int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H,
 // Particle-sharded decomposition (ST_DECOMP_SHARDED): sum the whole-domain source
 // accumulator over all ranks in place (one all-reduce).  Returns 0 on success.
 int comm_allreduce_sum(Comm* c, float* buf, size_t n, cudaStream_t s, std::string& why);
+// max over ranks of n ints in place (collective agreement on a status)
+int comm_allreduce_max_i32(Comm* c, int* buf, size_t n, cudaStream_t s, std::string& why);
 
 // Migration after the local stable sort (store S[*cur] sorted by key[*cur]):
 // send each owner segment to its rank, build kept ++ arrivals (ascending source

@@ -70,3 +70,16 @@ def test_multigpu_weighted_slabs_match_emulation():
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "MR_REPORT" in out
+
+
+def test_collective_failure_is_collective():
+    """A collective call failing on one rank raises on every rank (no hang)."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29760", os.path.join(ROOT, "tests", "mr_error_worker.py")]
+    r = subprocess.run(cmd, env=dict(os.environ), capture_output=True, text=True, timeout=300)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count("ok=True") == 2, out[-2000:]
