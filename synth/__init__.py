@@ -218,3 +218,27 @@ def domain_box(wl: Workload, z_range=None):
         lo[2] = wl.origin[2] + z_range[0] * wl.cell_size[2]
         hi[2] = wl.origin[2] + z_range[1] * wl.cell_size[2]
     return lo, hi
+
+
+def micro_field(dims, origin, cell_size, seed=0, T0=283.15, dT=1.0, rho_v0=0.0095, rel=0.02,
+                u_rms=0.3, dtype=np.float32):
+    """5-component cell-centred field (u_x, u_y, u_z, T_f, rho_v) for the droplet
+    workload: random-Fourier velocity; temperature
+    T0 + dT sin-mode (K); vapour density rho_v0 (1 + rel cos-mode) (kg/m^3; about 1 %
+    supersaturated at 283 K).  Plain numbers, no microphysics."""
+    U = fourier_field(dims, origin, cell_size, modes=64, kmax=4, u_rms=u_rms, seed=seed).numpy()
+    cx, cy, cz = cell_centres(dims, origin, cell_size)
+    L = [dims[a] * cell_size[a] for a in range(3)]
+    Z, Y, X = np.meshgrid(cz, cy, cx, indexing="ij")
+    px, py, pz = (2 * math.pi * (X - origin[0]) / L[0], 2 * math.pi * (Y - origin[1]) / L[1],
+                  2 * math.pi * (Z - origin[2]) / L[2])
+    T = T0 + dT * np.sin(px) * np.cos(py) * np.cos(pz)
+    rv = rho_v0 * (1.0 + rel * np.cos(px + py) * np.sin(pz))
+    return np.concatenate([U, T[None], rv[None]]).astype(dtype)
+
+
+def droplets_np(n, lo, hi, d_range=(5e-6, 30e-6), T_range=(281.0, 285.0), w=100.0, seed=0, dtype=np.float32):
+    """Droplet cloud: particles_np positions/diameters, u = 0, T ~ U(T_range), weight w."""
+    x, u, d, wv = particles_np(n, lo, hi, d_range, "uniform", w, seed, dtype)
+    T = np.random.default_rng(seed + 7919).uniform(T_range[0], T_range[1], n).astype(dtype)
+    return x, u, d, T, wv
