@@ -16,9 +16,16 @@ ORACLE    := oracle/liboracle_st.so
 
 all: $(LIB) $(ORACLE)
 
-$(LIB): $(CU) $(HDR)
+MICRO_O   := build/st_micro.o
+
+# the droplet step rounds every fp64 operation on its own (no FMA contraction, C-28)
+$(MICRO_O): $(SRC)/st_micro.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -fmad=false -c -o $@ $< 2> build/ptxas_micro.log || (cat build/ptxas_micro.log; exit 1)
+
+$(LIB): $(CU) $(MICRO_O) $(HDR)
 	@mkdir -p $(PKG)/lib build
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU) $(MICRO_O) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
 	  -Xlinker -rpath=$(NCCL_DIR)/lib 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
 
 $(ORACLE): oracle/st_oracle.c oracle/st_oracle_step.inc

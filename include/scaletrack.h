@@ -305,6 +305,57 @@ st_status st_ec_backlog(st_ec* ec, int32_t* steps);
 /* Message of the last error on ec ("" if none); NULL ec: last init error. */
 const char* st_ec_last_error(const st_ec* ec);
 
+
+/* ---------------------------------------------------------------------------------
+ * Droplet microphysics step (§2.3 Eq. 7, 8, 9-11, 12, 13,
+ * P:138-167; closures SPEC S:143-200; readings C-28..C-33 in DESIGN.md §3).
+ *
+ * For every droplet and each of nsteps sub-steps of length dt, field frozen (C-7):
+ *   interpolate (u_f, T_f, rho_v) trilinearly at x (C-5); semi-implicit Euler drag
+ *   (Schiller-Naumann or Stokes, + gravity); dm/dt = 2 pi D_v d rho_sat(T_f)
+ *   (rho_v/rho_sat - S_v,p) (Eq. 7, Magnus rho_sat C-30); m' = max(m + dt dm/dt, 0.01 m)
+ *   (C-32); T' = T + dt [pi Nu kappa d (T_f - T) - L dm/dt] / (m C_p) (Eq. 12, literal
+ *   sign C-31); d' = (6 m'/(pi rho_p))^(1/3); into the cell of the start position add
+ *   acc_u -= w (m'u' - m u - m g dt), acc_rv -= w (m' - m), acc_e -= w C_p (m'T' - m T)
+ *   (Eq. 8, 11, 13; C-8, C-33); reflect / wrap at the walls (C-11, C-12).
+ * State fp32, arithmetic fp64, accumulators fp64 (C-28).  Test oracle:
+ * oracle/microphysics.py.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t abi_version;   /* ST_ABI_VERSION */
+  int32_t dims[3];       /* cells (nx, ny, nz), each >= 1 */
+  double origin[3];      /* m */
+  double cell_size[3];   /* m, > 0 */
+  int32_t bc[3];         /* ST_BC_PERIODIC | ST_BC_REFLECT per axis */
+  double rho_f, nu_f, rho_p;
+  double gravity[3];     /* m/s^2 */
+  int32_t drag_law;      /* ST_DRAG_STOKES | ST_DRAG_SCHILLER_NAUMANN */
+  double D_v;            /* vapour diffusivity, m^2/s */
+  double kappa_f;        /* fluid conductivity, W/(m K) */
+  double cp_p;           /* droplet specific heat, J/(kg K) */
+  double latent;         /* latent heat, J/kg */
+  double nusselt;        /* Nu_p */
+  double s_vp;           /* surface saturation S_v,p */
+  int32_t device;        /* CUDA device ordinal */
+  void* stream;          /* cudaStream_t, NULL = the legacy default stream */
+} st_micro_config;
+
+/* Fill *cfg with the DESIGN.md C-30 constants (air / water, 1 m cells, reflecting). */
+void st_micro_config_default(st_micro_config* cfg);
+
+/* nsteps sub-steps of dt for n droplets.  All arrays are DEVICE pointers, caller-owned:
+ *   x, u: [3][n] fp32 (updated in place); d, T: [n] fp32 (updated); w: [n] fp32 weights;
+ *   F: [5][nz][ny][nx] fp32 cell-centred (u_x, u_y, u_z, T_f, rho_v);
+ *   acc: [5][nz][ny][nx] fp64 fluid-side accumulators (kg m/s x3, kg, J), ADDED to.
+ * n_clamped (host, NULL to skip) receives the number of mass-floor clamps (C-32).
+ * Runs on cfg->stream and blocks until done.  n == 0 is a no-op.
+ * Errors: ST_ERR_INVALID_ARG (bad cfg, n < 0, nsteps < 0, dt <= 0, NULL arrays with
+ * n > 0, host pointers), ST_ERR_CFL (a droplet still outside after one reflection /
+ * wrap: the state is updated, the result is not trustworthy), ST_ERR_CUDA. */
+st_status st_micro_advance(const st_micro_config* cfg, int64_t n, float* x, float* u, float* d, float* T,
+                           const float* w, const float* F, double dt, int32_t nsteps, double* acc,
+                           int64_t* n_clamped);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,23 @@ class StEcConfig(ctypes.Structure):
     ]
 
 
+class StMicroConfig(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("dims", ctypes.c_int32 * 3),
+        ("origin", ctypes.c_double * 3),
+        ("cell_size", ctypes.c_double * 3),
+        ("bc", ctypes.c_int32 * 3),
+        ("rho_f", ctypes.c_double), ("nu_f", ctypes.c_double), ("rho_p", ctypes.c_double),
+        ("gravity", ctypes.c_double * 3),
+        ("drag_law", ctypes.c_int32),
+        ("D_v", ctypes.c_double), ("kappa_f", ctypes.c_double), ("cp_p", ctypes.c_double),
+        ("latent", ctypes.c_double), ("nusselt", ctypes.c_double), ("s_vp", ctypes.c_double),
+        ("device", ctypes.c_int32),
+        ("stream", ctypes.c_void_p),
+    ]
+
+
 SIGNATURES = {
     "st_config_default": (None, [ctypes.POINTER(StConfig)]),
     "st_init": (_i32, [ctypes.POINTER(StConfig), ctypes.POINTER(_vp)]),
@@ -120,6 +137,9 @@ SIGNATURES = {
     "st_ec_ledger": (_i32, [_vp, _vp, _vp, _vp, _vp]),
     "st_ec_backlog": (_i32, [_vp, ctypes.POINTER(_i32)]),
     "st_ec_last_error": (ctypes.c_char_p, [_vp]),
+    "st_micro_config_default": (None, [ctypes.POINTER(StMicroConfig)]),
+    "st_micro_advance": (_i32, [ctypes.POINTER(StMicroConfig), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i32,
+                                _vp, ctypes.POINTER(_i64)]),
 }
 
 _lib = None

@@ -311,3 +311,52 @@ class Extrapolator:
             self.close()
         except Exception:
             pass
+
+
+@dataclass
+class MicroConfig:
+    """Python mirror of st_micro_config (defaults = st_micro_config_default, C-30)."""
+
+    dims: tuple = (1, 1, 1)
+    origin: tuple = (0.0, 0.0, 0.0)
+    cell_size: tuple = (1.0, 1.0, 1.0)
+    bc: tuple = (N.BC_REFLECT,) * 3
+    rho_f: float = 1.2
+    nu_f: float = 1.5e-5
+    rho_p: float = 1000.0
+    gravity: tuple = (0.0, 0.0, -9.81)
+    drag_law: int = N.DRAG_SCHILLER_NAUMANN
+    D_v: float = 2.5e-5
+    kappa_f: float = 0.025
+    cp_p: float = 4186.0
+    latent: float = 2.45e6
+    nusselt: float = 2.0
+    s_vp: float = 1.0
+    device: int = 0
+    stream: int | None = None
+
+    def to_c(self) -> N.StMicroConfig:
+        c = N.StMicroConfig()
+        c.abi_version = N.ST_ABI_VERSION
+        for k in range(3):
+            c.dims[k], c.origin[k], c.cell_size[k] = int(self.dims[k]), float(self.origin[k]), float(self.cell_size[k])
+            c.bc[k], c.gravity[k] = int(self.bc[k]), float(self.gravity[k])
+        for f in ("rho_f", "nu_f", "rho_p", "D_v", "kappa_f", "cp_p", "latent", "nusselt", "s_vp"):
+            setattr(c, f, float(getattr(self, f)))
+        c.drag_law, c.device, c.stream = int(self.drag_law), int(self.device), self.stream
+        return c
+
+
+def micro_advance(cfg: MicroConfig, x, u, d, T, w, F, dt: float, nsteps: int, acc) -> int:
+    """st_micro_advance: nsteps droplet sub-steps (PAPER Eq. 7-13) on CUDA
+    tensors x, u [3, n], d, T, w [n] (fp32, x/u/d/T updated in place), F [5, nz, ny, nx]
+    fp32, acc [5, nz, ny, nx] fp64 (added to).  Returns the number of mass-floor clamps."""
+    lib = N.load()
+    n = int(d.shape[0])
+    c = cfg.to_c()
+    nc = ctypes.c_int64()
+    rc = lib.st_micro_advance(ctypes.byref(c), n, _ptr(x), _ptr(u), _ptr(d), _ptr(T), _ptr(w), _ptr(F),
+                              float(dt), int(nsteps), _ptr(acc), ctypes.byref(nc))
+    if rc:
+        raise N.StError(rc, "st_micro_advance failed")
+    return int(nc.value)

@@ -1,0 +1,55 @@
+"""Time st_micro_advance at the C5 grid with N droplets resident in HBM:
+CUDA events on the launching stream around `calls` calls of `nsteps` sub-steps each,
+after warm-up.  Prints one JSON line (droplet-updates/s and the kernel's HBM roofline:
+algorithmic bytes = 52 B per droplet per call + 5 x 8 B fp64 reductions per droplet
+sub-step)."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2603_26691_b200 import MicroConfig, micro_advance  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=200_000_000)
+ap.add_argument("--nsteps", type=int, default=1)
+ap.add_argument("--calls", type=int, default=5)
+ap.add_argument("--warmup", type=int, default=3)
+a = ap.parse_args()
+
+dims, h = (192, 192, 72), 1.0 / 32
+dev = torch.device("cuda:0")
+F = torch.from_numpy(synth.micro_field(dims, (0.0, 0.0, 0.0), (h,) * 3, seed=4)).to(dev)
+g = torch.Generator(device=dev)
+g.manual_seed(1)
+n = a.n
+x = torch.rand((3, n), generator=g, device=dev) * torch.tensor([6.0, 6.0, 2.25], device=dev)[:, None]
+x = torch.minimum(x, torch.tensor([6.0, 6.0, 2.25], device=dev)[:, None] * (1 - 1e-7))
+u = torch.zeros((3, n), device=dev)
+d = 5e-6 + 25e-6 * torch.rand(n, generator=g, device=dev)
+T = 281.0 + 4.0 * torch.rand(n, generator=g, device=dev)
+w = torch.full((n,), 100.0, device=dev)
+acc = torch.zeros((5, 72, 192, 192), dtype=torch.float64, device=dev)
+cfg = MicroConfig(dims=dims, cell_size=(h,) * 3, bc=(0, 0, 1))
+s = torch.cuda.current_stream()
+cfg.stream = s.cuda_stream
+for _ in range(a.warmup):
+    micro_advance(cfg, x, u, d, T, w, F, 5e-3, a.nsteps, acc)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(s)
+for _ in range(a.calls):
+    micro_advance(cfg, x, u, d, T, w, F, 5e-3, a.nsteps, acc)
+e1.record(s)
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.calls
+peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
+alg = n * (52 + 40 * a.nsteps)
+print(json.dumps({"metric": "droplet-updates/s (microphysics step, f3)", "value": n * a.nsteps / (ms * 1e-3),
+                  "n": n, "nsteps": a.nsteps, "ms_per_call": ms, "alg_bytes_per_call": alg,
+                  "achieved_GBs": alg / (ms * 1e-3) / 1e9, "peaks": peaks}))

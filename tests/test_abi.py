@@ -107,3 +107,45 @@ def test_binding_refuses_missing_library(tmp_path, monkeypatch):
     monkeypatch.setattr(N, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(ImportError):
         N.load()
+
+
+def test_micro_config_layout_default_and_validation(lib):
+    """st_micro_config: C layout == ctypes mirror; defaults are the C-30
+    constants and match MicroConfig; invalid arguments fail before any device work."""
+    from paper_2603_26691_b200 import _native as N
+    from paper_2603_26691_b200.api import MicroConfig
+    prog = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "scaletrack.h"
+int main(void){
+  printf("%zu %zu %zu %zu\n", sizeof(st_micro_config), offsetof(st_micro_config, D_v),
+         offsetof(st_micro_config, device), offsetof(st_micro_config, stream));
+  return 0;
+}'''
+    tmp = os.path.join(ROOT, "build")
+    os.makedirs(tmp, exist_ok=True)
+    c_src, exe = os.path.join(tmp, "micro_probe.c"), os.path.join(tmp, "micro_probe")
+    open(c_src, "w").write(prog)
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", exe, c_src])
+    vals = [int(v) for v in subprocess.check_output([exe]).split()]
+    M = N.StMicroConfig
+    assert vals == [ctypes.sizeof(M), M.D_v.offset, M.device.offset, M.stream.offset]
+    c = M()
+    lib.st_micro_config_default(ctypes.byref(c))
+    py = MicroConfig().to_c()
+    for f, _ in M._fields_:
+        got, want = getattr(c, f), getattr(py, f)
+        if hasattr(got, "_length_"):
+            got, want = list(got), list(want)
+        assert got == want, f
+    nc = ctypes.c_int64(7)
+    # n == 0 is a no-op even without a GPU; bad arguments are rejected first
+    assert lib.st_micro_advance(ctypes.byref(c), 0, None, None, None, None, None, None, 1e-3, 1, None,
+                                ctypes.byref(nc)) == 0 and nc.value == 0
+    assert lib.st_micro_advance(ctypes.byref(c), 4, None, None, None, None, None, None, 1e-3, 1, None, None) == 1
+    assert lib.st_micro_advance(ctypes.byref(c), 4, None, None, None, None, None, None, 0.0, 1, None, None) == 1
+    bad = M()
+    lib.st_micro_config_default(ctypes.byref(bad))
+    bad.cell_size[1] = 0.0
+    assert lib.st_micro_advance(ctypes.byref(bad), 0, None, None, None, None, None, None, 1e-3, 1, None, None) == 1

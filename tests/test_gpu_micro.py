@@ -1,0 +1,135 @@
+"""GPU parity of the droplet-microphysics step (st_micro_advance) against
+the fp64-arithmetic / fp32-storage oracle (oracle/microphysics.py, reading C-28), through
+the C-ABI.  Tolerances: both sides round the same fp64 operations in the
+same order, so the fp32 state agrees to within one fp32 ulp of a rare last-bit flip
+(libm exp/pow/cbrt may differ by one fp64 ulp); sources differ only by the fp64
+summation order plus those flips: 1e-6 of the largest cell magnitude per component."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synth  # noqa: E402
+from oracle import microphysics as M  # noqa: E402
+
+
+def _setup(n, dims=(24, 20, 12), h=0.125, bc=(0, 0, 1), seed=11, field_kw=None, drop_kw=None):
+    mesh = M.MicroMesh(dims=dims, origin=(0.0, 0.0, 0.0), cell_size=(h,) * 3, bc=bc)
+    F = synth.micro_field(dims, mesh.origin, mesh.cell_size, seed=seed, **(field_kw or {}))
+    hi = tuple(dims[a] * h for a in range(3))
+    x, u, d, T, w = synth.droplets_np(n, (0.0, 0.0, 0.0), hi, seed=seed + 1, **(drop_kw or {}))
+    return mesh, F, x, u, d, T, w
+
+
+def _gpu_run(mesh, props, F, x, u, d, T, w, dt, calls):
+    from paper_2603_26691_b200 import MicroConfig, micro_advance
+    cfg = MicroConfig(dims=mesh.dims, origin=mesh.origin, cell_size=mesh.cell_size, bc=mesh.bc,
+                      rho_f=props.rho_f, nu_f=props.nu_f, rho_p=props.rho_p, gravity=props.gravity,
+                      drag_law=props.drag_law, D_v=props.D_v, kappa_f=props.kappa_f, cp_p=props.cp_p,
+                      latent=props.latent, nusselt=props.nusselt, s_vp=props.s_vp)
+    dev = torch.device("cuda:0")
+    tx, tu, td, tT, tw = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, u, d, T, w))
+    tF = torch.from_numpy(np.ascontiguousarray(F)).to(dev)
+    acc = torch.zeros((5,) + tuple(reversed(mesh.dims)), dtype=torch.float64, device=dev)
+    clamps = 0
+    for k in calls:
+        clamps += micro_advance(cfg, tx, tu, td, tT, tw, tF, dt, k, acc)
+    return (tx.cpu().numpy(), tu.cpu().numpy(), td.cpu().numpy(), tT.cpu().numpy(),
+            acc.cpu().numpy().reshape(5, -1), clamps)
+
+
+def _oracle_run(mesh, props, F, x, u, d, T, w, dt, calls):
+    acc, clamps = None, 0
+    for k in calls:
+        x, u, d, T, acc, c = M.micro_advance(mesh, props, x, u, d, T, w, F, dt, k, acc=acc)
+        clamps += c
+    return x, u, d, T, acc, clamps
+
+
+def _compare(g, o, mesh, tag=""):
+    gx, gu, gd, gT, gacc, gc = g
+    ox, ou, od, oT, oacc, oc = o
+    L = max(mesh.dims[a] * mesh.cell_size[a] for a in range(3))
+    assert gc == oc, tag
+    np.testing.assert_allclose(gx, ox, rtol=0, atol=2e-7 * L, err_msg=tag)
+    np.testing.assert_allclose(gu, ou, rtol=1e-5, atol=1e-6, err_msg=tag)
+    np.testing.assert_allclose(gd, od, rtol=1e-6, atol=0, err_msg=tag)
+    np.testing.assert_allclose(gT, oT, rtol=1e-6, atol=0, err_msg=tag)
+    assert np.mean(gx == ox) > 0.999 and np.mean(gd == od) > 0.999 and np.mean(gT == oT) > 0.999, tag
+    for k in range(5):
+        scale = np.max(np.abs(oacc[k])) + 1e-300
+        assert np.max(np.abs(gacc[k] - oacc[k])) <= 1e-6 * scale, (tag, k)
+
+
+@pytest.mark.parametrize("n,calls,bc", [
+    (20_000, (3, 2), (0, 0, 1)),        # many tiles + ragged tail, two calls accumulate
+    (257, (4,), (1, 1, 1)),             # one full CTA + 1, all walls reflecting
+    (1, (6,), (0, 0, 0)),               # a single droplet, fully periodic
+])
+def test_micro_parity(n, calls, bc):
+    mesh, F, x, u, d, T, w = _setup(n, bc=bc)
+    props = M.MicroProps()
+    dt = 5e-3
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, dt, calls)
+    o = _oracle_run(mesh, props, F, x, u, d, T, w, dt, calls)
+    _compare(g, o, mesh, f"n={n}")
+
+
+def test_micro_parity_stokes_fast_flow_walls():
+    """Stokes drag, u_rms = 2 m/s field so droplets cross cells and hit the z walls."""
+    mesh, F, x, u, d, T, w = _setup(5000, field_kw={"u_rms": 2.0}, drop_kw={"d_range": (20e-6, 60e-6)})
+    props = M.MicroProps(drag_law=M.DRAG_STOKES)
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 5e-3, (8,))
+    o = _oracle_run(mesh, props, F, x, u, d, T, w, 5e-3, (8,))
+    _compare(g, o, mesh, "stokes")
+
+
+def test_micro_mass_floor_clamps_match():
+    """Dry, warm field with tiny droplets and a long step: the C-32 floor engages."""
+    mesh, F, x, u, d, T, w = _setup(3000, field_kw={"T0": 300.0, "rho_v0": 1e-4},
+                                    drop_kw={"d_range": (0.5e-6, 3e-6)})
+    props = M.MicroProps()
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 0.2, (2,))
+    o = _oracle_run(mesh, props, F, x, u, d, T, w, 0.2, (2,))
+    assert o[5] > 0
+    _compare(g, o, mesh, "floor")
+
+
+def test_micro_empty_and_errors():
+    from paper_2603_26691_b200 import MicroConfig, StError, micro_advance
+    cfg = MicroConfig(dims=(4, 4, 4), cell_size=(0.25,) * 3)
+    dev = torch.device("cuda:0")
+    e3 = torch.empty((3, 0), device=dev)
+    e1 = torch.empty(0, device=dev)
+    F = torch.zeros((5, 4, 4, 4), device=dev)
+    acc = torch.zeros((5, 4, 4, 4), dtype=torch.float64, device=dev)
+    assert micro_advance(cfg, e3, e3.clone(), e1, e1.clone(), e1.clone(), F, 1e-3, 3, acc) == 0
+    x = torch.full((3, 4), 0.5)                     # host tensors -> rejected
+    with pytest.raises(StError):
+        micro_advance(cfg, x, x.clone(), torch.ones(4), torch.ones(4), torch.ones(4), F, 1e-3, 1, acc)
+
+
+def test_micro_full_size_sampled():
+    """2e7 droplets on the bench grid (192 x 192 x 72, h = 1/32): droplets are independent
+    given the frozen field, so the oracle run on a 2000-droplet sample gives exactly their
+    states; the vapour ledger of the whole field closes in fp64."""
+    from paper_2603_26691_b200 import MicroConfig, micro_advance
+    dims, h = (192, 192, 72), 1.0 / 32
+    mesh = M.MicroMesh(dims=dims, origin=(0.0, 0.0, 0.0), cell_size=(h,) * 3, bc=(0, 0, 1))
+    F = synth.micro_field(dims, mesh.origin, mesh.cell_size, seed=4)
+    n = 20_000_000
+    hi = (6.0, 6.0, 2.25)
+    x, u, d, T, w = synth.droplets_np(n, (0.0, 0.0, 0.0), hi, seed=9)
+    props = M.MicroProps()
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 5e-3, (2,))
+    idx = np.random.default_rng(0).choice(n, 2000, replace=False)
+    o = M.micro_advance(mesh, props, x[:, idx], u[:, idx], d[idx], T[idx], w[idx], F, 5e-3, 2)
+    np.testing.assert_allclose(g[0][:, idx], o[0], rtol=0, atol=2e-7 * 6.0)
+    np.testing.assert_allclose(g[2][idx], o[2], rtol=1e-6)
+    np.testing.assert_allclose(g[3][idx], o[3], rtol=1e-6)
+    m0 = M.droplet_mass(d, props.rho_p)
+    m1 = M.droplet_mass(g[2], props.rho_p)
+    dM = np.sum(w.astype(np.float64) * (m1 - m0))
+    # fp32 storage of d limits the droplet-side sum, not the GPU accumulation
+    assert abs(g[4][3].sum() + dM) <= 1e-4 * abs(dM) + 1e-6 * np.sum(w * m0) * 1e-6
