@@ -4,7 +4,8 @@
 // One thread per droplet carries its state in registers through all nsteps sub-steps
 // (the field is frozen within a call, C-7, so droplets are independent): the state is
 // read and written once per call (24 B in + 24 B out + 4 B weight per droplet) and
-// every sub-step adds 5 fp64 reductions into the start cell.  Arithmetic is fp64 on
+// every sub-step adds 5 fp64 reductions into the start cell, one per run of lanes that
+// share the cell (a binned store, C-15, makes those runs long).  Arithmetic is fp64 on
 // fp32 storage (C-28); this file is compiled with -fmad=false so each operation rounds
 // on its own, in the order the definition is written (the oracle's order), which keeps
 // the fp32 state and the cell decisions identical to the oracle's.
@@ -58,12 +59,17 @@ __global__ void __launch_bounds__(256) k_micro(MicroArgs a) {
   const int64_t ncell = (int64_t)a.nx * a.ny * a.nz;
   const int dims[3] = {a.nx, a.ny, a.nz};
   unsigned long long clamps = 0, cfl = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float xs[3] = {a.x[i], a.x[a.n + i], a.x[2 * a.n + i]};
-    float us[3] = {a.u[i], a.u[a.n + i], a.u[2 * a.n + i]};
-    float ds = a.d[i], Ts = a.T[i];
-    const double wn = -(double)a.w[i];
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // whole warps iterate together (the deposit reduction below is warp-collective)
+  const int64_t n_round = (a.n + 31) & ~(int64_t)31;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+    const bool valid = i < a.n;
+    const int64_t j = valid ? i : a.n - 1;          // tail lanes shadow the last droplet
+    float xs[3] = {a.x[j], a.x[a.n + j], a.x[2 * a.n + j]};
+    float us[3] = {a.u[j], a.u[a.n + j], a.u[2 * a.n + j]};
+    float ds = a.d[j], Ts = a.T[j];
+    const double wn = valid ? -(double)a.w[j] : 0.0;
     for (int s = 0; s < a.nsteps; ++s) {
       double xp[3] = {xs[0], xs[1], xs[2]}, up[3] = {us[0], us[1], us[2]};
       const double dp = ds, Tp = Ts;
@@ -120,25 +126,42 @@ __global__ void __launch_bounds__(256) k_micro(MicroArgs a) {
       const double mdot = a.c_m * dp * rs * (svf - a.s_vp);
       double mn = m + a.dt * mdot;
       const double mfloor = 0.01 * m;
-      if (mn < mfloor) { mn = mfloor; ++clamps; }
+      if (mn < mfloor) { mn = mfloor; clamps += valid; }
       const double q = a.c_q * dp * (Tf - Tp);
       const double Tn = Tp + a.dt * ((q - a.latent * mdot) / (m * a.cp_p));
       const double dn = cbrt(6.0 * mn / a.c_d);
       // 5 fluid-side sources into the start cell (Eq. 8, 11, 13; C-8, C-33)
-      for (int k = 0; k < 3; ++k)
-        atomicAdd(a.acc + k * ncell + cell, wn * ((mn * un[k] - m * up[k]) - m * a.g[k] * a.dt));
-      atomicAdd(a.acc + 3 * ncell + cell, wn * (mn - m));
-      atomicAdd(a.acc + 4 * ncell + cell, wn * a.cp_p * (mn * Tn - m * Tp));
+      double dep[5];
+      for (int k = 0; k < 3; ++k) dep[k] = wn * ((mn * un[k] - m * up[k]) - m * a.g[k] * a.dt);
+      dep[3] = wn * (mn - m);
+      dep[4] = wn * a.cp_p * (mn * Tn - m * Tp);
+      // Runs of lanes with the same start cell (contiguous in a binned store) are summed
+      // into the run's first lane by a segmented suffix scan; one fp64 reduction per run.
+      const int key = valid ? (int)cell : -1 - lane;
+      const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+      const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != key);
+      const unsigned above = lane == 31 ? 0u : heads & (0xffffffffu << (lane + 1));
+      const int end = above ? __ffs(above) - 1 : 32;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const double o = __shfl_down_sync(0xffffffffu, dep[k], off);
+          if (lane + off < end) dep[k] = dep[k] + o;
+        }
+      }
+      if (valid && ((heads >> lane) & 1u))
+        for (int k = 0; k < 5; ++k) atomicAdd(a.acc + k * ncell + cell, dep[k]);
       // 6 walls / periodic (C-11, C-12), round the state to fp32
       for (int k = 0; k < 3; ++k) {
         double v = xn[k];
         if (a.bc[k] == ST_BC_PERIODIC) {
           if (v < a.lo[k]) v = v + a.L[k];
           else if (v >= a.hi[k]) v = v - a.L[k];
-          if (v < a.lo[k] || v >= a.hi[k]) ++cfl;
+          if (v < a.lo[k] || v >= a.hi[k]) cfl += valid;
         } else {
-          if (v < a.lo[k]) { v = 2.0 * a.lo[k] - v; un[k] = -un[k]; if (v > a.hi[k]) ++cfl; }
-          else if (v > a.hi[k]) { v = 2.0 * a.hi[k] - v; un[k] = -un[k]; if (v < a.lo[k]) ++cfl; }
+          if (v < a.lo[k]) { v = 2.0 * a.lo[k] - v; un[k] = -un[k]; if (v > a.hi[k]) cfl += valid; }
+          else if (v > a.hi[k]) { v = 2.0 * a.hi[k] - v; un[k] = -un[k]; if (v < a.lo[k]) cfl += valid; }
         }
         xs[k] = (float)v;
         us[k] = (float)un[k];
@@ -146,6 +169,7 @@ __global__ void __launch_bounds__(256) k_micro(MicroArgs a) {
       ds = (float)dn;
       Ts = (float)Tn;
     }
+    if (!valid) continue;
     for (int k = 0; k < 3; ++k) {
       a.x[k * a.n + i] = xs[k];
       a.u[k * a.n + i] = us[k];
@@ -198,6 +222,7 @@ extern "C" st_status st_micro_advance(const st_micro_config* c, int64_t n, float
   for (int k = 0; k < 3; ++k)
     if (c->dims[k] < 1 || !(c->cell_size[k] > 0.0) || (c->bc[k] != ST_BC_PERIODIC && c->bc[k] != ST_BC_REFLECT))
       return ST_ERR_INVALID_ARG;
+  if ((int64_t)c->dims[0] * c->dims[1] * c->dims[2] >= (1ll << 31)) return ST_ERR_INVALID_ARG;
   if (c->drag_law != ST_DRAG_STOKES && c->drag_law != ST_DRAG_SCHILLER_NAUMANN) return ST_ERR_INVALID_ARG;
   if (!(c->rho_p > 0.0) || !(c->rho_f > 0.0) || !(c->nu_f > 0.0) || !(c->cp_p > 0.0)) return ST_ERR_INVALID_ARG;
   if (n_clamped) *n_clamped = 0;
@@ -250,7 +275,7 @@ extern "C" st_status st_micro_advance(const st_micro_config* c, int64_t n, float
   a.counters = cnt;
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-  const int64_t need = (n + 255) / 256;
+  const int64_t need = (n + 255) / 256;   // block size 256 = 8 whole warps
   const int64_t cap = (int64_t)nsm * 8;            // 8 resident 256-thread CTAs per SM
   const int grid = (int)(need < cap ? need : cap);
   k_micro<<<grid, 256, 0, s>>>(a);

@@ -76,6 +76,19 @@ def test_micro_parity(n, calls, bc):
     _compare(g, o, mesh, f"n={n}")
 
 
+def test_micro_parity_binned_store():
+    """Droplets ordered by cell (the binned store of C-15): long runs of lanes share a start
+    cell, so the segmented warp reduction of the deposits is exercised; 8 droplets/cell."""
+    mesh, F, x, u, d, T, w = _setup(8 * 24 * 20 * 12 + 77)
+    c = np.floor(x.astype(np.float64) / 0.125).astype(np.int64)
+    order = np.lexsort((c[0], c[1], c[2]))
+    x, u, d, T, w = x[:, order].copy(), u[:, order].copy(), d[order].copy(), T[order].copy(), w[order].copy()
+    props = M.MicroProps()
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 5e-3, (2, 3))
+    o = _oracle_run(mesh, props, F, x, u, d, T, w, 5e-3, (2, 3))
+    _compare(g, o, mesh, "binned")
+
+
 def test_micro_parity_stokes_fast_flow_walls():
     """Stokes drag, u_rms = 2 m/s field so droplets cross cells and hit the z walls."""
     mesh, F, x, u, d, T, w = _setup(5000, field_kw={"u_rms": 2.0}, drop_kw={"d_range": (20e-6, 60e-6)})
