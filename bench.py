@@ -49,6 +49,7 @@ def parse():
                     help="K: rebin (fused neighbour scatter) every K-th step; particles that moved more than one "
                          "cell in between go to their bin's far tail (C-15b, DESIGN.md section 9)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-micro", action="store_true", help="skip the droplet-microphysics side measurement (f3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target oracle CPU time for cpu_baseline")
     return ap.parse_args()
@@ -177,6 +178,47 @@ def bench_config(wl, n_per, K, G, decomp):
             "rebin_interval": K, "substeps_per_step": 1,
             "l2": "inputs larger than L2 (40 B x N resident particle state)",
             "parallelism": f"z-slab x{G}" if decomp == "slab" else f"particle-sharded x{G}"}
+
+
+def micro_leg(dev, n=200_000_000, calls=5, warmup=3):
+    """Side measurement of NEXT f3 (st_micro_advance): n droplets in the
+    binned (cell-sorted) order on the C5 grid, one sub-step per call, CUDA events on the
+    launching stream after warm-up.  Not part of the headline step."""
+    import torch
+
+    import synth
+    from paper_2603_26691_b200 import MicroConfig, micro_advance
+    dims, h = (192, 192, 72), 1.0 / 32
+    box = torch.tensor([6.0, 6.0, 2.25], device=dev)[:, None]
+    F = torch.from_numpy(synth.micro_field(dims, (0.0, 0.0, 0.0), (h,) * 3, seed=4)).to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1)
+    x = torch.minimum(torch.rand((3, n), generator=g, device=dev) * box, box * (1 - 1e-7))
+    c = torch.floor(x / h).to(torch.int64)
+    x = x[:, torch.argsort((c[2] * dims[1] + c[1]) * dims[0] + c[0])].contiguous()
+    del c
+    u = torch.zeros((3, n), device=dev)
+    d = 5e-6 + 25e-6 * torch.rand(n, generator=g, device=dev)
+    T = 281.0 + 4.0 * torch.rand(n, generator=g, device=dev)
+    w = torch.full((n,), 100.0, device=dev)
+    acc = torch.zeros((5, dims[2], dims[1], dims[0]), dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream()
+    cfg = MicroConfig(dims=dims, cell_size=(h,) * 3, bc=(0, 0, 1), stream=s.cuda_stream)
+    for _ in range(warmup):
+        micro_advance(cfg, x, u, d, T, w, F, 5e-3, 1, acc)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(calls):
+        micro_advance(cfg, x, u, d, T, w, F, 5e-3, 1, acc)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / calls
+    alg = n * (52 + 40)
+    return {"metric": "droplet-updates/s (microphysics sub-step, NEXT f3)", "value": n / (ms * 1e-3),
+            "unit": "droplet-updates/s", "droplets": n, "ms_per_call": ms, "calls": calls,
+            "order": "binned (cell-sorted)", "alg_bytes_per_call": alg, "achieved_GBs": alg / (ms * 1e-3) / 1e9,
+            "bound": "alu (fp64 transcendentals; DESIGN.md 9e)"}
 
 
 def run_reference(args):
@@ -386,6 +428,14 @@ def run_ours(args):
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, args.cpu_seconds, K)
 
+    micro = None
+    if rank == 0 and G == 1 and not args.no_micro:
+        try:
+            micro = micro_leg(dev)
+        except Exception as e:                      # a side measurement never sinks the bench line
+            micro = {"error": f"{type(e).__name__}: {e}"[:300]}
+        torch.cuda.empty_cache()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
@@ -402,6 +452,7 @@ def run_ours(args):
             "f_move_chunk": f_move, "fused_rebins": st_stats["fused_rebins"],
             "general_rebins": st_stats["general_rebins"], "far_last_rebin": st_stats["last_far"],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+            "micro_f3": micro,
         }
         print(json.dumps(line), flush=True)
     st.close()
