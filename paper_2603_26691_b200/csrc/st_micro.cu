@@ -44,8 +44,9 @@ struct MicroArgs {
   unsigned long long* counters;   // [0] clamps, [1] CFL violations
 };
 
+// Ghost mapping of i in [-1, n] (C-5): periodic wraps, reflecting replicates the edge.
 __device__ __forceinline__ int ghost(int i, int n, int bc) {
-  if (bc == ST_BC_PERIODIC) return ((i % n) + n) % n;
+  if (bc == ST_BC_PERIODIC) return i < 0 ? i + n : (i >= n ? i - n : i);
   return i < 0 ? 0 : (i > n - 1 ? n - 1 : i);
 }
 
@@ -92,15 +93,20 @@ __global__ void __launch_bounds__(256, 4) k_micro(MicroArgs a) {
         i0[k] = ii;
         fr[k] = f;
       }
+      int gi[3][2];
+      for (int k = 0; k < 3; ++k) {
+        gi[k][0] = ghost(i0[k], dims[k], a.bc[k]);
+        gi[k][1] = ghost(i0[k] + 1, dims[k], a.bc[k]);
+      }
       double fv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
       for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
         for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
           for (int cx = 0; cx < 2; ++cx) {
             double wt = ((cx ? fr[0] : 1.0 - fr[0]) * (cy ? fr[1] : 1.0 - fr[1])) * (cz ? fr[2] : 1.0 - fr[2]);
-            const int ix = ghost(i0[0] + cx, a.nx, a.bc[0]);
-            const int iy = ghost(i0[1] + cy, a.ny, a.bc[1]);
-            const int iz = ghost(i0[2] + cz, a.nz, a.bc[2]);
-            const int64_t cc = ((int64_t)iz * a.ny + iy) * a.nx + ix;
+            const int64_t cc = ((int64_t)gi[2][cz] * a.ny + gi[1][cy]) * a.nx + gi[0][cx];
 #pragma unroll
             for (int k = 0; k < 5; ++k) fv[k] = fv[k] + wt * (double)__ldg(a.F + k * ncell + cc);
           }
