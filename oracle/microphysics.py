@@ -31,6 +31,8 @@ are rounded to ``store`` at the end of each sub-step.
 Parity status: pinned by tests/test_oracle_micro.py (SPEC worked examples, d^2-law
 closed form and first-order convergence, the exact discrete temperature relaxation,
 mass / momentum / energy ledgers, equilibrium, interpolation against the C oracle).
+Parity unpinned: trajectory values of the coupled step in a non-uniform field beyond
+those invariants (no closed form exists); they are checked GPU-vs-oracle only.
 """
 from __future__ import annotations
 
