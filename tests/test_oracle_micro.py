@@ -1,7 +1,9 @@
 """Pins of the droplet-microphysics oracle (oracle/microphysics.py) against
 what the paper, SPEC worked examples, textbook tables and closed forms fix — never against
 the oracle's own formulas retyped.  CPU only."""
+import json
 import math
+import os
 
 import numpy as np
 import pytest
@@ -11,6 +13,7 @@ import synth
 from oracle import microphysics as M
 
 P = M.MicroProps()
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
 
 
 def _box(dims=(4, 4, 4), h=0.25, bc=M.BC_PERIODIC):
@@ -35,8 +38,8 @@ def test_saturation_density_spec_and_table():
     """S:154-156 (293.15 K -> 0.0173, 273.15 K -> 0.00485, +-5 %) and the psychrometric
     table (saturated vapour density 9.40e-3 kg/m^3 at 10 C, 30.4e-3 at 30 C, +-2 %)."""
     rs = M.saturation_vapor_density
-    assert abs(rs(293.15) / 0.0173 - 1) < 0.05
-    assert abs(rs(273.15) / 0.00485 - 1) < 0.05
+    for c in GOLDEN["saturation_vapor_density"]["cases"]:
+        assert abs(rs(c["T"]) / c["expect"] - 1) < c["rel"]
     assert abs(rs(283.15) / 9.40e-3 - 1) < 0.02
     assert abs(rs(303.15) / 30.4e-3 - 1) < 0.02
     T = np.linspace(200, 350, 301)
@@ -46,9 +49,10 @@ def test_saturation_density_spec_and_table():
 def test_mass_transfer_spec_example():
     """d=1e-5, D_v=2.5e-5, rho_v,sat=0.01, S_v,f - S_v,p = 0.01 -> 1.5708e-13 kg/s."""
     from scipy.optimize import brentq
-    T = brentq(lambda t: M.saturation_vapor_density(t) - 0.01, 250.0, 320.0, xtol=1e-12)
-    r = M.mass_transfer_rate(1e-5, 0.01 * 1.01, T, M.MicroProps(D_v=2.5e-5))
-    assert abs(r / 1.5708e-13 - 1) < 1e-4
+    g = GOLDEN["mass_transfer_rate"]
+    T = brentq(lambda t: M.saturation_vapor_density(t) - g["rho_v_sat"], 250.0, 320.0, xtol=1e-12)
+    r = M.mass_transfer_rate(g["d_p"], g["rho_v_sat"] * (1 + g["dS"]), T, M.MicroProps(D_v=g["D_v"]))
+    assert abs(r / g["expect"] - 1) < g["rel"]
     assert M.mass_transfer_rate(1e-5, M.saturation_vapor_density(T), T, P) == 0.0                    # S:145
     assert M.mass_transfer_rate(1e-5, 0.0102, T, P) > 0                              # S:146
 
