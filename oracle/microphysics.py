@@ -21,7 +21,8 @@ What it follows (PAPER.md = P, SPEC.md = S; readings C-28..C-33 in DESIGN.md §3
   acc_e  += -w C_p (m' T' - m T);   S = acc / (V_cell * dt * nsteps)  (C-13);
 * mass floor: m' = max(m + dt dm/dt, 0.01 m), counted (S:199, C-32);
 * diameter recomputed from the new mass, d' = (6 m' / (pi rho_p))^(1/3) (S:173, C-33);
-* walls: specular reflection or periodic wrap (C-11, C-12).
+* walls: specular reflection or periodic wrap (C-11, C-12); the C-12
+  fix-up is applied to the stored value (a wrap that rounds onto hi is stored as lo).
 
 Storage (C-28): the state (x, u, d, T, w) and the 5-component field are stored in
 ``store`` precision (float32 for the GPU parity tests, float64 for the pins); every
@@ -226,6 +227,12 @@ def micro_advance(mesh: MicroMesh, props: MicroProps, x, u, d, T, w, F, dt, nste
         for a in range(3):
             xn[a], un[a] = _apply_bc(xn[a], un[a], lo[a], hi[a], mesh.bc[a])
         x, u, d, T = xn.astype(store), un.astype(store), dn.astype(store), Tn.astype(store)
+        # C-12 fix-up in storage precision: a wrapped position that rounds onto hi (or
+        # below lo) is stored as lo, so the periodic domain stays half-open [lo, hi)
+        for a in range(3):
+            if mesh.bc[a] == BC_PERIODIC:
+                lo_s, hi_s = store(lo[a]), store(hi[a])
+                x[a] = np.where((x[a] >= hi_s) | (x[a] < lo_s), lo_s, x[a])
     return x, u, d, T, acc, n_clamped
 
 

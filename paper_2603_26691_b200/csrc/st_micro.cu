@@ -171,6 +171,8 @@ __global__ void __launch_bounds__(256, 4) k_micro(MicroArgs a) {
           else if (v > a.hi[k]) { v = 2.0 * a.hi[k] - v; un[k] = -un[k]; if (v < a.lo[k]) cfl += valid; }
         }
         xs[k] = (float)v;
+        // C-12 fix-up in storage precision: a wrap that rounds onto hi is stored as lo
+        if (a.bc[k] == ST_BC_PERIODIC && (xs[k] >= (float)a.hi[k] || xs[k] < (float)a.lo[k])) xs[k] = (float)a.lo[k];
         us[k] = (float)un[k];
       }
       ds = (float)dn;

@@ -146,3 +146,43 @@ def test_micro_full_size_sampled():
     dM = np.sum(w.astype(np.float64) * (m1 - m0))
     # fp32 storage of d limits the droplet-side sum, not the GPU accumulation
     assert abs(g[4][3].sum() + dM) <= 1e-4 * abs(dM) + 1e-6 * np.sum(w * m0) * 1e-6
+
+
+@pytest.mark.parametrize("side", ["lo", "hi"])
+def test_micro_periodic_wrap_fixup_gpu(side):
+    """C-12 on the GPU: the stored fp32 position after a periodic wrap is in [lo, hi);
+    a wrap that rounds onto hi is stored as lo, exactly as the oracle pin fixes it."""
+    mesh = M.MicroMesh(dims=(4, 4, 4), origin=(0.0, 0.0, 0.0), cell_size=(0.25,) * 3, bc=(0, 0, 0))
+    props = M.MicroProps(gravity=(0.0, 0.0, 0.0), drag_law=M.DRAG_STOKES, rho_p=1e9)
+    Tf = 283.15
+    F = np.empty((5, 4, 4, 4), np.float32)
+    F[:3], F[3], F[4] = 0.0, Tf, float(M.saturation_vapor_density(Tf))
+    x0 = 1e-9 if side == "lo" else float(np.nextafter(np.float32(1.0), np.float32(0.0)))
+    u0 = -1.0 if side == "lo" else 1.0
+    x = np.array([[x0], [0.5], [0.5]], np.float32)
+    u = np.array([[u0], [0.0], [0.0]], np.float32)
+    d, T, w = np.array([2e-5], np.float32), np.array([Tf], np.float32), np.ones(1, np.float32)
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 2e-9, (1,))
+    o = _oracle_run(mesh, props, F, x, u, d, T, w, 2e-9, (1,))
+    assert 0.0 <= g[0][0, 0] < 1.0
+    assert g[0][0, 0] == o[0][0, 0]
+    if side == "lo":
+        assert g[0][0, 0] == np.float32(0.0)
+
+
+def test_micro_deposit_start_cell_gpu():
+    """C-10 on the GPU: a droplet crossing a face deposits into its start cell only."""
+    mesh = M.MicroMesh(dims=(4, 4, 4), origin=(0.0, 0.0, 0.0), cell_size=(0.25,) * 3, bc=(1, 1, 1))
+    props = M.MicroProps(gravity=(0.0, 0.0, -9.81), drag_law=M.DRAG_STOKES)
+    F = np.empty((5, 4, 4, 4), np.float32)
+    F[:3], F[3], F[4] = 0.0, 290.0, 0.006
+    x = np.array([[0.499], [0.6], [0.3]], np.float32)
+    u = np.array([[2.0], [0.0], [0.0]], np.float32)
+    d, T, w = np.array([4e-4], np.float32), np.array([285.0], np.float32), np.array([3.0], np.float32)
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 2e-3, (1,))
+    o = _oracle_run(mesh, props, F, x, u, d, T, w, 2e-3, (1,))
+    assert g[0][0, 0] > 0.5
+    start = (1 * 4 + 2) * 4 + 1
+    for k in (0, 2, 3, 4):
+        assert np.flatnonzero(g[4][k]).tolist() == [start], k
+    _compare(g, o, mesh, "start-cell")

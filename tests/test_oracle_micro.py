@@ -221,3 +221,51 @@ def test_trilinear_matches_pinned_c_oracle():
         np.testing.assert_allclose(got[0:3], a, rtol=0, atol=1e-13)
         np.testing.assert_allclose(got[3], b[0], rtol=1e-14)
         np.testing.assert_allclose(got[4], b[1], rtol=1e-13)
+
+
+# ---- deposit cell (C-10) and periodic wrap (C-12) ------------------------------------
+
+def test_deposit_goes_to_start_cell():
+    """C-10 (P:146 "the Eulerian grid cell containing the particle"; Eq. 8, 11, 13): a
+    droplet that crosses a face during the sub-step deposits all five fluid-side sources
+    into the cell of the sub-step START position; the end cell receives nothing.  The
+    vapour source is minus the droplet's mass gain, read from its new diameter."""
+    mesh = _box(dims=(4, 4, 4), h=0.25, bc=M.BC_REFLECT)
+    props = M.MicroProps(gravity=(0.0, 0.0, -9.81), drag_law=M.DRAG_STOKES)
+    F = _uniform_field(mesh, uf=(0.0, 0.0, 0.0), Tf=290.0, rv=0.006)        # sub-saturated: evaporates
+    x, u, d, T, w = _one(x=(0.499, 0.6, 0.3), u=(2.0, 0.0, 0.0), d=4e-4, T=285.0, w=3.0)
+    dt = 2e-3
+    xn, un, dn, Tn, acc, _ = M.micro_advance(mesh, props, x, u, d, T, w, F, dt, 1, store=np.float64)
+    assert xn[0, 0] > 0.5                                   # crossed x = 0.5 into cell ix = 2
+    start = (1 * 4 + 2) * 4 + 1                             # (iz, iy, ix) = (1, 2, 1)
+    end = (1 * 4 + 2) * 4 + 2
+    for k in range(5):
+        nz = np.flatnonzero(acc[k])
+        assert nz.tolist() == ([] if k == 1 else [start]), (k, nz)     # no y motion: S_u,y = 0
+    assert acc[:, end].tolist() == [0.0] * 5
+    m0, m1 = M.droplet_mass(d, props.rho_p), M.droplet_mass(dn, props.rho_p)
+    assert m1[0] < m0[0]
+    assert acc[3, start] == pytest.approx(-3.0 * (m1[0] - m0[0]), rel=1e-9)
+
+
+@pytest.mark.parametrize("side", ["lo", "hi"])
+def test_periodic_wrap_stays_half_open_fp32(side):
+    """C-12 (the main oracle's P-8 fix-up): after a periodic wrap the STORED fp32
+    position lies in [lo, hi).  A droplet 1e-9 m below lo wraps to lo + L - 1e-9, which
+    rounds to hi in fp32; C-12 maps it to lo.  From just below hi the wrap lands at lo
+    exactly.  Without the fix-up the stored x would equal hi (outside [lo, hi))."""
+    mesh = _box(dims=(4, 4, 4), h=0.25, bc=M.BC_PERIODIC)
+    props = M.MicroProps(gravity=(0.0, 0.0, 0.0), drag_law=M.DRAG_STOKES, rho_p=1e9)   # ballistic
+    Tf = 283.15
+    F = _uniform_field(mesh, Tf=Tf, rv=float(M.saturation_vapor_density(Tf)))
+    if side == "lo":
+        x, u, d, T, w = _one(x=(1e-9, 0.5, 0.5), u=(-1.0, 0.0, 0.0), T=Tf)
+    else:
+        x, u, d, T, w = _one(x=(float(np.nextafter(np.float32(1.0), np.float32(0.0))), 0.5, 0.5),
+                             u=(1.0, 0.0, 0.0), T=Tf)
+    xn, un, *_ = M.micro_advance(mesh, props, x, u, d, T, w, F, 2e-9, 1, store=np.float32)
+    assert xn.dtype == np.float32
+    assert 0.0 <= xn[0, 0] < 1.0
+    if side == "lo":
+        assert xn[0, 0] == np.float32(0.0)
+    assert un[0, 0] == np.float32(u[0, 0])                 # a wrap keeps the velocity

@@ -272,6 +272,56 @@ def test_p5_interpolation_linear_and_convex():
         assert v[k].min() >= G[k].min() - 1e-14 and v[k].max() <= G[k].max() + 1e-14
 
 
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_p5_reflect_ghost_clamps_to_edge_cell(precision):
+    """C-5 reflect ghost (zero gradient, "degrades to value clamping (nearest
+    interior stencil)"; P:146, P:289 walls): between a wall and the first (last) cell
+    centre of an axis the sample equals the value at that centre, i.e. the linear
+    field evaluated at the coordinate clamped to [first centre, last centre].  A
+    periodic-wrap ghost mixes in the opposite edge cell (error ~ slope * L) and a
+    linear-extrapolation ghost keeps the slope (error ~ slope * h / 2): both fail."""
+    mesh = Mesh(dims=(6, 5, 7), origin=(0.25, -1.0, 3.0), cell_size=(0.5, 0.25, 0.125),
+                bc=(oracle.BC_REFLECT,) * 3, chunk_cells=4)
+    sim = Sim(mesh, precision=precision)
+    nx, ny, nz = mesh.dims
+    c = [mesh.origin[a] + (np.arange(mesh.dims[a]) + 0.5) * mesh.cell_size[a] for a in range(3)]
+    slope = (2.0, -3.0, 5.0)
+    F = np.zeros((3, nz, ny, nx))
+    F[0] = slope[0] * c[0][None, None, :] + slope[1] * c[1][None, :, None] + slope[2] * c[2][:, None, None] + 1.0
+    F[1] = -F[0]
+    F[2] = slope[2] * c[2][:, None, None]
+    rng = np.random.default_rng(11)
+    lo = np.array(mesh.origin)
+    hi = lo + np.array(mesh.dims) * np.array(mesh.cell_size)
+    h = np.array(mesh.cell_size)
+    n = 4000
+    x = np.empty((3, n))
+    for a in range(3):
+        # a quarter in each wall band [lo, first centre] / [last centre, hi], half inside
+        band = rng.integers(0, 4, n)
+        x[a] = np.where(band == 0, rng.uniform(lo[a], lo[a] + h[a] / 2, n),
+                        np.where(band == 1, rng.uniform(hi[a] - h[a] / 2, hi[a], n),
+                                 rng.uniform(lo[a] + h[a] / 2, hi[a] - h[a] / 2, n)))
+    x[:, :8] = np.array([lo, hi, [lo[0], hi[1], lo[2]], [hi[0], lo[1], hi[2]],
+                         lo + h / 4, hi - h / 4, [lo[0], c[1][2], c[2][3]], [hi[0], c[1][0], c[2][-1]]]).T
+    real = np.float32 if precision == "f32" else np.float64
+    x = x.astype(real).astype(np.float64)
+    v = sim.interpolate(x, F)
+    xc = np.stack([np.clip(x[a], c[a][0], c[a][-1]) for a in range(3)])
+    want0 = slope[0] * xc[0] + slope[1] * xc[1] + slope[2] * xc[2] + 1.0
+    tol = 1e-12 if precision == "f64" else 3e-5
+    assert np.max(np.abs(v[0] - want0)) < tol * 10
+    assert np.max(np.abs(v[1] + want0)) < tol * 10
+    assert np.max(np.abs(v[2] - slope[2] * xc[2])) < tol * 10
+    # in the x wall bands the x-derivative of the sample is zero (constant along x)
+    near_lo = x[0] < c[0][0]
+    xs = x.copy()
+    xs[0] = np.where(near_lo, lo[0], hi[0])
+    inband = near_lo | (x[0] > c[0][-1])
+    vs = sim.interpolate(xs[:, inband], F)
+    assert np.max(np.abs(vs[0] - v[0][inband])) < tol * 10
+
+
 def test_p5_periodic_wrap_stencil():
     """C-5 periodic ghost: on the face x = lo the sample is the mean of the first and
     last cell (wrap), in the middle of cell 0 it is exactly cell 0's value."""
