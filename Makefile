@@ -10,7 +10,7 @@ CU        := $(SRC)/st_api.cu $(SRC)/st_comm.cu $(SRC)/k_advance.cu $(SRC)/k_fie
              $(SRC)/k_step.cu $(SRC)/st_ec.cu
 HDR       := include/scaletrack.h $(wildcard $(SRC)/*.h) $(wildcard $(SRC)/*.cuh)
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -Iinclude -I$(NCCL_DIR)/include \
+NVFLAGS   := $(ARCH) $(NVFLAGS_EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -Iinclude -I$(NCCL_DIR)/include \
              -Xptxas -v --expt-relaxed-constexpr
 ORACLE    := oracle/liboracle_st.so
 

@@ -78,8 +78,10 @@ enum { ST_ONE_WAY = 0, ST_TWO_WAY = 1 };                        /* P:69 */
  *   drag_law, integrator, coupling : ST_DRAG_*, ST_INT_*, ST_ONE_WAY/ST_TWO_WAY.
  *   rebin_interval (K >= 1) : the store is stable-sorted by chunk after the last
  *                             sub-step of every K-th st_advance call (C-15).
- *   capacity                : maximum particles resident on this rank.
- *   device                  : CUDA ordinal; stream: cudaStream_t (NULL = library's own).
+ *   capacity                : maximum particles resident on this rank (<= 2^31 - 65: the step
+ *                             kernels index the store with 32-bit TMA coordinates).
+ *   device                  : CUDA ordinal; stream: cudaStream_t (NULL = the library creates a
+ *                             BLOCKING stream of its own, ordered with the legacy default stream).
  *   rank, nranks            : position in the one-box job (nranks == 1: single GPU).
  *   nccl_unique_id          : 128-byte ncclUniqueId broadcast by the caller (nranks > 1).
  *   decomposition           : ST_DECOMP_SLAB (default): z-slabs of chunk planes, particles

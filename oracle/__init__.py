@@ -12,6 +12,13 @@ inject -> set fluid field -> advance(dt, nsteps) -> get sources, with
 * the rebin rule C-15: after the last sub-step of every K-th ``advance`` call the
   store is stable-sorted by the bin key (chunk id, cell within the chunk)
   (``orc_bin_key_*`` + ``orc_stable_order``, a counting sort);
+* the far-tail rule C-15b: at a rebin of a store that is already
+  binned (no injection since its last rebin) with 8^3-cell chunks, a particle whose
+  cell is more than one cell (per axis, periodic-aware) from the cell of its home bin
+  (the bin it was sorted into at the previous rebin) is "far"; the sort key is then
+  (bin key, far), i.e. within every bin the near particles in their prior order,
+  then the far ones in their prior order.  In a multi-rank job a far particle whose
+  cell is owned by another rank makes every rank take the plain sort;
 * the R-rank emulation rule C-16: rank r owns chunk planes
   [floor(r*NCz/R), floor((r+1)*NCz/R)); at a rebin every rank keeps its own
   particles in order, appends arrivals in ascending source rank (each in the
@@ -231,6 +238,8 @@ class Sim:
         self.next_id = [0] * self.nranks
         self.M = np.zeros((self.nranks, self.nranks), np.int64)
         self.last_status = 0
+        self.home = [None] * self.nranks    # C-15b: home bin key per particle (None: not binned)
+        self.last_far = 0
 
     # ---- geometry (C-6, C-14, C-16) ----
     def plane_range(self, r: int) -> tuple:
@@ -291,6 +300,12 @@ class Sim:
         if not (np.all(x >= lo[:, None]) and np.all(x <= hi[:, None])):
             raise ValueError("out of domain")
         s = self.stores[rank]
+        # an injection leaves the store unbinned (every rank of a multi-rank job: the
+        # call is collective); the next rebin is the plain stable sort (C-15b)
+        if self.nranks > 1:
+            self.home = [None] * self.nranks
+        elif n > 0:
+            self.home[rank] = None
         self.stores[rank] = _Store(np.concatenate([s.x, x], 1), np.concatenate([s.u, u], 1),
                                    np.concatenate([s.d, d]), np.concatenate([s.w, w]),
                                    np.concatenate([s.id, ids]))
@@ -316,32 +331,76 @@ class Sim:
         self.last_status = status
         return status
 
+    def home_cell(self, key: np.ndarray) -> np.ndarray:
+        """Cell (x, y, z) of a bin key (C-15: chunk * cc^3 + (lz*cc + ly)*cc + lx)."""
+        cc = int(self.mesh.chunk_cells)
+        ncx, ncy, _ = self.mesh.nchunk
+        key = np.asarray(key, np.int64)
+        chunk, local = key // cc ** 3, key % cc ** 3
+        kx, ky, kz = chunk % ncx, (chunk // ncx) % ncy, chunk // (ncx * ncy)
+        lx, ly, lz = local % cc, (local // cc) % cc, local // (cc * cc)
+        return np.stack([kx * cc + lx, ky * cc + ly, kz * cc + lz])
+
+    def far_mask(self, home_key: np.ndarray, x: np.ndarray) -> np.ndarray:
+        """C-15b: the particle's current cell is more than one cell from its home bin's
+        cell along some axis (periodic axes: the shorter way round when n >= 3)."""
+        nx, ny, _ = self.mesh.dims
+        cell, _ = self.locate(x)
+        cell = cell.astype(np.int64)
+        cur = np.stack([cell % nx, (cell // nx) % ny, cell // (nx * ny)])
+        hc = self.home_cell(home_key)
+        far = np.zeros(cell.shape, bool)
+        for a in range(3):
+            n = int(self.mesh.dims[a])
+            d = cur[a] - hc[a]
+            if self.mesh.bc[a] == BC_PERIODIC and n >= 3:
+                d = np.where(d == n - 1, -1, np.where(d == -(n - 1), 1, d))
+            far |= np.abs(d) > 1
+        return far
+
     def rebin(self):
-        """C-15 / C-16: migrate to owners, then stable sort by bin key on every rank."""
+        """C-15 / C-15b / C-16: migrate to owners, then stable sort on every rank by the
+        bin key (plain), or by (bin key, far) when the store was binned (C-15b)."""
         R = self.nranks
         M = np.zeros((R, R), np.int64)
         parts = [[None] * R for _ in range(R)]   # parts[src][dst] = index array in src order
+        owners, fars = [], []
         for src, s in enumerate(self.stores):
             _, chunk = self.locate(s.x)
             own = self.owner_of_chunk(chunk.astype(np.int64))
+            owners.append(own)
             for dst in range(R):
                 idx = np.nonzero(own == dst)[0]
                 parts[src][dst] = idx
                 M[src, dst] = idx.size
-        new = []
+        # C-15b applies when every rank's store is binned and no far particle leaves its rank
+        fused = int(self.mesh.chunk_cells) == 8 and all(h is not None for h in self.home)
+        if fused:
+            for src, s in enumerate(self.stores):
+                f = self.far_mask(self.home[src], s.x) if s.n else np.zeros(0, bool)
+                fars.append(f)
+                if np.any(f & (owners[src] != src)):
+                    fused = False
+        self.last_far = int(sum(int(f.sum()) for f in fars)) if fused else 0
+        new, homes = [], []
         for dst in range(R):
             order = [dst] + [src for src in range(R) if src != dst]   # kept first, then arrivals by source rank
-            xs, us, ds, ws, ids = [], [], [], [], []
+            xs, us, ds, ws, ids, fs = [], [], [], [], [], []
             for src in order:
                 s, idx = self.stores[src], parts[src][dst]
                 xs.append(s.x[:, idx]); us.append(s.u[:, idx]); ds.append(s.d[idx])
                 ws.append(s.w[idx]); ids.append(s.id[idx])
+                fs.append(fars[src][idx] if fused else np.zeros(idx.size, bool))
             st = _Store(np.concatenate(xs, 1), np.concatenate(us, 1), np.concatenate(ds),
                         np.concatenate(ws), np.concatenate(ids))
-            perm, _ = stable_order(self.bin_key(st.x), self.mesh.n_bins)
+            key = self.bin_key(st.x)
+            far = np.concatenate(fs)
+            perm, _ = stable_order(2 * key + far.astype(np.int64), 2 * self.mesh.n_bins)
             new.append(_Store(np.ascontiguousarray(st.x[:, perm]), np.ascontiguousarray(st.u[:, perm]),
                               st.d[perm].copy(), st.w[perm].copy(), st.id[perm].copy()))
+            homes.append(key[perm])
         self.stores = new
+        self.home = homes
         self.M = M
 
     def get_sources(self):

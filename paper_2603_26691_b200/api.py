@@ -29,6 +29,31 @@ def _ptr(a):
     raise TypeError(f"unsupported array type {type(a)}")
 
 
+def _numel(a) -> int:
+    if a is None:
+        return 0
+    return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
+
+
+def _need(a, n: int, what: str):
+    """The C side copies fixed sizes: a wrong shape would read or write out of bounds."""
+    if a is not None and _numel(a) != n:
+        raise ValueError(f"{what}: expected {n} elements, got {_numel(a)}")
+
+
+def _default_stream(device: int):
+    """torch's current stream on `device` (None for the legacy default stream, which the
+    library orders against by creating a blocking stream of its own)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            h = torch.cuda.current_stream(device).cuda_stream
+            return h or None
+    except Exception:
+        pass
+    return None
+
+
 def _as_f32(a):
     if a is None:
         return None
@@ -132,6 +157,8 @@ class ScaleTrack:
     def __init__(self, cfg: Config, stream=None, unique_id: bytes | None = None):
         self.lib = N.load()
         self.cfg = cfg
+        if stream is None:
+            stream = _default_stream(int(cfg.device))
         c = cfg.to_c(stream=stream)
         self._uid = None
         if unique_id is not None:
@@ -161,8 +188,13 @@ class ScaleTrack:
             raise N.StError(rc, self.lib.st_last_error(self.h).decode())
 
     # -- st_* --
+    def _owned_cells(self) -> int:
+        nx, ny, _ = self.cfg.dims
+        return int(nx) * int(ny) * int(self.layout.z1 - self.layout.z0)
+
     def set_fluid_field(self, u):
         u = _as_f32(u)
+        _need(u, 3 * self._owned_cells(), "set_fluid_field u [3][z1-z0][ny][nx]")
         self._check(self.lib.st_set_fluid_field(self.h, _ptr(u)))
         self._keep = u   # device inputs stay alive until stream-ordered consumption
 
@@ -171,6 +203,10 @@ class ScaleTrack:
         n = int(d.shape[0])
         if ids is not None and isinstance(ids, np.ndarray):
             ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        _need(x, 3 * n, "inject x [3][n]")
+        _need(u, 3 * n, "inject u [3][n]")
+        _need(w, n, "inject w [n]")
+        _need(ids, n, "inject ids [n]")
         self._check(self.lib.st_inject(self.h, n, _ptr(x), _ptr(u), _ptr(d), _ptr(w), _ptr(ids)))
 
     def advance(self, dt: float, nsteps: int = 1):
@@ -181,6 +217,7 @@ class ScaleTrack:
         if out is None:
             nx, ny, _ = self.cfg.dims
             out = np.empty((3, self.layout.z1 - self.layout.z0, ny, nx), np.float32)
+        _need(out, 3 * self._owned_cells(), "get_sources out [3][z1-z0][ny][nx]")
         T = ctypes.c_double()
         self._check(self.lib.st_get_sources(self.h, _ptr(out), ctypes.byref(T)))
         return out, T.value
@@ -192,6 +229,7 @@ class ScaleTrack:
         if out is None:
             nx, ny, _ = self.cfg.dims
             out = np.empty((3, self.layout.z1 - self.layout.z0, ny, nx), np.float32)
+        _need(out, 3 * self._owned_cells(), "wait_sources out [3][z1-z0][ny][nx]")
         T = ctypes.c_double()
         self._check(self.lib.st_wait_sources(self.h, _ptr(out), ctypes.byref(T)))
         return out, T.value
@@ -218,6 +256,7 @@ class ScaleTrack:
     def locate(self, x):
         x = _as_f32(x)
         n = int(x.shape[1])
+        _need(x, 3 * n, "locate x [3][n]")
         cell = np.empty(n, np.int32)
         chunk = np.empty(n, np.int32)
         self._check(self.lib.st_locate(self.h, n, _ptr(x), _ptr(cell), _ptr(chunk)))
@@ -286,6 +325,7 @@ class Extrapolator:
                 raise ValueError(f"received must hold k*n = {k}*{self.n} values")
         if out is None:
             out = np.empty(self.n, dtype=np.float32)
+        _need(out, self.n, "Extrapolator.step out [n]")
         self._check(self.lib.st_ec_step(self.h, k, _ptr(received) if k else None, float(dt_ratio), _ptr(out)))
         return out
 
@@ -353,6 +393,10 @@ def micro_advance(cfg: MicroConfig, x, u, d, T, w, F, dt: float, nsteps: int, ac
     fp32, acc [5, nz, ny, nx] fp64 (added to).  Returns the number of mass-floor clamps."""
     lib = N.load()
     n = int(d.shape[0])
+    ncell = int(cfg.dims[0]) * int(cfg.dims[1]) * int(cfg.dims[2])
+    for a, k, what in ((x, 3 * n, "x"), (u, 3 * n, "u"), (T, n, "T"), (w, n, "w"), (F, 5 * ncell, "F"),
+                       (acc, 5 * ncell, "acc")):
+        _need(a, k, f"micro_advance {what}")
     c = cfg.to_c()
     nc = ctypes.c_int64()
     rc = lib.st_micro_advance(ctypes.byref(c), n, _ptr(x), _ptr(u), _ptr(d), _ptr(T), _ptr(w), _ptr(F),

@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(32 * pwarps(SCATTER && ADVANCE), (SCATTER && A
           const int kz = c2 >> SH;
           if (a.far_cur && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
             fdest = (long long)atomicAdd(a.far_cur + bin_of_cell<SH>(g, a.bg, c0, c1, c2), 1ULL);
+            a.far_src[fdest] = (int32_t)(p0 + r);   // prior index: k_far_order sorts the tail by it
           } else {
             flags |= ERRF_SCATTER;
             write_ok = false;

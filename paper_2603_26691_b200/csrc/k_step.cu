@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
 }
 
 #include "k_pstep.cuh"
+#include "k_ip.cuh"
 
 // ---------------------------------------------------------------- rebin preparation
 // Per destination bin d: sources s = d - delta over the 27 deltas (canonical,
@@ -575,22 +576,71 @@ __global__ void k_dbase(Geom g, BinGeom bg, int nbins, const int* __restrict__ b
   }
 }
 
-// Arrival counts from the neighbours land after the local particles of the
-// boundary-plane bins (C-16: kept first, then arrivals).
+// Arrival counts from the neighbours land after the local runs of the boundary-plane
+// bins and before their far tails: one layout per bin, runs | arrivals | far tail
+// (C-16: kept first, then arrivals; C-15b: far last).  new_cnt[d] already counts the
+// far particles (k_rebin_prep), so the arrivals start at new_cnt - far_cnt.
 __global__ void k_vcombine(Geom g, BinGeom bg, uint32_t* __restrict__ new_cnt, const uint32_t* __restrict__ rcnt_dn,
                            const uint32_t* __restrict__ rcnt_up, uint32_t* __restrict__ kept_dn,
-                           uint32_t* __restrict__ kept_up, int oz0, int oz1) {
+                           uint32_t* __restrict__ kept_up, int oz0, int oz1, const int* __restrict__ far_cnt) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= bg.nvb) return;
   int x, y;
   cell_of_vbin(g, v, x, y);
   if (x >= g.n[0] || y >= g.n[1]) return;
   const int db = bin_of_cell<0>(g, bg, x, y, oz0);
-  kept_dn[v] = new_cnt[db];
+  kept_dn[v] = new_cnt[db] - (far_cnt ? (uint32_t)far_cnt[db] : 0u);
   new_cnt[db] += rcnt_dn[v];
   const int dt = bin_of_cell<0>(g, bg, x, y, oz1 - 1);
-  kept_up[v] = new_cnt[dt];
+  kept_up[v] = new_cnt[dt] - (far_cnt ? (uint32_t)far_cnt[dt] : 0u);
   new_cnt[dt] += rcnt_up[v];
+}
+
+// C-15b, deterministic: the fused scatter placed bin d's F far particles in the last F
+// slots of d in atomic order and recorded each one's old-layout index in far_src; one
+// thread per bin sorts that tail by it (insertion sort, payload moved with the key), so
+// the far tail is in prior store order — the (bin, far)-stable sort of the oracle.
+__global__ void k_far_order(int nbins, const int* __restrict__ far_cnt, const int64_t* __restrict__ off_new,
+                            int32_t* __restrict__ far_src, Store B, int64_t cap) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= nbins) return;
+  const int F = far_cnt[d];
+  if (F < 2) return;
+  const int64_t t0 = off_new[d + 1] - F;
+  for (int i = 1; i < F; ++i) {
+    const int32_t key = far_src[t0 + i];
+    float v[8];
+    for (int a = 0; a < 3; ++a) {
+      v[a] = B.x[a * cap + t0 + i];
+      v[3 + a] = B.u[a * cap + t0 + i];
+    }
+    v[6] = B.d[t0 + i];
+    v[7] = B.w[t0 + i];
+    const uint64_t id = B.id[t0 + i];
+    int j = i - 1;
+    for (; j >= 0 && far_src[t0 + j] > key; --j) {
+      const int64_t s = t0 + j, t = s + 1;
+      far_src[t] = far_src[s];
+      for (int a = 0; a < 3; ++a) {
+        B.x[a * cap + t] = B.x[a * cap + s];
+        B.u[a * cap + t] = B.u[a * cap + s];
+      }
+      B.d[t] = B.d[s];
+      B.w[t] = B.w[s];
+      B.id[t] = B.id[s];
+    }
+    const int64_t t = t0 + j + 1;
+    if (t != t0 + i) {
+      far_src[t] = key;
+      for (int a = 0; a < 3; ++a) {
+        B.x[a * cap + t] = v[a];
+        B.u[a * cap + t] = v[3 + a];
+      }
+      B.d[t] = v[6];
+      B.w[t] = v[7];
+      B.id[t] = id;
+    }
+  }
 }
 
 // Insert the arrivals of one side into B and count their slots for the next rebin.
@@ -809,9 +859,11 @@ int launch_pspec(const StepArgs& a, cudaStream_t s) {
   }
 }
 
-// Performance ablation (ST_ABLATE env var, benchmarking only; results are wrong):
-// FEAT bits 1 physics, 2 field gather, 4 deposit, 16 stores (only in the single-rank,
+// Performance ablation (benchmarking builds only: results are wrong).  Compiled in only
+// with -DST_ABLATION_BUILD (scripts/gpu_ablate.sh); the product library never reads the
+// environment.  FEAT bits 1 physics, 2 field gather, 4 deposit, 16 stores (single-rank,
 // one-sub-step, reflecting-wall specialisation).
+#ifdef ST_ABLATION_BUILD
 int ablate_mask() {
   static int m = -2;
   if (m == -2) {
@@ -820,12 +872,14 @@ int ablate_mask() {
   }
   return m;
 }
+#endif
 
 template <bool S, bool A>
 int launch_mode(const StepArgs& a, cudaStream_t s) {
   const int bcm = (a.g.bc[0] == ST_BC_PERIODIC ? 1 : 0) | (a.g.bc[1] == ST_BC_PERIODIC ? 2 : 0) |
                   (a.g.bc[2] == ST_BC_PERIODIC ? 4 : 0);
   if (a.g.cc == 8) {   // chunk-row items with the staged fluid box (k_pstep.cuh)
+#ifdef ST_ABLATION_BUILD
     if (S && A && bcm == 0 && a.bg.nvb == 0 && a.nsteps == 1 && ablate_mask() >= 0) {
       switch (ablate_mask()) {
         case 29: return launch_pvariant<S, A, 0, 0, 29>(a, s);   // no field gather
@@ -837,6 +891,17 @@ int launch_mode(const StepArgs& a, cudaStream_t s) {
         default: break;
       }
     }
+#endif
+#ifndef ST_OLD_INPLACE
+    if (!S && A) {   // in place: the two-particles-per-lane kernel (k_ip.cuh)
+      switch (bcm) {
+        case 0: return launch_ip<0>(a, s);
+        case 7: return launch_ip<7>(a, s);
+        case 3: return launch_ip<3>(a, s);
+        default: return launch_ip<-1>(a, s);
+      }
+    }
+#endif
     switch (bcm) {
       case 0: return launch_pspec<S, A, 0>(a, s);
       case 7: return launch_pspec<S, A, 7>(a, s);
@@ -863,9 +928,16 @@ int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t*
 }
 
 int launch_vcombine(const Geom& g, const BinGeom& bg, uint32_t* new_cnt, const uint32_t* rcnt_dn, const uint32_t* rcnt_up,
-                    uint32_t* kept_dn, uint32_t* kept_up, int oz0, int oz1, cudaStream_t s) {
+                    uint32_t* kept_dn, uint32_t* kept_up, int oz0, int oz1, const int* far_cnt, cudaStream_t s) {
   if (bg.nvb <= 0) return 0;
-  k_vcombine<<<blocks_for(bg.nvb), 256, 0, s>>>(g, bg, new_cnt, rcnt_dn, rcnt_up, kept_dn, kept_up, oz0, oz1);
+  k_vcombine<<<blocks_for(bg.nvb), 256, 0, s>>>(g, bg, new_cnt, rcnt_dn, rcnt_up, kept_dn, kept_up, oz0, oz1, far_cnt);
+  return 1;
+}
+
+int launch_far_order(const BinGeom& bg, const int* far_cnt, const int64_t* off_new, const int32_t* far_src, Store B,
+                     int64_t cap, cudaStream_t s) {
+  if (!far_cnt || !far_src || bg.nbins <= 0) return 0;
+  k_far_order<<<blocks_for(bg.nbins), 256, 0, s>>>(bg.nbins, far_cnt, off_new, const_cast<int32_t*>(far_src), B, cap);
   return 1;
 }
 

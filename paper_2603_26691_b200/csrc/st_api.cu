@@ -43,6 +43,7 @@ struct st_ctx {
   Store S[2];
   int cur = 0;
   CUtensorMap tmap[4];        // [2 stores][float rows, ids] TMA descriptors (kernel parameters)
+  CUtensorMap tmap_ip[2];     // [2 stores] float rows with the {68, 8} box of k_ip
   CUtensorMap tmap_win[2][2]; // [field buffer][window shape] TMA descriptors of the fluid field
   long long* dtab = nullptr;  // [nbins][27] destination table of the fused scatter (k_dbase)
   int* far_cnt = nullptr;     // [nbins] far particles per destination bin (C-15b; k_count)
@@ -267,6 +268,8 @@ static st_status validate(const st_config* c, std::string& why) {
       c->coupling > 1) { why = "bad enum"; return ST_ERR_INVALID_ARG; }
   if (c->rebin_interval < 1) { why = "rebin_interval must be >= 1"; return ST_ERR_INVALID_ARG; }
   if (c->capacity < 0) { why = "capacity must be >= 0"; return ST_ERR_INVALID_ARG; }
+  // TMA box coordinates, store slots and far-tail indices are 32-bit in the step kernels
+  if (c->capacity > (int64_t)INT32_MAX - 64) { why = "capacity must be <= 2^31 - 65 (32-bit store indices)"; return ST_ERR_INVALID_ARG; }
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) { why = "bad rank/nranks"; return ST_ERR_INVALID_ARG; }
   const int ncz = (c->dims[2] + c->chunk_cells - 1) / c->chunk_cells;
   if (c->nranks > ncz) { why = "need at least one chunk plane per rank"; return ST_ERR_INVALID_ARG; }
@@ -391,6 +394,11 @@ static st_status make_tensor_maps(st_ctx* c) {
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(c, ST_ERR_CUDA, "tensor map (float rows) encode failed: " + std::to_string((int)r));
+    const cuuint32_t boxf64[2] = {68, 8};                // k_ip.cuh kIpBoxF
+    r = encode(&c->tmap_ip[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, c->S[i].x, dimf, stridef, boxf64, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, ST_ERR_CUDA, "tensor map (float rows, 64) encode failed: " + std::to_string((int)r));
     const cuuint64_t dimi[2] = {(cuuint64_t)c->cap, 1};
     const cuuint64_t stridei[1] = {(cuuint64_t)c->cap * sizeof(uint64_t)};
     const cuuint32_t boxi[2] = {34, 1};                    // k_pstep.cuh kBoxI
@@ -428,7 +436,9 @@ static st_status init_impl(st_ctx* c) {
   if (c->cfg.stream) {
     c->cs = (cudaStream_t)c->cfg.stream;
   } else {
-    ST_CUDA(c, cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+    // no stream given: a BLOCKING stream, so device inputs produced on the legacy
+    // default stream (torch's default) are ordered before the library reads them
+    ST_CUDA(c, cudaStreamCreateWithFlags(&c->cs, cudaStreamDefault));
     c->own_cs = true;
   }
   ST_CUDA(c, cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking));
@@ -750,10 +760,12 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.B = c->S[1 - c->cur];
   a.tm_f = c->tmap[2 * c->cur];
   a.tm_id = c->tmap[2 * c->cur + 1];
+  a.tm_f64 = c->tmap_ip[c->cur];
   a.tm_win[0] = c->tmap_win[c->front < 0 ? 0 : c->front][0];
   a.tm_win[1] = c->tmap_win[c->front < 0 ? 0 : c->front][1];
   a.dtab = c->dtab;
   a.far_cur = c->far_cur;
+  a.far_src = c->key[0];      // the radix keys are free outside the general sort
   a.cap = c->cap;
   a.n = c->n;
   a.off = c->off[c->lay];
@@ -883,6 +895,18 @@ static st_status count_slots(st_ctx* c, bool* far) {
   return ST_OK;
 }
 
+// Bitwise-OR-agree an error flag over all ranks (NCCL max of each bit pattern's
+// disjoint flags is their OR for the small flags used here); host-blocking.
+static st_status agree_flags(st_ctx* c, int* flags) {
+  if (!c->comm) return ST_OK;
+  std::string why;
+  ST_CUDA(c, cudaMemcpyAsync(c->d_farg, flags, sizeof(int), cudaMemcpyHostToDevice, c->cs));
+  if (comm_allreduce_max_i32(c->comm, c->d_farg, 1, c->cs, why)) return fail(c, ST_ERR_NCCL, why);
+  ST_CUDA(c, cudaMemcpyAsync(flags, c->d_farg, sizeof(int), cudaMemcpyDeviceToHost, c->cs));
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  return ST_OK;
+}
+
 // Neighbour-slot scatter from the current layout into the other buffer; fused
 // with the advance when `advance` (the field/accumulator must be set up).
 // nranks > 1: the movers into the neighbour planes are scattered into send
@@ -905,7 +929,8 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     if (comm_rebin_counts(c->comm, c->new_cnt + nb, c->new_cnt + nb + nv, c->rcnt[0], c->rcnt[1], nv, c->d_farg,
                           g.bc[2] == ST_BC_PERIODIC, c->cs, why))
       return fail(c, ST_ERR_NCCL, why);
-    nl += launch_vcombine(g, c->bg, c->new_cnt, c->rcnt[0], c->rcnt[1], c->kept[0], c->kept[1], c->z0, c->z1, c->cs);
+    nl += launch_vcombine(g, c->bg, c->new_cnt, c->rcnt[0], c->rcnt[1], c->kept[0], c->kept[1], c->z0, c->z1,
+                          c->far_cnt, c->cs);
     nl += launch_exclusive_scan_u32(c->new_cnt + nb, nv, c->voff[0], c->sc.partial, c->cs);
     nl += launch_exclusive_scan_u32(c->new_cnt + nb + nv, nv, c->voff[1], c->sc.partial, c->cs);
     nl += launch_exclusive_scan_u32(c->rcnt[0], nv, c->roff[0], c->sc.partial, c->cs);
@@ -933,10 +958,16 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
       *fell_back = true;
       return general_rebin(c);
     }
+    int bad = 0;
     for (int k = 0; k < 4; ++k)
-      if (c->h_tot[k] > c->scap) return fail(c, ST_ERR_CAPACITY, "migration buffer too small (more movers than cap/16)");
+      if (c->h_tot[k] > c->scap) bad |= 1;
     n_new = c->n - c->h_tot[0] - c->h_tot[1] + c->h_tot[2] + c->h_tot[3];
-    if (n_new > c->cfg.capacity) return fail(c, ST_ERR_CAPACITY, "migration would exceed the store capacity");
+    if (n_new > c->cfg.capacity) bad |= 2;
+    // every rank must take the same branch before the payload exchange (else the ranks
+    // that did not fail would wait in ncclSend/Recv for ones that returned)
+    if ((s = agree_flags(c, &bad))) return s;
+    if (bad & 1) return fail(c, ST_ERR_CAPACITY, "migration buffer too small (more movers than cap/16) on some rank");
+    if (bad & 2) return fail(c, ST_ERR_CAPACITY, "migration would exceed the store capacity on some rank");
   }
   StepArgs a = step_args(c, dt, nsteps);
   a.n = n_new;
@@ -980,6 +1011,10 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   } else {
     c->mig_row[0] = c->n;
   }
+  // C-15b: far tails into prior store order (after the arrivals: they precede the tail)
+  if ((s = check_launch(c, launch_far_order(c->bg, c->far_cnt, c->off[nlay], c->key[0], c->S[1 - c->cur], c->cap,
+                                            c->cs))))
+    return s;
   if (advance) {
     ST_CUDA(c, cudaEventRecord(c->t_adv1, c->cs));
     c->timed_adv = true;

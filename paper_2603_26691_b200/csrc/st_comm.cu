@@ -24,6 +24,7 @@ struct Comm {
   int64_t* d_counts = nullptr;  // [nranks * nranks]
   int64_t* d_bounds = nullptr;  // [nranks + 1]
   int32_t* d_bases = nullptr;   // [nranks + 1]
+  int* d_flag = nullptr;        // agreed error flag of comm_migrate
 };
 
 namespace {
@@ -110,7 +111,8 @@ Comm* comm_create(const void* unique_id, int rank, int nranks, const int32_t* sl
       cudaEventCreateWithFlags(&c->e_out, cudaEventDisableTiming) != cudaSuccess ||
       cudaMalloc(&c->d_counts, sizeof(int64_t) * nranks * nranks) != cudaSuccess ||
       cudaMalloc(&c->d_bounds, sizeof(int64_t) * (nranks + 1)) != cudaSuccess ||
-      cudaMalloc(&c->d_bases, sizeof(int32_t) * (nranks + 1)) != cudaSuccess) {
+      cudaMalloc(&c->d_bases, sizeof(int32_t) * (nranks + 1)) != cudaSuccess ||
+      cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess) {
     why = "comm_create: CUDA allocation failed";
     comm_destroy(c);
     return nullptr;
@@ -129,6 +131,7 @@ void comm_destroy(Comm* c) {
   cudaFree(c->d_counts);
   cudaFree(c->d_bounds);
   cudaFree(c->d_bases);
+  cudaFree(c->d_flag);
   delete c;
 }
 
@@ -227,9 +230,19 @@ int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int6
   int64_t total = M[(size_t)r * G + r];
   for (int src = 0; src < G; ++src)
     if (src != r) total += M[(size_t)src * G + r];
-  if (total > cap) {
-    why = "migration would exceed the store capacity";
-    return 3;
+  {
+    // agree on the capacity check before any payload moves (a rank that returned alone
+    // would leave the others waiting in the grouped send/recv)
+    int bad = total > cap ? 1 : 0;
+    CUCK(cudaMemcpyAsync(c->d_flag, &bad, sizeof(int), cudaMemcpyHostToDevice, c->ns), why);
+    NCCK(ncclAllReduce(c->d_flag, c->d_flag, 1, ncclInt32, ncclMax, c->nc, c->ns), why);
+    CUCK(cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->ns), why);
+    CUCK(cudaStreamSynchronize(c->ns), why);
+    if (bad) {
+      join_out(c, s, why);
+      why = total > cap ? "migration would exceed the store capacity" : "migration would exceed the store capacity on another rank";
+      return 3;
+    }
   }
   const int o = 1 - *cur;
   Store A = S[*cur], B = S[o];

@@ -32,6 +32,7 @@ struct StepArgs {
   Store A, B;                 // input layout / output layout (scatter)
   CUtensorMap tm_f;           // TMA tensor map of A's float rows (2-D {cap, 8}; k_pstep)
   CUtensorMap tm_id;          // TMA tensor map of A's ids (2-D {cap, 1}; k_pstep)
+  CUtensorMap tm_f64;         // TMA tensor map of A's float rows, box {68, 8} (k_ip: 64-particle batches)
   CUtensorMap tm_win[2];      // TMA maps of the front fluid field, window boxes of k_pstep:
                               // [0] 10x3x3 cells (in place), [1] 12x5x5 cells (fused scatter)
   int64_t cap, n;
@@ -40,6 +41,8 @@ struct StepArgs {
   const int* slot_base;       // [27][nbins] base[j][s] (scatter; rebin_prep output; k_step)
   const long long* dtab;      // [nbins][27] destination table (scatter; k_dbase output; k_pstep)
   unsigned long long* far_cur;// [nbins] next free slot of each bin's far tail (C-15b), or NULL
+  int32_t* far_src;           // [cap] by new-layout slot: old-layout index of a far particle
+                              // (k_far_order sorts each tail by it: prior order, C-15b)
   // slot histogram produced by an in-place step whose call makes a rebin due (k_count's
   // outputs, same meaning; cnt_hist == NULL: not produced by this launch)
   int* cnt_hist;
@@ -63,7 +66,11 @@ struct StepArgs {
 
 // Multi-GPU rebin helpers (k_step.cu)
 int launch_vcombine(const Geom& g, const BinGeom& bg, uint32_t* new_cnt, const uint32_t* rcnt_dn,
-                    const uint32_t* rcnt_up, uint32_t* kept_dn, uint32_t* kept_up, int oz0, int oz1, cudaStream_t s);
+                    const uint32_t* rcnt_up, uint32_t* kept_dn, uint32_t* kept_up, int oz0, int oz1,
+                    const int* far_cnt, cudaStream_t s);
+// C-15b: sort every bin's far tail of the new layout B by the old-layout index (far_src)
+int launch_far_order(const BinGeom& bg, const int* far_cnt, const int64_t* off_new, const int32_t* far_src, Store B,
+                     int64_t cap, cudaStream_t s);
 struct InsertArgs {
   Geom g;
   BinGeom bg;

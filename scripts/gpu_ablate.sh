@@ -1,5 +1,6 @@
 #!/bin/bash
 # Step-kernel ablation on C5 (K=1 fused): which stage costs what.
+# Needs the ablation build: make clean && make NVFLAGS_EXTRA=-DST_ABLATION_BUILD (never ship it).
 NP=${1:-1e9}
 for M in ${MODES:--1 29 27 30 16}; do
   ST_ABLATE=$M timeout 600 python bench.py --particles $NP --steps 4 --warmup 2 --no-cpu-baseline --no-e2e --rebin-interval 1 \

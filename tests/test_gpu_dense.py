@@ -1,0 +1,209 @@
+"""GPU vs oracle in the DENSE-BIN regime the bench runs in (C5: ~377 particles per cell).
+
+At this density a warp's 32 particles nearly always share one bin, so the paths that
+only trigger there are exercised: a lane keeps its bin across batches and integrates
+many deposits in registers before one reduction (k_pstep stayer accumulators), bins
+span several 32-particle batches (carried stayer ranks of the fused scatter), and the
+per-bin run tables are long.  Bars (BASELINE.json north_star):
+  * x within 1e-5 of L, u within 1e-5 of U_max after free-running calls, sources
+    within 1e-5 relative L2 every call (fp32-state oracle);
+  * the order produced by the FUSED scatter + advance launch is bit-exact given the
+    GPU's own positions (C-15 / C-15b), checked through the launch itself.
+
+The fused launch's order is observed without a flush in between: the call that runs
+the fused rebin uses dt = 1e-9 s, so its advance moves no particle by even one fp32 ulp
+(|u| dt ~ 3e-10 m << ulp(1.0) = 1.2e-7 m; the domain starts at 1.0 m for that reason)
+and the observed positions are exactly the ones the rebin sorted by."""
+import numpy as np
+import pytest
+
+import synth
+from tests.conftest import gpu_available
+from tests.helpers import by_id, gpu_config, oracle_sim
+
+pytestmark = pytest.mark.gpu
+
+if not gpu_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from paper_2603_26691_b200 import ScaleTrack  # noqa: E402
+
+import oracle  # noqa: E402
+
+N_DENSE = 5_000_000          # 24^3 cells -> 362 particles per cell
+
+
+def _dense_workload(n=N_DENSE):
+    wl = synth.workload("C5", n_particles=n)
+    wl.dims, wl.origin = (24, 24, 24), (1.0, 1.0, 1.0)
+    return wl
+
+
+def _setup(wl, K):
+    lo, hi = synth.domain_box(wl)
+    x, u, d, w = synth.particles_np(wl.n_particles, lo, hi, wl.d_range, wl.d_dist, wl.w, 31)
+    F = synth.make_field(wl)
+    g = ScaleTrack(gpu_config(wl, capacity=wl.n_particles, rebin_interval=K))
+    o = oracle_sim(wl, "f32", K, 0)
+    for s in (g, o):
+        s.inject(x, u, d, w)
+        s.set_fluid_field(F)
+    return g, o, F
+
+
+@pytest.mark.parametrize("K", [1, 2])
+def test_dense_bins_free_running(K):
+    """6 free-running calls at ~362 particles/cell: x and u against the oracle.  (The
+    per-cell sources are compared for the same particle state below: free-running fp32
+    trajectories differ in the last bit, and the rare particle that then starts a
+    sub-step on the other side of a face moves its whole NGP deposit to the neighbour
+    cell — a discontinuity of the method, not of the kernel; SURVEY §8(c4) "drive both
+    sides with the same field each step so the comparison measures the step".)"""
+    wl = _dense_workload()
+    g, o, F = _setup(wl, K)
+    U = float(np.max(np.linalg.norm(F.reshape(3, -1), axis=0)))
+    for _ in range(6):
+        g.advance(wl.dt, 1)
+        o.advance(wl.dt, 1)
+    st = g.stats()
+    assert st["fused_rebins"] >= (4 if K == 1 else 2), st
+    a, b = by_id(g.get_particles()), by_id(o.particles())
+    assert np.array_equal(a["id"], b["id"])
+    L = np.array(wl.lengths)[:, None]
+    pos = float(np.max(np.abs(a["x"].astype(np.float64) - b["x"]) / L))
+    vel = float(np.max(np.abs(a["u"].astype(np.float64) - b["u"])) / U)
+    assert pos <= 1e-5, pos
+    assert vel <= 1e-5, vel
+
+
+def _restart_oracle(wl, K, P, F):
+    o = oracle_sim(wl, "f32", K, 0)
+    o.inject(P["x"], P["u"], P["d"], P["w"], P["id"])
+    o.set_fluid_field(F)
+    return o
+
+
+def _rel_l2(Sg, So):
+    return float(np.linalg.norm(Sg.astype(np.float64) - So) / np.linalg.norm(So))
+
+
+@pytest.mark.parametrize("K", [1, 2])
+def test_dense_sources_same_state(K):
+    """Per-cell sources within 1e-5 relative L2 at ~362 particles/cell, for the same
+    particle state, through BOTH step kernels: the fused scatter + advance launch and
+    the in-place launch.  The state the fused call starts from is pinned without a flush:
+    the calls before it use dt = 1e-9 s, which moves no position (module docstring) and
+    changes u by ~1e-6 relative, identically on both sides to fp32 rounding."""
+    wl = _dense_workload()
+    g, _, F = _setup(wl, K)
+    tiny = 1e-9
+    if K == 1:
+        g.advance(tiny, 1)                      # general rebin now; no rebin pending
+        A = g.get_particles()
+        g.get_sources()
+        g.advance(tiny, 1)                      # in place + slot count; rebin due
+        g.advance(wl.dt, 1)                     # FUSED rebin + advance
+    else:
+        g.advance(wl.dt, 1)
+        g.advance(tiny, 1)                      # general rebin of call-1 positions
+        g.advance(tiny, 1)                      # in place; no rebin pending
+        A = g.get_particles()
+        g.get_sources()
+        g.advance(tiny, 1)                      # in place + slot count; rebin due
+        g.advance(wl.dt, 1)                     # FUSED rebin + advance
+    f0 = g.stats()["fused_rebins"]
+    Sg, Tg = g.get_sources()
+    o = _restart_oracle(wl, K, A, F)
+    o.advance(tiny, 1)
+    o.advance(wl.dt, 1)
+    So, To = o.get_sources()
+    assert f0 >= 1
+    assert Tg == pytest.approx(To, rel=1e-15)
+    err_fused = _rel_l2(Sg, So)
+    # the in-place launch from an observed state (no rebin pending after an odd call at K = 2;
+    # at K = 1 the observation flushes the pending rebin first, which is the contract)
+    C = g.get_particles()
+    g.advance(wl.dt, 1)
+    Sg2, _ = g.get_sources()
+    o2 = _restart_oracle(wl, K, C, F)
+    o2.advance(wl.dt, 1)
+    So2, _ = o2.get_sources()
+    err_ip = _rel_l2(Sg2, So2)
+    assert err_fused <= 1e-5, err_fused
+    assert err_ip <= 1e-5, err_ip
+
+
+def _expected_order(o, A, B):
+    """The oracle's rebin (C-15 / C-15b) applied to the prior layout A (home bins =
+    bin keys of A's positions) with the positions B holds: ids in the new order."""
+    pos = {int(i): k for k, i in enumerate(A["id"])}
+    idx = np.array([pos[int(i)] for i in B["id"]])
+    X = np.ascontiguousarray(B["x"][:, np.argsort(idx)])     # B's positions in A's order
+    home = o.bin_key(A["x"])
+    far = o.far_mask(home, X)
+    perm, _ = oracle.stable_order(2 * o.bin_key(X) + far.astype(np.int64), 2 * o.mesh.n_bins)
+    return A["id"][perm], int(far.sum())
+
+
+@pytest.mark.parametrize("K", [1, 2])
+def test_dense_fused_rebin_order_bit_exact(K):
+    """The fused scatter + advance launch (k_pstep<1,1>) at ~362 particles/cell puts the
+    store in exactly the oracle's C-15 / C-15b order given the GPU's positions."""
+    wl = _dense_workload()
+    g, o, F = _setup(wl, K)
+    tiny = 1e-9
+    if K == 1:
+        g.advance(tiny, 1)          # unbinned -> general rebin now; nothing moved
+        A = g.get_particles()       # no rebin pending: not a flush
+        g.advance(wl.dt, 1)         # in place (+ slot count); rebin due
+        g.advance(tiny, 1)          # FUSED rebin of that state; the advance moves nothing
+        B = g.get_particles()       # flushes the next rebin, an identity (nothing moved)
+    else:
+        g.advance(wl.dt, 1)
+        g.advance(tiny, 1)          # call 2: general rebin (unbinned) of call-1 positions
+        g.advance(tiny, 1)          # call 3: in place, moves nothing; no rebin due
+        A = g.get_particles()
+        g.advance(wl.dt, 1)         # call 4: in place + slot count; rebin due
+        g.advance(tiny, 1)          # call 5: FUSED rebin; no rebin due after it
+        B = g.get_particles()
+    st = g.stats()
+    assert st["fused_rebins"] >= 1, st
+    want, nfar = _expected_order(o, A, B)
+    assert np.array_equal(B["id"], want)
+    c, k = o.locate(B["x"])
+    assert np.array_equal(B["cell"], c) and np.array_equal(B["chunk"], k)
+    assert st["last_far"] == nfar
+
+
+def test_far_tails_deterministic_order_fused():
+    """C-15b through the fused launch: a fast flow at K = 4 makes particles far (more than
+    one cell from their home bin); the far tails come out in prior store order, equal to
+    the oracle's (bin, far) sort, and two identical runs give identical stores."""
+    wl = synth.workload("C2", n_particles=200_000)
+    wl.origin = (1.0, 1.0, 1.0)
+    K = 4
+    lo, hi = synth.domain_box(wl)
+    x, u, d, w = synth.particles_np(wl.n_particles, lo, hi, wl.d_range, wl.d_dist, wl.w, 5)
+    F = (synth.make_field(wl) * 20.0).astype(np.float32)
+    o = oracle_sim(wl, "f32", K, 0)
+    runs = []
+    for _ in range(2):
+        g = ScaleTrack(gpu_config(wl, capacity=wl.n_particles, rebin_interval=K))
+        g.inject(x, u, d, w)
+        g.set_fluid_field(F)
+        for _ in range(3):
+            g.advance(wl.dt, 1)
+        g.advance(1e-9, 1)          # call 4: general rebin of call-3 positions, nothing moved
+        A = g.get_particles()
+        for _ in range(3):
+            g.advance(wl.dt, 1)     # calls 5-7 in place
+        g.advance(1e-9, 1)          # call 8 in place, counts the slots -> rebin due (K = 4)
+        g.advance(1e-9, 1)          # call 9: FUSED rebin, moves nothing
+        B = g.get_particles()
+        st = g.stats()
+        want, nfar = _expected_order(o, A, B)
+        assert nfar > 100 and st["last_far"] == nfar, (nfar, st["last_far"])
+        assert np.array_equal(B["id"], want)
+        runs.append(B)
+        g.close()
+    assert all(np.array_equal(runs[0][k], runs[1][k]) for k in ("id", "x", "u"))

@@ -632,3 +632,62 @@ def test_p4_deposit_goes_to_start_cell():
     m = np.pi / 6 * RHO_P * d ** 3
     du = p["u"][0, 0] - 1.0
     assert S[0, 2, 2, 1] * T == pytest.approx(-w * m * du, rel=1e-12)
+
+
+# ---------------------------------------------------------------- P-9b far tails (C-15b)
+def _brute_bin_and_cell(mesh, cell):
+    """bin key and (x, y, z) cell from a flat cell id, by plain integer arithmetic."""
+    nx, ny, _ = mesh.dims
+    cc = mesh.chunk_cells
+    ncx, ncy, _ = mesh.nchunk
+    cx, cy, cz = cell % nx, (cell // nx) % ny, cell // (nx * ny)
+    chunk = ((cz // cc) * ncy + cy // cc) * ncx + cx // cc
+    return chunk * cc ** 3 + ((cz % cc) * cc + cy % cc) * cc + cx % cc, (cx, cy, cz)
+
+
+@pytest.mark.parametrize("bc", [oracle.BC_PERIODIC, oracle.BC_REFLECT])
+def test_p9b_far_tail_order_brute_force(bc):
+    """C-15b: at a rebin of a binned store, within each bin the particles
+    within one cell (per axis; periodic the short way round) of their home bin come
+    first in prior order, then the far ones in prior order.  Checked against a
+    pure-Python brute force (per-particle loops, `sorted` on (bin, far, prior index));
+    the first rebin after an injection is the plain stable sort."""
+    mesh = Mesh(dims=(16, 16, 24), cell_size=(1 / 16,) * 3, chunk_cells=8, bc=(bc,) * 3)
+    rng = np.random.default_rng(21)
+    n = 4000
+    sim = Sim(mesh, Physics(coupling=oracle.ONE_WAY, drag_law=oracle.DRAG_STOKES), rebin_interval=1,
+              precision="f32")
+    sim.inject(rng.random((3, n)) * np.array([[1.0], [1.0], [1.5]]), rng.normal(size=(3, n)) * 3.0,
+               np.full(n, 400e-6))                     # ballistic-ish: tau ~ 0.5 s
+    sim.set_fluid_field(np.zeros((3, 24, 16, 16)))
+    sim.advance(1e-3, 1)                               # first rebin: plain stable sort
+    assert sim.last_far == 0
+    P1 = sim.particles()
+    homes = [_brute_bin_and_cell(mesh, int(c)) for c in P1["cell"]]
+    sim.advance(0.03, 1)                               # 3 m/s x 0.03 s ~ 1.4 cells: some far
+    P2 = sim.particles()
+    pos = {int(i): k for k, i in enumerate(P1["id"])}
+    cell2, _ = sim.locate(P2["x"])
+    rows = []
+    for k in range(n):
+        prior = pos[int(P2["id"][k])]
+        b, (cx, cy, cz) = _brute_bin_and_cell(mesh, int(cell2[k]))
+        hx, hy, hz = homes[prior][1]
+        far = False
+        for c, h, m in ((cx, hx, 16), (cy, hy, 16), (cz, hz, 24)):
+            d = c - h
+            if bc == oracle.BC_PERIODIC:
+                d = -1 if d == m - 1 else (1 if d == -(m - 1) else d)
+            far |= abs(d) > 1
+        rows.append((b, far, prior))
+    nfar = sum(r[1] for r in rows)
+    assert 20 < nfar < n - 20, nfar
+    assert sim.last_far == nfar
+    assert rows == sorted(rows)                       # the oracle's order is the brute-force order
+    # a particle injected in between makes the next rebin the plain sort again
+    sim.inject(np.full((3, 1), 0.5), np.zeros((3, 1)), np.full(1, 400e-6))
+    sim.advance(0.03, 1)
+    assert sim.last_far == 0
+    P3 = sim.particles()
+    b3 = sim.bin_key(P3["x"])
+    assert np.all(np.diff(b3) >= 0)
