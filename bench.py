@@ -134,11 +134,7 @@ def algorithmic_bytes_per_update(two_way=True):
 
 
 # ---------------------------------------------------------------- oracle (CPU) legs
-def run_oracle_sample(wl, n_sample, steps, z_range=None, K=4):
-    """Time the oracle (fp32, single-threaded, as it stands) on a bounded sample of the
-    workload: same grid and field recipe, n_sample particles, `steps` calls."""
-    import numpy as np
-
+def _oracle_sim(wl, n_sample, K, F=None):
     import oracle
     import synth
     mesh = oracle.Mesh(dims=wl.dims, origin=wl.origin, cell_size=wl.cell_size, chunk_cells=wl.chunk_cells, bc=wl.bc)
@@ -148,8 +144,17 @@ def run_oracle_sample(wl, n_sample, steps, z_range=None, K=4):
     lo, hi = synth.domain_box(wl)
     x, u, d, w = synth.particles_np(n_sample, lo, hi, wl.d_range, wl.d_dist, wl.w, wl.seed_particles)
     sim.inject(x, u, d, w)
-    F = synth.make_field(wl)
+    F = synth.make_field(wl) if F is None else F
     sim.set_fluid_field(F)
+    return sim, F
+
+
+def run_oracle_sample(wl, n_sample, steps, z_range=None, K=4, F=None, barrier=None):
+    """Time the oracle (fp32, single-threaded, as it stands) on a bounded sample of the
+    workload: same grid and field recipe, n_sample particles, `steps` calls."""
+    sim, F = _oracle_sim(wl, n_sample, K, F)
+    if barrier is not None:
+        barrier.wait()
     t0 = time.perf_counter()
     for _ in range(steps):
         sim.set_fluid_field(F)
@@ -158,15 +163,65 @@ def run_oracle_sample(wl, n_sample, steps, z_range=None, K=4):
     return time.perf_counter() - t0
 
 
+_SHARD = {}
+
+
+def _shard_init(F, barrier):
+    _SHARD["F"], _SHARD["barrier"] = F, barrier
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _oracle_shard(args):
+    """One independent oracle process of the all-core figure: its own
+    shard of particles (seed per shard) on the full grid and field, `steps` calls, timed
+    from a barrier all shards pass together; returns seconds."""
+    name, n, steps, K, shard = args
+    import synth
+    wl = synth.workload(name)
+    wl.seed_particles = 1000 + shard
+    return run_oracle_sample(wl, n, steps, K=K, F=_SHARD["F"], barrier=_SHARD["barrier"])
+
+
 def cpu_baseline(wl, target_s, K):
+    """The oracle as it stands on the host: 1 core (one process), then every core
+    (os.cpu_count() independent processes on disjoint particle shards),
+    each a bounded sample of the workload; pu/s = particles x steps / wall seconds."""
+    import multiprocessing as mp
+
+    import synth
     n = 200_000
-    t1 = run_oracle_sample(wl, n, 1, K=K)
+    F = synth.make_field(wl)
+    t1 = run_oracle_sample(wl, n, 1, K=K, F=F)
     steps = max(1, int(target_s / max(t1, 1e-3)))
     steps = min(steps, 200)
-    t = run_oracle_sample(wl, n, steps, K=K)
-    return {"value": n * steps / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+    t = run_oracle_sample(wl, n, steps, K=K, F=F)
+    cores = os.cpu_count() or 1
+    all_core = None
+    if cores > 1:
+        n_sh = n
+        steps_sh = max(1, min(200, int(0.5 * target_s / max(t1, 1e-3))))
+        ctx = mp.get_context("spawn")
+        barrier = ctx.Barrier(cores)
+        with ctx.Pool(cores, initializer=_shard_init, initargs=(F, barrier)) as pool:
+            ts = pool.map(_oracle_shard, [(wl.name, n_sh, steps_sh, K, k) for k in range(cores)])
+        tw = max(ts)
+        all_core = {"value": cores * n_sh * steps_sh / tw, "cores": cores,
+                    "sample": f"{cores} independent oracle processes x {n_sh} particles x {steps_sh} steps on "
+                              f"disjoint shards, timed from a common barrier, slowest {tw:.1f} s"}
+    return {"value": n * steps / t, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{n} particles x {steps} steps of {wl.name} (full {wl.dims} grid, same field recipe), "
-                      f"fp32 oracle, single-threaded, {t:.1f} s"}
+                      f"fp32 oracle, single-threaded, {t:.1f} s",
+            "all_core": all_core}
 
 
 def bench_config(wl, n_per, K, G, decomp):

@@ -23,7 +23,8 @@
  *   - Array arguments are caller-owned.  Pointers may be host (pageable or
  *     pinned) or device memory of the context's GPU; the kind is detected with
  *     cudaPointerGetAttributes.  Device inputs are consumed in order on
- *     cfg.stream; host inputs are copied before the call returns.
+ *     cfg.stream; host inputs are copied before the call returns, except the
+ *     pinned-host field of st_set_fluid_field (see there).
  *   - Vectors are structure-of-arrays: x[3][n] means x[0..n) = x-components,
  *     x[n..2n) = y, x[2n..3n) = z.  Fields are [3][nz][ny][nx], x fastest.
  *   - Cell linear index: (cz*ny + cy)*nx + cx (global indices).
@@ -161,8 +162,14 @@ st_status st_destroy(st_ctx* ctx);
 /* Fluid state in ("receive the required states").  u = [3][z1-z0][ny][nx]
  * fp32 cell-centre velocities of the cells this rank owns.  Asynchronous: the
  * copy goes into the back buffer on the copy stream (it waits for the last
- * st_advance still reading that buffer); the next st_advance uses it.  With
- * nranks > 1 the halo planes are exchanged with the neighbour ranks (collective). */
+ * st_advance still reading that buffer); the next st_advance uses it.  The copy
+ * stream is not shared with the source readout (st_request_sources), so a field
+ * copy never waits behind a readout that waits for the running step (P:198-202,
+ * field in and sources out overlap the Lagrangian step).  Pageable host u
+ * is consumed before the call returns; PINNED host u (cudaHostAlloc) is copied
+ * asynchronously and must stay unchanged until the next st_set_fluid_field or
+ * st_sync returns (that call waits for the copy).  With nranks > 1 the halo planes
+ * are exchanged with the neighbour ranks (collective). */
 st_status st_set_fluid_field(st_ctx* ctx, const float* u);
 
 /* Append n particles in the given order ("particles are created directly

@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
 
 #include "k_pstep.cuh"
 #include "k_ip.cuh"
+#include "k_fs.cuh"
 
 // ---------------------------------------------------------------- rebin preparation
 // Per destination bin d: sources s = d - delta over the 27 deltas (canonical,
@@ -889,6 +890,16 @@ int launch_mode(const StepArgs& a, cudaStream_t s) {
         case 16: return launch_pvariant<S, A, 0, 0, 16>(a, s);   // loads + scatter stores only
         case 0: return launch_pvariant<S, A, 0, 0, 0>(a, s);  // loads + rank only
         default: break;
+      }
+    }
+#endif
+#ifndef ST_OLD_FUSED
+    if (S && A) {    // fused rebin scatter + advance: two particles per lane (k_fs.cuh)
+      switch (bcm) {
+        case 0: return launch_fs<0>(a, s);
+        case 7: return launch_fs<7>(a, s);
+        case 3: return launch_fs<3>(a, s);
+        default: return launch_fs<-1>(a, s);
       }
     }
 #endif

@@ -36,14 +36,19 @@ struct st_ctx {
   // streams
   cudaStream_t cs = nullptr;  // compute
   bool own_cs = false;
-  cudaStream_t xs = nullptr;  // copy / coupling
+  cudaStream_t xs = nullptr;  // coupling buffer, field side (ingest)
+  cudaStream_t xo = nullptr;  // coupling buffer, source side (readout): a readout waiting for
+                              // the running step never delays the next field's copy
+  cudaEvent_t ev_pinned_in{}; // last asynchronous copy from pinned host field memory
+  bool pinned_in_flight = false;
 
   // store
   int64_t cap = 0, n = 0;
   Store S[2];
   int cur = 0;
   CUtensorMap tmap[4];        // [2 stores][float rows, ids] TMA descriptors (kernel parameters)
-  CUtensorMap tmap_ip[2];     // [2 stores] float rows with the {68, 8} box of k_ip
+  CUtensorMap tmap_ip[2];     // [2 stores] float rows with the {68, 8} box of k_ip / k_fs
+  CUtensorMap tmap_id66[2];   // [2 stores] ids with the {66, 1} box of k_fs
   CUtensorMap tmap_win[2][2]; // [field buffer][window shape] TMA descriptors of the fluid field
   long long* dtab = nullptr;  // [nbins][27] destination table of the fused scatter (k_dbase)
   int* far_cnt = nullptr;     // [nbins] far particles per destination bin (C-15b; k_count)
@@ -143,6 +148,17 @@ static st_status fail(st_ctx* c, st_status s, const std::string& msg) {
     if (!(ctx)) return ST_ERR_INVALID_ARG;                                              \
     if ((ctx)->dead) return ST_ERR_CUDA;                                                \
   } while (0)
+
+// page-locked host memory (cudaHostAlloc / cudaHostRegister): copies can be asynchronous
+static bool is_pinned_host_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
 
 static bool is_device_ptr(const void* p) {
   if (!p) return false;
@@ -406,6 +422,11 @@ static st_status make_tensor_maps(st_ctx* c) {
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(c, ST_ERR_CUDA, "tensor map (ids) encode failed: " + std::to_string((int)r));
+    const cuuint32_t boxi66[2] = {66, 1};                  // k_fs.cuh kFsBoxI
+    r = encode(&c->tmap_id66[i], CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, c->S[i].id, dimi, stridei, boxi66, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, ST_ERR_CUDA, "tensor map (ids, 64) encode failed: " + std::to_string((int)r));
   }
   // fluid field float4 [wnz][gy][gx] seen as fp32 {4 gx, gy, wnz}: k_pstep's window boxes
   // of (10 + 2R) x (3 + 2R) x (3 + 2R) cells, R = 0 (in place) / 1 (fused scatter);
@@ -442,6 +463,8 @@ static st_status init_impl(st_ctx* c) {
     c->own_cs = true;
   }
   ST_CUDA(c, cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking));
+  ST_CUDA(c, cudaStreamCreateWithFlags(&c->xo, cudaStreamNonBlocking));
+  ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_pinned_in, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
     st_status s = alloc_store(c, c->S[i], c->cap);
     if (s) return s;
@@ -540,6 +563,7 @@ st_status st_destroy(st_ctx* c) {
   if (!c) return ST_OK;
   if (c->cs) cudaStreamSynchronize(c->cs);
   if (c->xs) cudaStreamSynchronize(c->xs);
+  if (c->xo) cudaStreamSynchronize(c->xo);
   if (c->comm) comm_destroy(c->comm);
   if (c->shard) comm_destroy(c->shard);
   for (int i = 0; i < 2; ++i) {
@@ -591,6 +615,8 @@ st_status st_destroy(st_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->own_cs && c->cs) cudaStreamDestroy(c->cs);
   if (c->xs) cudaStreamDestroy(c->xs);
+  if (c->xo) cudaStreamDestroy(c->xo);
+  if (c->ev_pinned_in) cudaEventDestroy(c->ev_pinned_in);
   cudaGetLastError();
   delete c;
   return ST_OK;
@@ -639,6 +665,13 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
   const Geom& g = c->g;
   const int64_t own_cells = c->local_cells;
   const bool dev = is_device_ptr(u);
+  const bool pinned = !dev && is_pinned_host_ptr(u);
+  // the previous pinned copy is complete before this call returns (header contract: a
+  // pinned buffer may be rewritten once the next st_set_fluid_field has returned)
+  if (c->pinned_in_flight) {
+    ST_CUDA(c, cudaEventSynchronize(c->ev_pinned_in));
+    c->pinned_in_flight = false;
+  }
   float* stage = c->field_stage;
   // staging layout: [3][ext_nz][ny][nx]; owned planes start at plane (z0 - ext_z0)
   const int64_t plane = (int64_t)g.n[0] * g.n[1];
@@ -651,8 +684,12 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
   for (int k = 0; k < 3; ++k)
     ST_CUDA(c, cudaMemcpyAsync(stage + k * comp + own_off * plane, u + k * own_cells, own_cells * sizeof(float),
                                dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->xs));
-  if (!dev) {
-    // host inputs are consumed before the call returns (header contract)
+  if (pinned) {
+    // pinned host input: stream-ordered like device input, overlapping the running step
+    ST_CUDA(c, cudaEventRecord(c->ev_pinned_in, c->xs));
+    c->pinned_in_flight = true;
+  } else if (!dev) {
+    // pageable host inputs are consumed before the call returns (header contract)
     ST_CUDA(c, cudaEventRecord(c->ev_in, c->xs));
     ST_CUDA(c, cudaEventSynchronize(c->ev_in));
   }
@@ -761,6 +798,7 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.tm_f = c->tmap[2 * c->cur];
   a.tm_id = c->tmap[2 * c->cur + 1];
   a.tm_f64 = c->tmap_ip[c->cur];
+  a.tm_id66 = c->tmap_id66[c->cur];
   a.tm_win[0] = c->tmap_win[c->front < 0 ? 0 : c->front][0];
   a.tm_win[1] = c->tmap_win[c->front < 0 ? 0 : c->front][1];
   a.dtab = c->dtab;
@@ -848,8 +886,8 @@ static st_status count_slots(st_ctx* c, bool* far) {
     c->hist_ready = false;
     ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
     c->reb_t0 = true;
-    if (c->comm) {
-      *far = false;
+    if (c->comm || c->far_cnt) {   // several ranks: decided on the device; 8^3 chunks on
+      *far = false;                 // one rank: every far particle has a tail (no host sync)
       return ST_OK;
     }
     ST_CUDA(c, cudaEventSynchronize(c->ev_step_done));
@@ -878,6 +916,8 @@ static st_status count_slots(st_ctx* c, bool* far) {
   if (c->comm) {
     ST_CUDA(c, cudaMemsetAsync(c->d_farg, 0, sizeof(int), c->cs));
     ca.far = c->d_farg;
+  } else if (c->far_cnt) {
+    ca.far = c->d_farg;             // never set on one rank with far tails: not read back
   } else {
     ST_CUDA(c, cudaEventSynchronize(c->ev_count));   // the previous count has read nothing since
     *c->h_far = 0;
@@ -885,7 +925,7 @@ static st_status count_slots(st_ctx* c, bool* far) {
   }
   st_status s = check_launch(c, launch_count(ca, c->cs));
   if (s) return s;
-  if (c->comm) {
+  if (c->comm || c->far_cnt) {
     *far = false;
     return ST_OK;
   }
@@ -1082,12 +1122,8 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
         ST_CUDA(c, cudaMemsetAsync(c->far_cnt, 0, (size_t)c->bg.nbins * sizeof(int), c->cs));
         if (c->comm) {
           ST_CUDA(c, cudaMemsetAsync(c->d_farg, 0, sizeof(int), c->cs));
-          a.cnt_far = c->d_farg;
-        } else {
-          ST_CUDA(c, cudaEventSynchronize(c->ev_count));   // no kernel still writes the flag
-          *c->h_far = 0;
-          a.cnt_far = c->d_far;
         }
+        a.cnt_far = c->d_farg;      // one rank: never set (8^3 chunks place every far particle)
         a.cnt_hist = c->hist;
         a.cnt_far_cnt = c->far_cnt;
         a.cnt_movers = c->d_movers;
@@ -1129,24 +1165,24 @@ st_status st_request_sources(st_ctx* c) {
   c->readout_T = c->T_acc[old];
   c->T_acc[old] = 0.0;
   const Geom& g = c->g;
-  ST_CUDA(c, cudaStreamWaitEvent(c->xs, c->ev_acc_writer[old], 0));
+  ST_CUDA(c, cudaStreamWaitEvent(c->xo, c->ev_acc_writer[old], 0));
   if (c->comm) {
     std::string why;
-    if (comm_source_halo(c->comm, c->acc[old], g, c->z0, c->z1, c->H, c->xs, why)) return fail(c, ST_ERR_NCCL, why);
+    if (comm_source_halo(c->comm, c->acc[old], g, c->z0, c->z1, c->H, c->xo, why)) return fail(c, ST_ERR_NCCL, why);
   }
   if (c->shard) {   // particle-sharded: every rank deposited into the whole domain
     std::string why;
-    if (comm_allreduce_sum(c->shard, reinterpret_cast<float*>(c->acc[old]), (size_t)g.anz * g.n[1] * g.n[0] * 4, c->xs,
+    if (comm_allreduce_sum(c->shard, reinterpret_cast<float*>(c->acc[old]), (size_t)g.anz * g.n[1] * g.n[0] * 4, c->xo,
                            why))
       return fail(c, ST_ERR_NCCL, why);
   }
   const double V = c->cfg.cell_size[0] * c->cfg.cell_size[1] * c->cfg.cell_size[2];
   const float scale = c->readout_T > 0.0 ? (float)(1.0 / (V * c->readout_T)) : 0.0f;
-  st_status s = check_launch(c, launch_source_readout(g, c->acc[old], c->z0, c->z1, scale, c->S_dev, c->xs));
+  st_status s = check_launch(c, launch_source_readout(g, c->acc[old], c->z0, c->z1, scale, c->S_dev, c->xo));
   if (s) return s;
-  ST_CUDA(c, cudaMemsetAsync(c->acc[old], 0, (size_t)g.anz * g.n[1] * g.n[0] * sizeof(float4), c->xs));
-  ST_CUDA(c, cudaEventRecord(c->ev_acc_free[old], c->xs));
-  ST_CUDA(c, cudaEventRecord(c->ev_readout_done, c->xs));
+  ST_CUDA(c, cudaMemsetAsync(c->acc[old], 0, (size_t)g.anz * g.n[1] * g.n[0] * sizeof(float4), c->xo));
+  ST_CUDA(c, cudaEventRecord(c->ev_acc_free[old], c->xo));
+  ST_CUDA(c, cudaEventRecord(c->ev_readout_done, c->xo));
   c->readout_pending = true;
   return ST_OK;
 }
@@ -1158,9 +1194,9 @@ st_status st_wait_sources(st_ctx* c, float* S, double* interval_s) {
   if (S) {
     const bool dev = is_device_ptr(S);
     ST_CUDA(c, cudaMemcpyAsync(S, c->S_dev, 3 * c->local_cells * sizeof(float),
-                               dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->xs));
+                               dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->xo));
   }
-  ST_CUDA(c, cudaStreamSynchronize(c->xs));
+  ST_CUDA(c, cudaStreamSynchronize(c->xo));
   if (interval_s) *interval_s = c->readout_T;
   return consume_flags(c);
 }
@@ -1176,6 +1212,8 @@ st_status st_sync(st_ctx* c) {
   ST_ALIVE(c);
   ST_CUDA(c, cudaStreamSynchronize(c->cs));
   ST_CUDA(c, cudaStreamSynchronize(c->xs));
+  ST_CUDA(c, cudaStreamSynchronize(c->xo));
+  c->pinned_in_flight = false;
   return consume_flags(c);
 }
 

@@ -32,7 +32,8 @@ struct StepArgs {
   Store A, B;                 // input layout / output layout (scatter)
   CUtensorMap tm_f;           // TMA tensor map of A's float rows (2-D {cap, 8}; k_pstep)
   CUtensorMap tm_id;          // TMA tensor map of A's ids (2-D {cap, 1}; k_pstep)
-  CUtensorMap tm_f64;         // TMA tensor map of A's float rows, box {68, 8} (k_ip: 64-particle batches)
+  CUtensorMap tm_f64;         // TMA tensor map of A's float rows, box {68, 8} (k_ip / k_fs: 64-particle batches)
+  CUtensorMap tm_id66;        // TMA tensor map of A's ids, box {66, 1} (k_fs)
   CUtensorMap tm_win[2];      // TMA maps of the front fluid field, window boxes of k_pstep:
                               // [0] 10x3x3 cells (in place), [1] 12x5x5 cells (fused scatter)
   int64_t cap, n;
