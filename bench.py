@@ -345,14 +345,17 @@ def run_ours(args):
         if args.partition == "weighted" and G > 1:
             cfg.slab_planes = plan_partition(cfg, counts)
         lay0 = __import__("paper_2603_26691_b200").plan_layout(cfg)
-        n_mine = int(round(sum(counts[lay0.kz0:lay0.kz1])))
-        cfg.capacity = cap = int(n_mine * 1.1) + 1_000_000
+        if args.decomp == "slab":
+            n_mine = int(round(sum(counts[lay0.kz0:lay0.kz1])))
+            cfg.capacity = cap = int(n_mine * 1.1) + 1_000_000
     st = ScaleTrack(cfg, stream=stream.cuda_stream, unique_id=uid)
     lay = st.layout
-    z_range = (lay.z0, lay.z1)
-    # particles: uniform in this rank's slab, drawn on the device in batches (seed 8 + rank);
-    # clustered: z redrawn from the exponential restricted to the slab (inverse CDF)
-    lo, hi = synth.domain_box(wl, z_range)
+    z_range = (lay.z0, lay.z1)      # this rank's Eulerian partition (field in, sources out)
+    # particles: uniform in this rank's slab (slab decomposition) or anywhere in the domain
+    # (particle-sharded: n_per per rank whatever the clustering, Fig. 1c), drawn on the
+    # device in batches (seed 8 + rank); clustered: z redrawn from the exponential
+    # restricted to that box (inverse CDF)
+    lo, hi = synth.domain_box(wl, z_range if args.decomp == "slab" else None)
     batch = 100_000_000
     for b0 in range(0, n_mine, batch):
         nb = min(batch, n_mine - b0)

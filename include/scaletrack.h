@@ -243,6 +243,15 @@ st_status st_sync(st_ctx* ctx);
  * advance_ms: the advance (+ fused rebin) kernel; rebin_ms: standalone rebin. */
 st_status st_last_timings(st_ctx* ctx, float* advance_ms, float* rebin_ms);
 
+/* Timeline of the asynchronous coupling buffer (SURVEY §8(d6) asks
+ * for copy/compute overlap evidence): t[6] receives, in ms since the context was
+ * created, the begin and end of the most recent field copy (st_set_fluid_field, copy
+ * stream), of the most recent st_advance (compute stream) and of the most recent
+ * source readout (st_request_sources .. the copy out in st_wait_sources, readout
+ * stream), measured with CUDA events on those streams; -1 where not yet recorded.
+ * Blocks on those events. */
+st_status st_last_trace(st_ctx* ctx, double* t);
+
 /* Message of the last error on ctx ("" if none).  NULL ctx: last init error. */
 const char* st_last_error(const st_ctx* ctx);
 

@@ -280,6 +280,12 @@ class ScaleTrack:
     def sync(self):
         self._check(self.lib.st_sync(self.h))
 
+    def last_trace(self) -> np.ndarray:
+        """st_last_trace: [copy in begin, end, step begin, end, readout begin, end] in ms."""
+        t = np.empty(6, np.float64)
+        self._check(self.lib.st_last_trace(self.h, t.ctypes.data))
+        return t
+
     def last_timings(self):
         a, r = ctypes.c_float(), ctypes.c_float()
         self._check(self.lib.st_last_timings(self.h, ctypes.byref(a), ctypes.byref(r)))

@@ -14,7 +14,13 @@
 // the two particles of a lane interleave.
 #pragma once
 
-constexpr int kFsStages = 3;
+#ifndef ST_FS_STAGES
+#define ST_FS_STAGES 3   // one CTA of 8 warps per SM (measured: 2 CTAs/SM with 2 stages or 6 warps are slower)
+#endif
+#ifndef ST_FS_WARPS
+#define ST_FS_WARPS 8
+#endif
+constexpr int kFsStages = ST_FS_STAGES;
 constexpr int kFsBoxI = 66;                                   // 64 ids + 2 of alignment slack
 constexpr int kFsStageBytes = (8 * kIpBoxF * 4 + kFsBoxI * 8 + 127) / 128 * 128;   // 2176 + 528 -> 2816
 constexpr int kFsOffId = 8 * kIpBoxF * 4;                     // ids after the float rows (128-B aligned)
@@ -24,7 +30,7 @@ constexpr int kFsOffRun = kFsOffTab + kTable * 8;             // run i32[216]
 constexpr int kFsOffRel = kFsOffRun + kTable * 4;
 constexpr int kFsOffBar = kFsOffRel + 48;
 constexpr int kFsWarpBytes = (kFsOffBar + 8 * (kFsStages + 1) + 127) / 128 * 128;
-constexpr int kFsWarps = 8;
+constexpr int kFsWarps = ST_FS_WARPS;
 constexpr uint32_t kFsTx = 8u * kIpBoxF * 4u + kFsBoxI * 8u;
 
 template <int BCM, int SPEC>

@@ -59,6 +59,10 @@ struct st_ctx {
   Comm* shard = nullptr;      // ST_DECOMP_SHARDED: communicator of the source all-reduce
   std::vector<int32_t> slab_copy;   // cfg.slab_planes, owned (the caller's array is read at init only)
   int shard_rank = 0, shard_nranks = 1;
+  // ST_DECOMP_SHARDED: the Eulerian partition this rank owns (cell planes [eu_z0, eu_z1);
+  // eu_zb = every rank's boundaries): the field comes in and the sources go out per owner
+  int eu_z0 = 0, eu_z1 = 0;
+  std::vector<int> eu_zb;
   int32_t* key[2] = {nullptr, nullptr};
   SortScratch sc;
   uint64_t next_id = 0;
@@ -119,6 +123,10 @@ struct st_ctx {
 
   // timing
   cudaEvent_t t_adv0{}, t_adv1{}, t_reb0{}, t_reb1{};
+  // coupling-buffer trace (st_last_trace): [field copy begin/end (xs), step begin/end (cs),
+  // readout begin/end (xo)] of the most recent calls, against a reference event
+  cudaEvent_t tr_ref{}, tr[6]{};
+  bool tr_set[6] = {false, false, false, false, false, false};
   bool timed_adv = false, timed_reb = false;
   bool reb_t0 = false;        // t_reb0 already recorded for the rebin in progress (k_count)
 
@@ -241,6 +249,19 @@ static void slab_range(const st_config* c, int ncz, int r, int* k0, int* k1) {
   }
 }
 
+// Cell-plane boundaries of the Eulerian partitions (rank r owns [zb[r], zb[r+1])): the
+// slab rule of the slab decomposition (equal chunk planes, or cfg->slab_planes).
+static void eulerian_slabs(const st_config* c, std::vector<int>& zb) {
+  const int ncz = (c->dims[2] + c->chunk_cells - 1) / c->chunk_cells;
+  zb.assign(c->nranks + 1, 0);
+  for (int r = 0; r < c->nranks; ++r) {
+    int k0, k1;
+    slab_range(c, ncz, r, &k0, &k1);
+    zb[r] = std::min(k0 * c->chunk_cells, c->dims[2]);
+    zb[r + 1] = std::min(k1 * c->chunk_cells, c->dims[2]);
+  }
+}
+
 // The geometry a rank sees: its own slab (ST_DECOMP_SLAB), or the whole domain as if
 // alone (ST_DECOMP_SHARDED: the paper's Fig. 1c scheme, particles stay where injected).
 static st_config geometry_view(const st_config* c) {
@@ -249,6 +270,7 @@ static st_config geometry_view(const st_config* c) {
     v.rank = 0;
     v.nranks = 1;
     v.decomposition = ST_DECOMP_SLAB;   // one rank's slab = the whole domain
+    v.slab_planes = nullptr;            // (they bound the Eulerian partitions: eulerian_slabs)
   }
   return v;
 }
@@ -264,6 +286,16 @@ static st_status validate(const st_config* c, std::string& why) {
   if (c->decomposition == ST_DECOMP_SHARDED) {
     if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) { why = "bad rank/nranks"; return ST_ERR_INVALID_ARG; }
     if (c->nranks > 1 && !c->nccl_unique_id) { why = "nccl_unique_id required when nranks > 1"; return ST_ERR_INVALID_ARG; }
+    if (c->chunk_cells >= 1 && c->dims[2] >= 1 && c->nranks > (c->dims[2] + c->chunk_cells - 1) / c->chunk_cells) {
+      why = "need at least one chunk plane per rank (Eulerian partitions)";
+      return ST_ERR_INVALID_ARG;
+    }
+    if (c->slab_planes && c->chunk_cells >= 1) {
+      const int ncz = (c->dims[2] + c->chunk_cells - 1) / c->chunk_cells;
+      if (c->slab_planes[0] != 0 || c->slab_planes[c->nranks] != ncz) { why = "slab_planes must span [0, ncz]"; return ST_ERR_INVALID_ARG; }
+      for (int r = 0; r < c->nranks; ++r)
+        if (c->slab_planes[r + 1] <= c->slab_planes[r]) { why = "slab_planes must be strictly ascending"; return ST_ERR_INVALID_ARG; }
+    }
     const st_config v = geometry_view(c);
     return validate(&v, why);
   }
@@ -484,6 +516,8 @@ static st_status init_impl(st_ctx* c) {
   ST_CUDA(c, cudaEventCreate(&c->t_adv1));
   ST_CUDA(c, cudaEventCreate(&c->t_reb0));
   ST_CUDA(c, cudaEventCreate(&c->t_reb1));
+  ST_CUDA(c, cudaEventCreate(&c->tr_ref));
+  for (int k = 0; k < 6; ++k) ST_CUDA(c, cudaEventCreate(&c->tr[k]));
   {
     st_status ts = make_tensor_maps(c);
     if (ts) return ts;
@@ -555,6 +589,7 @@ static st_status init_impl(st_ctx* c) {
     c->shard = comm_create(c->cfg.nccl_unique_id, c->shard_rank, c->shard_nranks, nullptr, c->cs, why);
     if (!c->shard) return fail(c, ST_ERR_NCCL, why);
   }
+  ST_CUDA(c, cudaEventRecord(c->tr_ref, c->cs));
   ST_CUDA(c, cudaStreamSynchronize(c->cs));
   return ST_OK;
 }
@@ -611,8 +646,10 @@ st_status st_destroy(st_ctx* c) {
   cudaFree(c->sc.hist);
   cudaFree(c->sc.offs);
   cudaFree(c->sc.partial);
-  for (cudaEvent_t e : {c->ev_readout_done, c->ev_in, c->t_adv0, c->t_adv1, c->t_reb0, c->t_reb1})
+  for (cudaEvent_t e : {c->ev_readout_done, c->ev_in, c->t_adv0, c->t_adv1, c->t_reb0, c->t_reb1, c->tr_ref})
     if (e) cudaEventDestroy(e);
+  for (int k = 0; k < 6; ++k)
+    if (c->tr[k]) cudaEventDestroy(c->tr[k]);
   if (c->own_cs && c->cs) cudaStreamDestroy(c->cs);
   if (c->xs) cudaStreamDestroy(c->xs);
   if (c->xo) cudaStreamDestroy(c->xo);
@@ -644,6 +681,9 @@ st_status st_init(const st_config* cfg, st_ctx** out) {
   if (cfg->decomposition == ST_DECOMP_SHARDED) {
     c->shard_rank = cfg->rank;
     c->shard_nranks = cfg->nranks;
+    eulerian_slabs(cfg, c->eu_zb);
+    c->eu_z0 = c->eu_zb[cfg->rank];
+    c->eu_z1 = c->eu_zb[cfg->rank + 1];
   }
   s = init_impl(c);
   if (s) {
@@ -663,7 +703,12 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
   // the back buffer may still be read by an advance enqueued earlier
   ST_CUDA(c, cudaStreamWaitEvent(c->xs, c->ev_field_reader[back], 0));
   const Geom& g = c->g;
-  const int64_t own_cells = c->local_cells;
+  ST_CUDA(c, cudaEventRecord(c->tr[0], c->xs));
+  c->tr_set[0] = true;
+  // cells the caller provides: this rank's slab (ST_DECOMP_SLAB) or its Eulerian
+  // partition (ST_DECOMP_SHARDED; the other partitions arrive from their owners)
+  const int in_z0 = c->shard ? c->eu_z0 : c->z0, in_z1 = c->shard ? c->eu_z1 : c->z1;
+  const int64_t own_cells = (int64_t)g.n[0] * g.n[1] * (in_z1 - in_z0);
   const bool dev = is_device_ptr(u);
   const bool pinned = !dev && is_pinned_host_ptr(u);
   // the previous pinned copy is complete before this call returns (header contract: a
@@ -681,8 +726,9 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
     ST_CUDA(c, cudaEventRecord(c->ev_in, c->cs));
     ST_CUDA(c, cudaStreamWaitEvent(c->xs, c->ev_in, 0));
   }
+  const int in_off = in_z0 - c->ext_z0;
   for (int k = 0; k < 3; ++k)
-    ST_CUDA(c, cudaMemcpyAsync(stage + k * comp + own_off * plane, u + k * own_cells, own_cells * sizeof(float),
+    ST_CUDA(c, cudaMemcpyAsync(stage + k * comp + in_off * plane, u + k * own_cells, own_cells * sizeof(float),
                                dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->xs));
   if (pinned) {
     // pinned host input: stream-ordered like device input, overlapping the running step
@@ -694,6 +740,11 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
     ST_CUDA(c, cudaEventSynchronize(c->ev_in));
   }
   int src_z0 = c->z0, src_nz = c->z1 - c->z0;
+  if (c->shard) {   // Fig. 1c: every rank gets every owner's planes
+    std::string why;
+    if (comm_shard_field(c->shard, stage, comp, plane, -c->ext_z0, c->eu_zb, c->xs, why))
+      return fail(c, ST_ERR_NCCL, why);
+  }
   if (c->comm) {
     std::string why;
     if (comm_field_halo(c->comm, stage, comp, plane, c->ext_z0, c->ext_nz, c->z0, c->z1, g.n[2], g.bc[2], c->xs, why))
@@ -705,6 +756,8 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
   st_status s = check_launch(c, launch_field_ingest(g, src, comp, src_z0, src_nz, c->field[back], c->xs));
   if (s) return s;
   ST_CUDA(c, cudaEventRecord(c->ev_field_ready[back], c->xs));
+  ST_CUDA(c, cudaEventRecord(c->tr[1], c->xs));
+  c->tr_set[1] = true;
   c->pending = back;
   return ST_OK;
 }
@@ -1092,6 +1145,8 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
   if (c->front < 0) return fail(c, ST_ERR_STATE, "st_advance before st_set_fluid_field (P:202: first step is synchronous)");
   // the accumulator must be free (its previous readout finished zeroing it)
   ST_CUDA(c, cudaStreamWaitEvent(c->cs, c->ev_acc_free[c->acc_cur], 0));
+  ST_CUDA(c, cudaEventRecord(c->tr[2], c->cs));
+  c->tr_set[2] = true;
   st_status st = ST_OK;
   bool done = false;
   c->timed_reb = false;
@@ -1143,6 +1198,8 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
   }
   ST_CUDA(c, cudaEventRecord(c->ev_field_reader[c->front], c->cs));
   ST_CUDA(c, cudaEventRecord(c->ev_acc_writer[c->acc_cur], c->cs));
+  ST_CUDA(c, cudaEventRecord(c->tr[3], c->cs));
+  c->tr_set[3] = true;
   c->T_acc[c->acc_cur] += (double)nsteps * dt;
   c->calls += 1;
   if (c->calls % c->cfg.rebin_interval == 0) {
@@ -1166,19 +1223,21 @@ st_status st_request_sources(st_ctx* c) {
   c->T_acc[old] = 0.0;
   const Geom& g = c->g;
   ST_CUDA(c, cudaStreamWaitEvent(c->xo, c->ev_acc_writer[old], 0));
+  ST_CUDA(c, cudaEventRecord(c->tr[4], c->xo));
+  c->tr_set[4] = true;
   if (c->comm) {
     std::string why;
     if (comm_source_halo(c->comm, c->acc[old], g, c->z0, c->z1, c->H, c->xo, why)) return fail(c, ST_ERR_NCCL, why);
   }
-  if (c->shard) {   // particle-sharded: every rank deposited into the whole domain
-    std::string why;
-    if (comm_allreduce_sum(c->shard, reinterpret_cast<float*>(c->acc[old]), (size_t)g.anz * g.n[1] * g.n[0] * 4, c->xo,
-                           why))
+  if (c->shard) {   // particle-sharded: every rank deposited into the whole domain; each
+    std::string why;  // owner receives the sum over ranks of its planes (reduce-scatter)
+    if (comm_shard_sources(c->shard, c->acc[old], (int64_t)g.n[0] * g.n[1], c->eu_zb, c->xo, why))
       return fail(c, ST_ERR_NCCL, why);
   }
   const double V = c->cfg.cell_size[0] * c->cfg.cell_size[1] * c->cfg.cell_size[2];
   const float scale = c->readout_T > 0.0 ? (float)(1.0 / (V * c->readout_T)) : 0.0f;
-  st_status s = check_launch(c, launch_source_readout(g, c->acc[old], c->z0, c->z1, scale, c->S_dev, c->xo));
+  const int out_z0 = c->shard ? c->eu_z0 : c->z0, out_z1 = c->shard ? c->eu_z1 : c->z1;
+  st_status s = check_launch(c, launch_source_readout(g, c->acc[old], out_z0, out_z1, scale, c->S_dev, c->xo));
   if (s) return s;
   ST_CUDA(c, cudaMemsetAsync(c->acc[old], 0, (size_t)g.anz * g.n[1] * g.n[0] * sizeof(float4), c->xo));
   ST_CUDA(c, cudaEventRecord(c->ev_acc_free[old], c->xo));
@@ -1193,9 +1252,12 @@ st_status st_wait_sources(st_ctx* c, float* S, double* interval_s) {
   c->readout_pending = false;
   if (S) {
     const bool dev = is_device_ptr(S);
-    ST_CUDA(c, cudaMemcpyAsync(S, c->S_dev, 3 * c->local_cells * sizeof(float),
+    const int64_t out_cells = c->shard ? (int64_t)c->g.n[0] * c->g.n[1] * (c->eu_z1 - c->eu_z0) : c->local_cells;
+    ST_CUDA(c, cudaMemcpyAsync(S, c->S_dev, 3 * out_cells * sizeof(float),
                                dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->xo));
   }
+  ST_CUDA(c, cudaEventRecord(c->tr[5], c->xo));
+  c->tr_set[5] = true;
   ST_CUDA(c, cudaStreamSynchronize(c->xo));
   if (interval_s) *interval_s = c->readout_T;
   return consume_flags(c);
@@ -1305,6 +1367,13 @@ st_status st_get_layout(st_ctx* c, st_layout* o) {
   for (int a = 0; a < 3; ++a) o->nchunk[a] = c->g.NC[a];
   o->local_cells = c->local_cells;
   o->halo_cells = c->H;
+  if (c->shard) {   // the Eulerian partition this rank feeds and reads (field in, sources out)
+    o->z0 = c->eu_z0;
+    o->z1 = c->eu_z1;
+    o->kz0 = c->eu_z0 / c->g.cc;
+    o->kz1 = (c->eu_z1 + c->g.cc - 1) / c->g.cc;
+    o->local_cells = (int64_t)c->g.n[0] * c->g.n[1] * (c->eu_z1 - c->eu_z0);
+  }
   return ST_OK;
 }
 
@@ -1373,6 +1442,15 @@ st_status st_plan_layout(const st_config* cfg, st_layout* o) {
   for (int a = 0; a < 3; ++a) o->nchunk[a] = tmp.g.NC[a];
   o->local_cells = tmp.local_cells;
   o->halo_cells = tmp.H;
+  if (cfg->decomposition == ST_DECOMP_SHARDED) {
+    std::vector<int> zb;
+    eulerian_slabs(cfg, zb);
+    o->z0 = zb[cfg->rank];
+    o->z1 = zb[cfg->rank + 1];
+    o->kz0 = o->z0 / cfg->chunk_cells;
+    o->kz1 = (o->z1 + cfg->chunk_cells - 1) / cfg->chunk_cells;
+    o->local_cells = (int64_t)cfg->dims[0] * cfg->dims[1] * (o->z1 - o->z0);
+  }
   return ST_OK;
 }
 
@@ -1395,6 +1473,20 @@ st_status st_get_stats(st_ctx* c, st_stats* o) {
   ST_CUDA(c, cudaMemcpy(&fn, c->d_far_n, sizeof(fn), cudaMemcpyDeviceToHost));
   o->general_rebins = c->general_rebins;
   o->last_far = (int64_t)fn;
+  return ST_OK;
+}
+
+st_status st_last_trace(st_ctx* c, double* t) {
+  ST_ALIVE(c);
+  if (!t) return fail(c, ST_ERR_INVALID_ARG, "t is NULL");
+  for (int k = 0; k < 6; ++k) {
+    t[k] = -1.0;
+    if (!c->tr_set[k]) continue;
+    float ms = 0.0f;
+    ST_CUDA(c, cudaEventSynchronize(c->tr[k]));
+    ST_CUDA(c, cudaEventElapsedTime(&ms, c->tr_ref, c->tr[k]));
+    t[k] = ms;
+  }
   return ST_OK;
 }
 

@@ -191,6 +191,36 @@ int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H,
   return join_out(c, s, why);
 }
 
+int comm_shard_field(Comm* c, float* stage, int64_t comp, int64_t plane, int plane0, const std::vector<int>& zb,
+                     cudaStream_t s, std::string& why) {
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclGroupStart(), why);
+  for (int r = 0; r < c->nranks; ++r) {
+    const size_t cnt = (size_t)(zb[r + 1] - zb[r]) * plane;
+    if (!cnt) continue;
+    for (int k = 0; k < 3; ++k) {
+      float* p = stage + k * comp + (int64_t)(plane0 + zb[r]) * plane;
+      NCCK(ncclBroadcast(p, p, cnt, ncclFloat, r, c->nc, c->ns), why);
+    }
+  }
+  NCCK(ncclGroupEnd(), why);
+  return join_out(c, s, why);
+}
+
+int comm_shard_sources(Comm* c, float4* acc, int64_t plane, const std::vector<int>& zb, cudaStream_t s,
+                       std::string& why) {
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclGroupStart(), why);
+  for (int r = 0; r < c->nranks; ++r) {
+    const size_t cnt = (size_t)(zb[r + 1] - zb[r]) * plane * 4;
+    if (!cnt) continue;
+    float* p = reinterpret_cast<float*>(acc + (int64_t)zb[r] * plane);
+    NCCK(ncclReduce(p, p, cnt, ncclFloat, ncclSum, r, c->nc, c->ns), why);
+  }
+  NCCK(ncclGroupEnd(), why);
+  return join_out(c, s, why);
+}
+
 int comm_allreduce_max_i32(Comm* c, int* buf, size_t n, cudaStream_t s, std::string& why) {
   if (join_in(c, s, why)) return 1;
   NCCK(ncclAllReduce(buf, buf, n, ncclInt32, ncclMax, c->nc, c->ns), why);

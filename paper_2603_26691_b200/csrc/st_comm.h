@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "st_internal.h"
 
@@ -33,6 +34,18 @@ int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H,
 // Particle-sharded decomposition (ST_DECOMP_SHARDED): sum the whole-domain source
 // accumulator over all ranks in place (one all-reduce).  Returns 0 on success.
 int comm_allreduce_sum(Comm* c, float* buf, size_t n, cudaStream_t s, std::string& why);
+// Particle-sharded decomposition, the paper's Fig. 1c data flow: the
+// Eulerian side stays partitioned (rank r owns cell planes [zb[r], zb[r+1])); every rank
+// needs the whole field (its chunks may be anywhere) and every rank's deposits reach
+// every owner.  Field: rank r's owned planes are broadcast from r into every rank's
+// staging buffer (grouped ncclBroadcast, one per owner and component; stage plane index
+// of global plane z is plane0 + z).  Sources: the whole-domain float4 accumulator is
+// reduced onto each owner's planes (grouped ncclReduce, root = owner) — a reduce-scatter
+// with per-rank sizes; non-owned planes are left as they were.  Returns 0 on success.
+int comm_shard_field(Comm* c, float* stage, int64_t comp, int64_t plane, int plane0, const std::vector<int>& zb,
+                     cudaStream_t s, std::string& why);
+int comm_shard_sources(Comm* c, float4* acc, int64_t plane, const std::vector<int>& zb, cudaStream_t s,
+                       std::string& why);
 // max over ranks of n ints in place (collective agreement on a status)
 int comm_allreduce_max_i32(Comm* c, int* buf, size_t n, cudaStream_t s, std::string& why);
 

@@ -46,6 +46,7 @@ def main():
     lay = st.layout
     # inputs: every rank injects particles drawn over its own slab, seed per rank
     L = [d * h for d in dims]
+    L_x = L[0]
     slabs = [(r * (dims[2] // 8) // world * 8, (r + 1) * (dims[2] // 8) // world * 8) for r in range(world)]
     if split is not None:
         slabs = [(split[r] * 8, split[r + 1] * 8) for r in range(world)]
@@ -55,19 +56,32 @@ def main():
     wl_f = synth.Workload("mr", dims, (0, 0, 0), (h, h, h), (1, 1, bcz), 8, 0, (0, 0), "uniform", 1.0,
                           (0, 0, -9.81), 1, 1, 2e-3, steps, "fourier", {"u_rms": 0.3, "modes": 64, "kmax": 6}, 9, 0)
     F = synth.make_field(wl_f)                               # global field [3][nz][ny][nx]
+    if os.environ.get("MR_FIELD") == "xshear":
+        # fast along x (about 2 cells per 3 calls: far particles, C-15b, in every plane,
+        # including the slab's boundary planes) and slow along z (near movers between
+        # ranks): boundary bins get local runs, arrivals and a far tail in one rebin
+        cx = (np.arange(dims[0]) + 0.5) * h
+        F = np.zeros_like(F)
+        F[0] = 20.0
+        F[2] = (2.0 * np.sin(2 * np.pi * cx / L_x))[None, None, :]
+        F = F.astype(np.float32)
     x, u, d, w = parts[rank]
     st.inject(x, u, d, w)
     st.set_fluid_field(np.ascontiguousarray(F[:, lay.z0:lay.z1]))
     rows, Ss = [], []
-    for s in range(steps):
+    observe = os.environ.get("MR_OBSERVE", "each")   # "end": no per-call migration_counts (it
+    for s in range(steps):                             # flushes a due rebin), so rebins run fused
         st.advance(2e-3, 1)
-        rows.append(st.migration_counts().tolist())
+        if observe == "each" or s == steps - 1:
+            rows.append(st.migration_counts().tolist())
         S, T = st.get_sources()
         Ss.append((S, T))
     p = st.get_particles()
     gathered = [None] * world
+    stt = st.stats()
     dist.all_gather_object(gathered, {"p": p, "rows": rows, "S": [s for s, _ in Ss], "T": [t for _, t in Ss],
-                                      "z": (lay.z0, lay.z1)})
+                                      "z": (lay.z0, lay.z1), "far": stt["last_far"],
+                                      "general": stt["general_rebins"]})
     ok = True
     report = {}
     if rank == 0:
@@ -110,7 +124,11 @@ def main():
             kz = pg["chunk"] // (mesh.nchunk[0] * mesh.nchunk[1])
             lo, hi = emu.plane_range(r)
             order_ok &= bool(np.all((kz >= lo) & (kz < hi)))
-        report.update(order_ok=bool(order_ok), worst_x=worst_x, worst_u=worst_u)
+        report.update(order_ok=bool(order_ok), worst_x=worst_x, worst_u=worst_u, oracle_last_far=int(emu.last_far),
+                      gpu_last_far=[int(gathered[r]["far"]) for r in range(world)],
+                      gpu_general=[int(gathered[r]["general"]) for r in range(world)])
+        if os.environ.get("MR_FIELD") == "xshear":
+            ok &= emu.last_far > 0 and sum(report["gpu_last_far"]) == emu.last_far
         ok &= order_ok and worst_x <= 1e-5 and worst_u <= 1e-5
         print("MR_REPORT " + json.dumps(report), flush=True)
     st.close()

@@ -22,16 +22,39 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("K,bcz", [(1, 1), (2, 1), (1, 0)])
-def test_multigpu_matches_emulation(K, bcz):
+@pytest.mark.parametrize("K,bcz,observe", [(1, 1, "each"), (2, 1, "each"), (1, 0, "each"), (2, 1, "end"),
+                                           (1, 0, "end")])
+def test_multigpu_matches_emulation(K, bcz, observe):
+    """observe = "each": migration counts read after every call (each due rebin is flushed
+    by that observation, standalone); "end": nothing observed in between, so every rebin
+    runs fused into the next call's k_fs launch (multi-rank send buffers, arrivals)."""
     n = _ngpu()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(n, 4)
-    env = dict(os.environ, MR_K=str(K), MR_BCZ=str(bcz), MR_STEPS=str(6))
+    env = dict(os.environ, MR_K=str(K), MR_BCZ=str(bcz), MR_STEPS=str(6 if observe == "each" else 7),
+               MR_OBSERVE=observe)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + 7 * K + bcz),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + 7 * K + bcz + (50 if observe == "end" else 0)),
            os.path.join(ROOT, "tests", "mr_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "MR_REPORT" in out
+
+
+def test_multigpu_far_tails_and_arrivals_in_boundary_bins():
+    """K = 3 in a flow fast along x and slow along z: far particles (C-15b) land in every
+    plane, the slab's boundary planes included, in the same rebin as arrivals from the
+    neighbour ranks.  Each boundary bin must come out as local runs | arrivals | far tail
+    (the oracle's (bin, far) sort of kept ++ arrivals), with no slot written twice."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    env = dict(os.environ, MR_K="3", MR_BCZ="1", MR_STEPS="7", MR_FIELD="xshear", MR_OBSERVE="end")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", "29770", os.path.join(ROOT, "tests", "mr_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
