@@ -7,7 +7,7 @@ PKG       := paper_2603_26691_b200
 SRC       := $(PKG)/csrc
 LIB       := $(PKG)/lib/libscaletrack.so
 CU        := $(SRC)/st_api.cu $(SRC)/st_comm.cu $(SRC)/k_advance.cu $(SRC)/k_field.cu $(SRC)/k_sort.cu \
-             $(SRC)/k_step.cu $(SRC)/st_ec.cu
+             $(SRC)/k_step.cu $(SRC)/st_ec.cu $(SRC)/st_hilbert.cu
 HDR       := include/scaletrack.h $(wildcard $(SRC)/*.h) $(wildcard $(SRC)/*.cuh)
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) $(NVFLAGS_EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -Iinclude -I$(NCCL_DIR)/include \

@@ -39,8 +39,10 @@ def parse():
     ap.add_argument("--workload", default="C5", choices=["C3", "C4", "C5"])
     ap.add_argument("--cluster", type=float, default=0.0,
                     help="clustered load: particle density ~ exp(-z / (c Lz)) over the whole job (0 = uniform)")
-    ap.add_argument("--partition", default="equal", choices=["equal", "weighted"],
-                    help="slab boundaries: equal chunk planes, or count-balanced (st_plan_partition, SURVEY f4)")
+    ap.add_argument("--partition", default="equal", choices=["equal", "weighted", "hilbert"],
+                    help="slab boundaries: equal chunk planes, or count-balanced (st_plan_partition, SURVEY f4); "
+                         "hilbert (with --decomp sharded): each rank holds the particles of a count-balanced "
+                         "range of chunks along the Hilbert curve (st_plan_hilbert, P:185)")
     ap.add_argument("--decomp", default="slab", choices=["slab", "sharded"],
                     help="slab: z-slabs with migration (north star); sharded: every GPU holds the whole "
                          "domain, particles stay, sources all-reduced (PAPER Fig. 1c, SURVEY f2)")
@@ -348,6 +350,31 @@ def run_ours(args):
         if args.decomp == "slab":
             n_mine = int(round(sum(counts[lay0.kz0:lay0.kz1])))
             cfg.capacity = cap = int(n_mine * 1.1) + 1_000_000
+    hil = None
+    if args.decomp == "sharded" and args.partition == "hilbert":
+        # f4: expected particles per chunk of the job's distribution (uniform, or the
+        # clustered z-profile), chunk ranges along the Hilbert curve balanced by count
+        from paper_2603_26691_b200 import plan_hilbert
+        cc = wl.chunk_cells
+        NC = [(d + cc - 1) // cc for d in wl.dims]
+        L = [d * h for d, h in zip(wl.dims, wl.cell_size)]
+        ze = [min(k * cc * wl.cell_size[2], L[2]) for k in range(NC[2] + 1)]
+        if args.cluster > 0:
+            lam_h = args.cluster * L[2]
+            pm = np.array([math.exp(-a / lam_h) - math.exp(-b / lam_h) for a, b in zip(ze[:-1], ze[1:])])
+        else:
+            pm = np.diff(np.array(ze))
+        cw = np.repeat(pm / pm.sum() / (NC[0] * NC[1]), NC[0] * NC[1])   # chunk ids z-major
+        # ragged chunks at the x / y edges hold proportionally fewer cells
+        fx = np.array([min(cc, wl.dims[0] - k * cc) / cc for k in range(NC[0])])
+        fy = np.array([min(cc, wl.dims[1] - k * cc) / cc for k in range(NC[1])])
+        cw = cw * np.tile(np.outer(fy, fx).ravel(), NC[2])
+        cw = cw / cw.sum()
+        owner = plan_hilbert(cfg, np.round(cw * G * n_per).astype(np.int64))
+        mine = np.nonzero(owner == rank)[0]
+        n_mine = int(round(cw[mine].sum() * G * n_per))
+        cfg.capacity = cap = int(n_mine * 1.05) + 1_000_000
+        hil = (mine, cw[mine], NC, L, ze)
     st = ScaleTrack(cfg, stream=stream.cuda_stream, unique_id=uid)
     lay = st.layout
     z_range = (lay.z0, lay.z1)      # this rank's Eulerian partition (field in, sources out)
@@ -361,7 +388,32 @@ def run_ours(args):
         nb = min(batch, n_mine - b0)
         x, u, d, w = synth.particles_torch(nb, lo, hi, wl.d_range, wl.d_dist, wl.w,
                                            seed=wl.seed_particles * 1000 + rank * 100 + b0 // batch, device=dev)
-        if args.cluster > 0:
+        if hil is not None:
+            # positions inside this rank's chunks: chunk by inverse CDF of its weights, then
+            # uniform in x, y and (uniform or clustered) z within the chunk
+            mine, wts, NC, L, ze = hil
+            gen = torch.Generator(device=dev).manual_seed(91 + rank * 1000 + b0 // batch)
+            cdf = torch.cumsum(torch.from_numpy(wts / wts.sum()).to(dev), 0)
+            pick = torch.searchsorted(cdf, torch.rand(nb, device=dev, dtype=torch.float64, generator=gen)).clamp_(
+                max=len(mine) - 1)
+            ch = torch.from_numpy(mine).to(dev)[pick]
+            kx, ky, kz = ch % NC[0], (ch // NC[0]) % NC[1], ch // (NC[0] * NC[1])
+            ext = wl.chunk_cells * torch.tensor(wl.cell_size, dtype=torch.float64, device=dev)
+            qs = torch.rand((3, nb), device=dev, dtype=torch.float64, generator=gen)
+            xs = [torch.minimum((k + qs[a]) * ext[a], torch.tensor(L[a], dtype=torch.float64, device=dev))
+                  for a, k in enumerate((kx, ky))]
+            z0 = torch.tensor(ze, dtype=torch.float64, device=dev)[kz]
+            z1 = torch.tensor(ze, dtype=torch.float64, device=dev)[kz + 1]
+            if args.cluster > 0:
+                ea, eb = torch.exp(-z0 / lam), torch.exp(-z1 / lam)
+                zz = -lam * torch.log(ea - qs[2] * (ea - eb))
+            else:
+                zz = z0 + qs[2] * (z1 - z0)
+            xs.append(zz)
+            for a in range(3):
+                hi32 = torch.tensor(L[a], dtype=torch.float32, device=dev)
+                x[a] = torch.minimum(xs[a].to(torch.float32), torch.nextafter(hi32, torch.zeros_like(hi32)))
+        elif args.cluster > 0:
             qz = torch.rand(nb, device=dev, dtype=torch.float64,
                             generator=torch.Generator(device=dev).manual_seed(77 + rank * 1000 + b0 // batch))
             ea, eb = math.exp(-lo[2] / lam), math.exp(-hi[2] / lam)

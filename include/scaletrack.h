@@ -252,6 +252,19 @@ st_status st_last_timings(st_ctx* ctx, float* advance_ms, float* rebin_ms);
  * Blocks on those events. */
 st_status st_last_trace(st_ctx* ctx, double* t);
 
+/* Rebalance the particle counts of the ranks (ST_DECOMP_SHARDED; P:356
+ * "the partitioning would be regularly checked and ... particles can be exchanged
+ * between chunks").  Collective.  If the largest count exceeds the mean by more than
+ * tolerance (relative), every rank ends with total/G particles (the first total%G ranks
+ * one more): ranks above target send their surplus — the END of their store, i.e. the
+ * last bins of their bin order, a compact set — to ranks below target in rank order
+ * (water-filling), receivers append in ascending sender rank.  Afterwards the store
+ * is unbinned (the next rebin is the plain stable sort, C-15b).  *sent / *received:
+ * particles this rank gave / took.  No-op (ST_OK) for one rank or the slab
+ * decomposition, whose ownership is spatial (use st_plan_partition there).
+ * ST_ERR_CAPACITY on every rank, nothing moved, if any rank would overflow. */
+st_status st_rebalance(st_ctx* ctx, double tolerance, int64_t* sent, int64_t* received);
+
 /* Message of the last error on ctx ("" if none).  NULL ctx: last init error. */
 const char* st_last_error(const st_ctx* ctx);
 
@@ -262,6 +275,22 @@ const char* st_last_error(const st_ctx* ctx);
  * neighbour needs); ties -> the lexicographically smallest boundaries.  Host-only.
  * ST_ERR_INVALID_ARG if cfg is invalid or no feasible split exists. */
 st_status st_plan_partition(const st_config* cfg, const int64_t* plane_counts, int32_t* slab_planes);
+
+/* 3-D Hilbert index of n cells ("initialization procedure using a
+ * Hilbert space-filling curve"): xyz = [n][3] integer coordinates in
+ * [0, 2^order), order 1..21; out[n] in [0, 8^order), a bijection along which
+ * consecutive indices are face-adjacent cells (Skilling's transpose algorithm).
+ * ST_ERR_INVALID_ARG for a coordinate out of range.  Host-only. */
+st_status st_hilbert_index(int32_t order, int64_t n, const int32_t* xyz, uint64_t* out);
+
+/* Count-balanced Hilbert partition of the chunks (SPEC
+ * S:252-258 initialize_chunks): chunks ordered along the 3-D Hilbert curve of their
+ * chunk coordinates are split into cfg->nranks contiguous, non-empty ranges minimising
+ * the largest sum of chunk_counts (counts per global chunk id, chunk ids as in the
+ * header conventions); owner[chunk] receives the rank.  With ST_DECOMP_SHARDED a rank
+ * that injects the particles of the chunks it owns holds a compact, balanced share
+ * (the bounding box of its particles covers few Eulerian partitions).  Host-only. */
+st_status st_plan_hilbert(const st_config* cfg, const int64_t* chunk_counts, int32_t* owner);
 
 /* ABI version the library was built with (== ST_ABI_VERSION). */
 int32_t st_abi_version(void);

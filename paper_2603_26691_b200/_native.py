@@ -125,6 +125,9 @@ SIGNATURES = {
     "st_get_layout": (_i32, [_vp, ctypes.POINTER(StLayout)]),
     "st_plan_layout": (_i32, [ctypes.POINTER(StConfig), ctypes.POINTER(StLayout)]),
     "st_plan_partition": (_i32, [ctypes.POINTER(StConfig), _vp, _vp]),
+    "st_hilbert_index": (_i32, [ctypes.c_int32, ctypes.c_int64, _vp, _vp]),
+    "st_plan_hilbert": (_i32, [ctypes.POINTER(StConfig), _vp, _vp]),
+    "st_rebalance": (_i32, [_vp, ctypes.c_double, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "st_get_stats": (_i32, [_vp, ctypes.POINTER(StStats)]),
     "st_sync": (_i32, [_vp]),
     "st_last_timings": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),

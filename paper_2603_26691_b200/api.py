@@ -143,6 +143,30 @@ def plan_partition(cfg: Config, plane_counts) -> tuple:
     return tuple(int(v) for v in out)
 
 
+def hilbert_index(order: int, xyz) -> np.ndarray:
+    """st_hilbert_index: 3-D Hilbert index of integer cells xyz [n][3] on a 2^order cube."""
+    lib = N.load()
+    xyz = np.ascontiguousarray(xyz, dtype=np.int32).reshape(-1, 3)
+    out = np.empty(xyz.shape[0], np.uint64)
+    rc = lib.st_hilbert_index(int(order), xyz.shape[0], xyz.ctypes.data, out.ctypes.data)
+    if rc:
+        raise N.StError(rc, "st_hilbert_index: coordinate out of range or bad order")
+    return out
+
+
+def plan_hilbert(cfg: Config, chunk_counts) -> np.ndarray:
+    """st_plan_hilbert: owner rank of every chunk, contiguous along the Hilbert curve of the
+    chunk coordinates and balanced by chunk_counts.  Host-only."""
+    lib = N.load()
+    c = cfg.to_c()
+    counts = np.ascontiguousarray(chunk_counts, dtype=np.int64)
+    out = np.empty(counts.size, np.int32)
+    rc = lib.st_plan_hilbert(ctypes.byref(c), counts.ctypes.data, out.ctypes.data)
+    if rc:
+        raise N.StError(rc, "st_plan_hilbert failed")
+    return out
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     rc = N.load().st_nccl_unique_id(buf)
@@ -279,6 +303,12 @@ class ScaleTrack:
 
     def sync(self):
         self._check(self.lib.st_sync(self.h))
+
+    def rebalance(self, tolerance: float = 0.05):
+        """st_rebalance (collective, ST_DECOMP_SHARDED): (sent, received) particles."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self.lib.st_rebalance(self.h, float(tolerance), ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     def last_trace(self) -> np.ndarray:
         """st_last_trace: [copy in begin, end, step begin, end, readout begin, end] in ms."""

@@ -1476,6 +1476,96 @@ st_status st_get_stats(st_ctx* c, st_stats* o) {
   return ST_OK;
 }
 
+// ---------------------------------------------------------------- rebalancing (f4)
+// ST_DECOMP_SHARDED: equalise the particle counts of the ranks when the largest exceeds
+// the mean by more than `tolerance` ("the partitioning would be regularly checked
+// and ... particles can be exchanged between chunks").  Targets: total/G, the first
+// total%G ranks one more.  Donors (above target) give their surplus from the END of
+// their store — the last bins of their bin order, a spatially compact set — to the
+// receivers (below target) in rank order (two-pointer water-filling, deterministic);
+// receivers append in ascending donor rank.  Collective; the store is then unbinned.
+st_status st_rebalance(st_ctx* c, double tolerance, int64_t* sent, int64_t* received) {
+  ST_ALIVE(c);
+  if (sent) *sent = 0;
+  if (received) *received = 0;
+  if (!(tolerance >= 0.0)) return fail(c, ST_ERR_INVALID_ARG, "tolerance must be >= 0");
+  if (!c->shard) return ST_OK;   // one rank, or the slab decomposition (ownership is spatial)
+  {
+    st_status fr = flush_rebin(c);
+    if (fr) return fr;
+  }
+  const int G = c->shard_nranks, r = c->shard_rank;
+  std::string why;
+  int64_t* d_cnt = reinterpret_cast<int64_t*>(c->sc.offs);   // scratch (>= G+1 int64)
+  ST_CUDA(c, cudaMemcpyAsync(d_cnt + r, &c->n, sizeof(int64_t), cudaMemcpyHostToDevice, c->cs));
+  if (comm_allgather_i64(c->shard, d_cnt, c->cs, why)) return fail(c, ST_ERR_NCCL, why);
+  std::vector<int64_t> n(G);
+  ST_CUDA(c, cudaMemcpyAsync(n.data(), d_cnt, G * sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  int64_t tot = 0, mx = 0;
+  for (int q = 0; q < G; ++q) {
+    tot += n[q];
+    mx = std::max(mx, n[q]);
+  }
+  if (tot == 0 || (double)mx <= (1.0 + tolerance) * ((double)tot / G)) return ST_OK;
+  std::vector<int64_t> target(G), surplus(G);
+  for (int q = 0; q < G; ++q) {
+    target[q] = tot / G + (q < tot % G ? 1 : 0);
+    surplus[q] = n[q] - target[q];
+  }
+  // water-filling plan T[src][dst]
+  std::vector<std::vector<int64_t>> T(G, std::vector<int64_t>(G, 0));
+  {
+    int d = 0, q = 0;
+    std::vector<int64_t> give(surplus);
+    while (true) {
+      while (d < G && give[d] <= 0) ++d;
+      while (q < G && give[q] >= 0) ++q;
+      if (d >= G || q >= G) break;
+      const int64_t m = std::min(give[d], -give[q]);
+      T[d][q] += m;
+      give[d] -= m;
+      give[q] += m;
+    }
+  }
+  std::vector<int64_t> snd(G, 0), soff(G, 0), rcv(G, 0), roff(G, 0);
+  int64_t out = 0, in = 0;
+  for (int q = 0; q < G; ++q) out += T[r][q];
+  for (int q = 0; q < G; ++q) in += T[q][r];
+  if (c->n - out + in > c->cfg.capacity) why = "rebalance would exceed the store capacity";
+  int bad = why.empty() ? 0 : 1;
+  // every rank checks every rank's capacity the same way: agree before moving anything
+  ST_CUDA(c, cudaMemcpyAsync(c->d_farg, &bad, sizeof(int), cudaMemcpyHostToDevice, c->cs));
+  if (comm_allreduce_max_i32(c->shard, c->d_farg, 1, c->cs, why)) return fail(c, ST_ERR_NCCL, why);
+  ST_CUDA(c, cudaMemcpyAsync(&bad, c->d_farg, sizeof(int), cudaMemcpyDeviceToHost, c->cs));
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  if (bad) return fail(c, ST_ERR_CAPACITY, why.empty() ? "rebalance would exceed the capacity of some rank" : why);
+  int64_t o = c->n - out;   // the donor's tail, to destinations in ascending rank
+  for (int q = 0; q < G; ++q) {
+    snd[q] = T[r][q];
+    soff[q] = o;
+    o += T[r][q];
+  }
+  int64_t a = c->n - out;   // receivers append after what they keep, by ascending donor rank
+  for (int q = 0; q < G; ++q) {
+    rcv[q] = T[q][r];
+    roff[q] = a;
+    a += T[q][r];
+  }
+  // a rank is never both donor and receiver, so the sent tail and the appended block of
+  // one rank never overlap
+  if (comm_exchange_store(c->shard, c->S[c->cur], c->cap, snd, soff, rcv, roff, c->cs, why))
+    return fail(c, ST_ERR_NCCL, why);
+  ST_CUDA(c, cudaStreamSynchronize(c->cs));
+  c->n = c->n - out + in;
+  c->binned = false;
+  c->hist_ready = false;
+  c->rebin_due = false;
+  if (sent) *sent = out;
+  if (received) *received = in;
+  return ST_OK;
+}
+
 st_status st_last_trace(st_ctx* c, double* t) {
   ST_ALIVE(c);
   if (!t) return fail(c, ST_ERR_INVALID_ARG, "t is NULL");

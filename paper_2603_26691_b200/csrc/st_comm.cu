@@ -221,6 +221,40 @@ int comm_shard_sources(Comm* c, float4* acc, int64_t plane, const std::vector<in
   return join_out(c, s, why);
 }
 
+int comm_allgather_i64(Comm* c, int64_t* buf, cudaStream_t s, std::string& why) {
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclAllGather(buf + c->rank, buf, 1, ncclInt64, c->nc, c->ns), why);
+  return join_out(c, s, why);
+}
+
+int comm_exchange_store(Comm* c, const Store& A, int64_t cap, const std::vector<int64_t>& send,
+                        const std::vector<int64_t>& send_off, const std::vector<int64_t>& recv,
+                        const std::vector<int64_t>& recv_off, cudaStream_t s, std::string& why) {
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclGroupStart(), why);
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) continue;
+    if (send[q] > 0) {
+      const int64_t o = send_off[q], m = send[q];
+      for (int a = 0; a < 3; ++a) NCCK(ncclSend(A.x + a * cap + o, m, ncclFloat, q, c->nc, c->ns), why);
+      for (int a = 0; a < 3; ++a) NCCK(ncclSend(A.u + a * cap + o, m, ncclFloat, q, c->nc, c->ns), why);
+      NCCK(ncclSend(A.d + o, m, ncclFloat, q, c->nc, c->ns), why);
+      NCCK(ncclSend(A.w + o, m, ncclFloat, q, c->nc, c->ns), why);
+      NCCK(ncclSend(A.id + o, m, ncclUint64, q, c->nc, c->ns), why);
+    }
+    if (recv[q] > 0) {
+      const int64_t o = recv_off[q], m = recv[q];
+      for (int a = 0; a < 3; ++a) NCCK(ncclRecv(A.x + a * cap + o, m, ncclFloat, q, c->nc, c->ns), why);
+      for (int a = 0; a < 3; ++a) NCCK(ncclRecv(A.u + a * cap + o, m, ncclFloat, q, c->nc, c->ns), why);
+      NCCK(ncclRecv(A.d + o, m, ncclFloat, q, c->nc, c->ns), why);
+      NCCK(ncclRecv(A.w + o, m, ncclFloat, q, c->nc, c->ns), why);
+      NCCK(ncclRecv(A.id + o, m, ncclUint64, q, c->nc, c->ns), why);
+    }
+  }
+  NCCK(ncclGroupEnd(), why);
+  return join_out(c, s, why);
+}
+
 int comm_allreduce_max_i32(Comm* c, int* buf, size_t n, cudaStream_t s, std::string& why) {
   if (join_in(c, s, why)) return 1;
   NCCK(ncclAllReduce(buf, buf, n, ncclInt32, ncclMax, c->nc, c->ns), why);

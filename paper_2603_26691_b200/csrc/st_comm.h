@@ -46,6 +46,15 @@ int comm_shard_field(Comm* c, float* stage, int64_t comp, int64_t plane, int pla
                      cudaStream_t s, std::string& why);
 int comm_shard_sources(Comm* c, float4* acc, int64_t plane, const std::vector<int>& zb, cudaStream_t s,
                        std::string& why);
+// All-gather one int64 per rank (device buffer of nranks; this rank's slot filled by the
+// caller) — the counts of the sharded rebalance.
+int comm_allgather_i64(Comm* c, int64_t* buf, cudaStream_t s, std::string& why);
+// Sharded rebalance payload: this rank sends send[q] particles starting at store index
+// send_off[q] to rank q and receives recv[q] from q at recv_off[q] (SoA x,u,d,w,id of
+// capacity cap); one grouped send/recv.
+int comm_exchange_store(Comm* c, const Store& A, int64_t cap, const std::vector<int64_t>& send,
+                        const std::vector<int64_t>& send_off, const std::vector<int64_t>& recv,
+                        const std::vector<int64_t>& recv_off, cudaStream_t s, std::string& why);
 // max over ranks of n ints in place (collective agreement on a status)
 int comm_allreduce_max_i32(Comm* c, int* buf, size_t n, cudaStream_t s, std::string& why);
 

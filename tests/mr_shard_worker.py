@@ -51,13 +51,17 @@ def main():
     st.inject(x, u, d, w)
     st.set_fluid_field(np.ascontiguousarray(F[:, lay.z0:lay.z1]))   # this rank's Eulerian partition
     Ss = []
+    rebalance = os.environ.get("MR_REBALANCE") == "1"
+    moved = (0, 0)
     for s in range(steps):
         st.advance(2e-3, 1)
         S, T = st.get_sources()
         Ss.append(S)
+        if rebalance and s == 1:      # f4: equalise the counts (15000 + 2000 r injected)
+            moved = st.rebalance(0.0)
     p = st.get_particles()
     gathered = [None] * world
-    dist.all_gather_object(gathered, {"p": p, "S": Ss, "z": (lay.z0, lay.z1)})
+    dist.all_gather_object(gathered, {"p": p, "S": Ss, "z": (lay.z0, lay.z1), "moved": moved})
     ok = True
     if rank == 0:
         mesh = oracle.Mesh(dims=dims, cell_size=(h, h, h), chunk_cells=8, bc=(1, 1, 1))
@@ -81,7 +85,8 @@ def main():
         for r in range(world):
             pg = gathered[r]["p"]
             gid = pg["id"].astype(np.uint64)
-            ids_ok &= bool(np.all((gid >> np.uint64(40)) == r)) and gid.size == parts[r][2].size
+            if not rebalance:
+                ids_ok &= bool(np.all((gid >> np.uint64(40)) == r)) and gid.size == parts[r][2].size
             idx = np.searchsorted(oid, gid, sorter=np.argsort(oid))
             oi = np.argsort(oid)[idx]
             ids_ok &= bool(np.array_equal(oid[oi], gid))
@@ -91,7 +96,16 @@ def main():
             worst_x = max(worst_x, float(dx.max() / max(L)))
             worst_u = max(worst_u, float(np.abs(pg["u"].astype(np.float64) - po["u"][:, oi]).max()))
             ok &= bool(np.all(np.diff(mesh_bins := o.bin_key(pg["x"])) >= 0))
-        report = dict(source_rel_l2=worst_s, eulerian_slabs_ok=same_all, ids_ok=ids_ok,
+        counts = [int(gathered[r]["p"]["id"].size) for r in range(world)]
+        all_ids = np.sort(np.concatenate([gathered[r]["p"]["id"] for r in range(world)]).astype(np.uint64))
+        ids_ok &= bool(np.array_equal(all_ids, np.sort(oid)))
+        if rebalance:
+            tot = sum(counts)
+            ids_ok &= counts == [tot // world + (1 if r < tot % world else 0) for r in range(world)]
+            ids_ok &= sum(gathered[r]["moved"][0] for r in range(world)) == sum(
+                gathered[r]["moved"][1] for r in range(world)) > 0
+        report = dict(counts=counts, moved=[gathered[r]["moved"] for r in range(world)],
+                      source_rel_l2=worst_s, eulerian_slabs_ok=same_all, ids_ok=ids_ok,
                       worst_x=worst_x, worst_u=worst_u)
         ok &= worst_s <= 1e-5 and same_all and ids_ok and worst_x <= 1e-5 and worst_u <= 1e-5
         print("MR_REPORT " + json.dumps(report), flush=True)

@@ -61,6 +61,23 @@ def test_multigpu_far_tails_and_arrivals_in_boundary_bins():
     assert "MR_REPORT" in out
 
 
+def test_sharded_rebalance_equalises_counts():
+    """f4: st_rebalance moves the surplus of the heavier ranks (15000 + 2000 r
+    injected) so every rank ends with total/G particles; the physics is unchanged (the
+    same single-oracle comparison as without rebalancing) and no particle is lost."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    env = dict(os.environ, MR_K="2", MR_STEPS="6", MR_REBALANCE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", "29780", os.path.join(ROOT, "tests", "mr_shard_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "MR_REPORT" in out
+
+
 @pytest.mark.parametrize("K", [1, 2])
 def test_sharded_decomposition_matches_one_oracle(K):
     """ST_DECOMP_SHARDED: whole domain per rank, particles stay where
