@@ -390,14 +390,16 @@ typedef struct {
 /* Fill *cfg with the DESIGN.md C-30 constants (air / water, 1 m cells, reflecting). */
 void st_micro_config_default(st_micro_config* cfg);
 
-/* nsteps sub-steps of dt for n droplets.  All arrays are DEVICE pointers, caller-owned:
+/* nsteps sub-steps of dt for n droplets.  Arrays are caller-owned, all DEVICE pointers
+ * or all HOST pointers (host arrays are staged through device memory and the updated
+ * ones copied back before the call returns):
  *   x, u: [3][n] fp32 (updated in place); d, T: [n] fp32 (updated); w: [n] fp32 weights;
  *   F: [5][nz][ny][nx] fp32 cell-centred (u_x, u_y, u_z, T_f, rho_v);
  *   acc: [5][nz][ny][nx] fp64 fluid-side accumulators (kg m/s x3, kg, J), ADDED to.
  * n_clamped (host, NULL to skip) receives the number of mass-floor clamps (C-32).
  * Runs on cfg->stream and blocks until done.  n == 0 is a no-op.
  * Errors: ST_ERR_INVALID_ARG (bad cfg, n < 0, nsteps < 0, dt <= 0, NULL arrays with
- * n > 0, host pointers), ST_ERR_CFL (a droplet still outside after one reflection /
+ * n > 0, a mix of host and device pointers), ST_ERR_CFL (a droplet still outside after one reflection /
  * wrap: the state is updated, the result is not trustworthy), ST_ERR_CUDA. */
 st_status st_micro_advance(const st_micro_config* cfg, int64_t n, float* x, float* u, float* d, float* T,
                            const float* w, const float* F, double dt, int32_t nsteps, double* acc,

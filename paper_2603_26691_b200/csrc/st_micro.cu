@@ -238,10 +238,48 @@ extern "C" st_status st_micro_advance(const st_micro_config* c, int64_t n, float
   if (n == 0 || nsteps == 0) return ST_OK;
   if (!x || !u || !d || !T || !w || !F || !acc) return ST_ERR_INVALID_ARG;
   if (cudaSetDevice(c->device) != cudaSuccess) return ST_ERR_CUDA;
-  const void* ptrs[7] = {x, u, d, T, w, F, acc};
-  for (const void* p : ptrs)
-    if (!is_device(p)) return ST_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)c->stream;
+  // host arrays (the other st_* calls accept host or device pointers too): stage every
+  // array through device memory, run, copy the updated ones back (blocking)
+  {
+    const void* ptrs[7] = {x, u, d, T, w, F, acc};
+    bool all_dev = true, any_dev = false;
+    for (const void* p : ptrs) {
+      const bool dv = is_device(p);
+      all_dev &= dv;
+      any_dev |= dv;
+    }
+    if (!all_dev) {
+      if (any_dev) return ST_ERR_INVALID_ARG;   // mixed host / device arrays
+      const int64_t nc = (int64_t)c->dims[0] * c->dims[1] * c->dims[2];
+      const size_t bx = 3 * n * sizeof(float), b1 = n * sizeof(float), bF = 5 * nc * sizeof(float),
+                   bA = 5 * nc * sizeof(double);
+      char* buf = nullptr;
+      if (cudaMallocAsync(&buf, 2 * bx + 3 * b1 + bF + bA, s) != cudaSuccess) return ST_ERR_CUDA;
+      float* dx = (float*)buf;
+      float* du = (float*)(buf + bx);
+      float* dd = (float*)(buf + 2 * bx);
+      float* dT = (float*)(buf + 2 * bx + b1);
+      float* dw = (float*)(buf + 2 * bx + 2 * b1);
+      float* dF = (float*)(buf + 2 * bx + 3 * b1);
+      double* dA = (double*)(buf + 2 * bx + 3 * b1 + bF);
+      cudaError_t e = cudaSuccess;
+      const void* src[7] = {x, u, d, T, w, F, acc};
+      void* dst[7] = {dx, du, dd, dT, dw, dF, dA};
+      const size_t sz[7] = {bx, bx, b1, b1, b1, bF, bA};
+      for (int k = 0; k < 7 && e == cudaSuccess; ++k) e = cudaMemcpyAsync(dst[k], src[k], sz[k], cudaMemcpyHostToDevice, s);
+      st_status st = e == cudaSuccess ? st_micro_advance(c, n, dx, du, dd, dT, dw, dF, dt, nsteps, dA, n_clamped)
+                                      : ST_ERR_CUDA;
+      void* back[5] = {x, u, d, T, acc};
+      const void* from[5] = {dx, du, dd, dT, dA};
+      const size_t bsz[5] = {bx, bx, b1, b1, bA};
+      for (int k = 0; k < 5 && (st == ST_OK || st == ST_ERR_CFL); ++k)
+        if (cudaMemcpyAsync(back[k], from[k], bsz[k], cudaMemcpyDeviceToHost, s) != cudaSuccess) st = ST_ERR_CUDA;
+      cudaFreeAsync(buf, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess) st = ST_ERR_CUDA;
+      return st;
+    }
+  }
 
   MicroArgs a{};
   a.n = n;

@@ -118,9 +118,23 @@ def test_micro_empty_and_errors():
     F = torch.zeros((5, 4, 4, 4), device=dev)
     acc = torch.zeros((5, 4, 4, 4), dtype=torch.float64, device=dev)
     assert micro_advance(cfg, e3, e3.clone(), e1, e1.clone(), e1.clone(), F, 1e-3, 3, acc) == 0
-    x = torch.full((3, 4), 0.5)                     # host tensors -> rejected
+    x = torch.full((3, 4), 0.5)                     # host and device arrays mixed -> rejected
     with pytest.raises(StError):
         micro_advance(cfg, x, x.clone(), torch.ones(4), torch.ones(4), torch.ones(4), F, 1e-3, 1, acc)
+
+
+def test_micro_host_arrays_equal_device_arrays():
+    """All-host arrays are staged through the device: the same results as device arrays."""
+    from paper_2603_26691_b200 import MicroConfig, micro_advance
+    mesh, F, x, u, d, T, w = _setup(3000)
+    props = M.MicroProps()
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 5e-3, (2,))
+    cfg = MicroConfig(dims=mesh.dims, origin=mesh.origin, cell_size=mesh.cell_size, bc=mesh.bc)
+    hx, hu, hd, hT = (np.ascontiguousarray(a).copy() for a in (x, u, d, T))
+    acc = np.zeros((5,) + tuple(reversed(mesh.dims)), np.float64)
+    micro_advance(cfg, hx, hu, hd, hT, np.ascontiguousarray(w), np.ascontiguousarray(F), 5e-3, 2, acc)
+    assert np.array_equal(hx, g[0]) and np.array_equal(hd, g[2]) and np.array_equal(hT, g[3])
+    assert np.allclose(acc.reshape(5, -1), g[4], rtol=1e-12, atol=1e-300 + 1e-9 * np.abs(g[4]).max())
 
 
 def test_micro_full_size_sampled():

@@ -44,7 +44,7 @@ def test_multigpu_matches_emulation(K, bcz, observe):
 
 
 def test_multigpu_far_tails_and_arrivals_in_boundary_bins():
-    """K = 3 in a flow fast along x and slow along z: far particles (C-15b) land in every
+    """K = 4 in a flow fast along x and slow along z: far particles (C-15b) land in every
     plane, the slab's boundary planes included, in the same rebin as arrivals from the
     neighbour ranks.  Each boundary bin must come out as local runs | arrivals | far tail
     (the oracle's (bin, far) sort of kept ++ arrivals), with no slot written twice."""
@@ -52,7 +52,7 @@ def test_multigpu_far_tails_and_arrivals_in_boundary_bins():
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(n, 4)
-    env = dict(os.environ, MR_K="3", MR_BCZ="1", MR_STEPS="7", MR_FIELD="xshear", MR_OBSERVE="end")
+    env = dict(os.environ, MR_K="4", MR_BCZ="1", MR_STEPS="9", MR_FIELD="xshear", MR_OBSERVE="end")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", "29770", os.path.join(ROOT, "tests", "mr_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
