@@ -384,6 +384,14 @@ def run_ours(args):
     # restricted to that box (inverse CDF)
     lo, hi = synth.domain_box(wl, z_range if args.decomp == "slab" else None)
     batch = 100_000_000
+    # st_inject is collective with nranks > 1 (slab decomposition): every rank makes the
+    # same number of calls, those with fewer particles pass n = 0
+    n_calls = (n_mine + batch - 1) // batch
+    if G > 1 and args.decomp == "slab":
+        t = torch.tensor([n_calls], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        for _ in range(int(t.item()) - n_calls):
+            st.inject(torch.empty((3, 0), device=dev), torch.empty((3, 0), device=dev), torch.empty(0, device=dev))
     for b0 in range(0, n_mine, batch):
         nb = min(batch, n_mine - b0)
         x, u, d, w = synth.particles_torch(nb, lo, hi, wl.d_range, wl.d_dist, wl.w,

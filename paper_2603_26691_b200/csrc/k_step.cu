@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
 // The slot-major layout makes consecutive threads touch consecutive words.
 // Destinations d >= nbins are the virtual bins of the neighbour planes (multi-GPU):
 // d = nbins + side * nvb + v.
+template <int SH>
 __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cnt_base, uint32_t* __restrict__ new_cnt,
                              const int* __restrict__ far_cnt) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
@@ -518,11 +519,11 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
     const int sy = axis_step(dy, -oy, g.n[1], g.bc[1], ok);
     const int sz = axis_step(dz, -oz, g.n[2], g.bc[2], ok);
     if (ok) {
-      const int kz = sz / g.cc;
+      const int kz = dcc<SH>(sz, g.cc);
       ok = kz >= kz_lo && kz < kz_hi &&                        // source on this rank
            slot_of<-1>(g, sx, sy, sz, dx, dy, dz) == j;          // canonical (no duplicate)
     }
-    key[j] = ok ? bin_of_cell<0>(g, bg, sx, sy, sz) : 0x7fffffff;
+    key[j] = ok ? bin_of_cell<SH>(g, bg, sx, sy, sz) : 0x7fffffff;
     cnt[j] = ok ? cnt_base[(int64_t)j * nbins + key[j]] : 0;
   }
   // stable order = ascending source bin: base of source q = sum of the counts of
@@ -547,34 +548,46 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
 // a neighbour rank's plane (the side is packed into bits 61-62), -1 if slot j leaves
 // the domain.  Row-major [nbins][27] so that one item (a chunk row of 8 bins) is one
 // contiguous 1728-byte bulk copy.
-__global__ void k_dbase(Geom g, BinGeom bg, int nbins, const int* __restrict__ base, const int64_t* __restrict__ off_new,
-                        const int64_t* __restrict__ voff0, const int64_t* __restrict__ voff1, long long* __restrict__ dtab,
-                        const int* __restrict__ far_cnt, unsigned long long* __restrict__ far_cur) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nbins) return;
-  if (far_cur) far_cur[s] = (unsigned long long)(off_new[s + 1] - far_cnt[s]);   // start of bin s's far tail
-  int sx, sy, sz;
-  cell_of_bin(g, bg, s, sx, sy, sz);
-  const bool cell_ok = sx < g.n[0] && sy < g.n[1] && sz < g.n[2];
-  for (int j = 0; j < kSlots; ++j) {
-    bool ok = cell_ok;
-    const int dx = axis_step(sx, j % 3 - 1, g.n[0], g.bc[0], ok);
-    const int dy = axis_step(sy, (j / 3) % 3 - 1, g.n[1], g.bc[1], ok);
-    const int dz = axis_step(sz, j / 9 - 1, g.n[2], g.bc[2], ok);
-    long long e = -1;
-    if (ok) {
-      const long long within = base[(int64_t)j * nbins + s];
-      if (bg.nvb > 0 && dz == bg.vz[0]) {
-        e = (voff0[vbin_of_cell<0>(g, dx, dy, g.cc)] + within) | (1LL << 61);
-      } else if (bg.nvb > 0 && dz == bg.vz[1]) {
-        e = (voff1[vbin_of_cell<0>(g, dx, dy, g.cc)] + within) | (2LL << 61);
-      } else {
-        const int kz = dz / g.cc;
-        if (kz >= bg.kz0 && kz < bg.kz0 + bg.nkz) e = off_new[bin_of_cell<0>(g, bg, dx, dy, dz)] + within;
+constexpr int kDbaseBlock = 128;
+template <int SH>
+__global__ void __launch_bounds__(kDbaseBlock) k_dbase(Geom g, BinGeom bg, int nbins, const int* __restrict__ base,
+                                                       const int64_t* __restrict__ off_new, const int64_t* __restrict__ voff0,
+                                                       const int64_t* __restrict__ voff1, long long* __restrict__ dtab,
+                                                       const int* __restrict__ far_cnt,
+                                                       unsigned long long* __restrict__ far_cur) {
+  // each thread builds its bin's 27-entry row in shared memory; the block then writes its
+  // 128 rows as one contiguous, coalesced run of 27 x 128 entries
+  __shared__ long long tile[kDbaseBlock * kSlots];
+  const int s0 = blockIdx.x * kDbaseBlock;
+  const int s = s0 + threadIdx.x;
+  if (s < nbins) {
+    if (far_cur) far_cur[s] = (unsigned long long)(off_new[s + 1] - far_cnt[s]);   // start of bin s's far tail
+    int sx, sy, sz;
+    cell_of_bin(g, bg, s, sx, sy, sz);
+    const bool cell_ok = sx < g.n[0] && sy < g.n[1] && sz < g.n[2];
+    for (int j = 0; j < kSlots; ++j) {
+      bool ok = cell_ok;
+      const int dx = axis_step(sx, j % 3 - 1, g.n[0], g.bc[0], ok);
+      const int dy = axis_step(sy, (j / 3) % 3 - 1, g.n[1], g.bc[1], ok);
+      const int dz = axis_step(sz, j / 9 - 1, g.n[2], g.bc[2], ok);
+      long long e = -1;
+      if (ok) {
+        const long long within = base[(int64_t)j * nbins + s];
+        if (bg.nvb > 0 && dz == bg.vz[0]) {
+          e = (voff0[vbin_of_cell<SH>(g, dx, dy, g.cc)] + within) | (1LL << 61);
+        } else if (bg.nvb > 0 && dz == bg.vz[1]) {
+          e = (voff1[vbin_of_cell<SH>(g, dx, dy, g.cc)] + within) | (2LL << 61);
+        } else {
+          const int kz = dcc<SH>(dz, g.cc);
+          if (kz >= bg.kz0 && kz < bg.kz0 + bg.nkz) e = off_new[bin_of_cell<SH>(g, bg, dx, dy, dz)] + within;
+        }
       }
+      tile[threadIdx.x * kSlots + j] = e;
     }
-    dtab[(int64_t)s * kSlots + j] = e;
   }
+  __syncthreads();
+  const int rows = min(kDbaseBlock, nbins - s0);
+  for (int k = threadIdx.x; k < rows * kSlots; k += kDbaseBlock) dtab[(int64_t)s0 * kSlots + k] = tile[k];
 }
 
 // Arrival counts from the neighbours land after the local runs of the boundary-plane
@@ -933,8 +946,12 @@ int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s) {
 
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, const int* far_cnt,
                       cudaStream_t s) {
-  k_rebin_prep<<<blocks_for((int64_t)bg.nbins + 2 * bg.nvb, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt,
-                                                                               far_cnt);
+  if (g.cc == 8)
+    k_rebin_prep<3><<<blocks_for((int64_t)bg.nbins + 2 * bg.nvb, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt,
+                                                                                  far_cnt);
+  else
+    k_rebin_prep<0><<<blocks_for((int64_t)bg.nbins + 2 * bg.nvb, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt,
+                                                                                  far_cnt);
   return 1;
 }
 
@@ -974,7 +991,12 @@ int launch_count_v(const CountArgs& a, cudaStream_t s) {
 
 int launch_dbase(const Geom& g, const BinGeom& bg, const int* base, const int64_t* off_new, const int64_t* voff0,
                  const int64_t* voff1, long long* dtab, const int* far_cnt, unsigned long long* far_cur, cudaStream_t s) {
-  k_dbase<<<blocks_for(bg.nbins), 256, 0, s>>>(g, bg, bg.nbins, base, off_new, voff0, voff1, dtab, far_cnt, far_cur);
+  if (g.cc == 8)
+    k_dbase<3><<<blocks_for(bg.nbins, kDbaseBlock), kDbaseBlock, 0, s>>>(g, bg, bg.nbins, base, off_new, voff0, voff1,
+                                                                        dtab, far_cnt, far_cur);
+  else
+    k_dbase<0><<<blocks_for(bg.nbins, kDbaseBlock), kDbaseBlock, 0, s>>>(g, bg, bg.nbins, base, off_new, voff0, voff1,
+                                                                        dtab, far_cnt, far_cur);
   return 1;
 }
 

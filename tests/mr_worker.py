@@ -122,7 +122,8 @@ def main():
             if same_set:
                 og, oo = np.argsort(pg["id"]), np.argsort(po["id"])
                 worst_x = max(worst_x, float(np.max(np.abs(pg["x"][:, og].astype(np.float64) - po["x"][:, oo])) / max(L)))
-                worst_u = max(worst_u, float(np.max(np.abs(pg["u"][:, og].astype(np.float64) - po["u"][:, oo]))))
+                U = max(1.0, float(np.max(np.abs(F))))       # velocities relative to the field's speed
+                worst_u = max(worst_u, float(np.max(np.abs(pg["u"][:, og].astype(np.float64) - po["u"][:, oo]))) / U)
             # the last call ended with a rebin (flushed by the observation): the store is
             # sorted by the bin key of its own positions and owned (else it is sorted by
             # the positions of the previous rebin and advanced since: nothing to check)
