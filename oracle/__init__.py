@@ -17,8 +17,9 @@ inject -> set fluid field -> advance(dt, nsteps) -> get sources, with
   cell is more than one cell (per axis, periodic-aware) from the cell of its home bin
   (the bin it was sorted into at the previous rebin) is "far"; the sort key is then
   (bin key, far), i.e. within every bin the near particles in their prior order,
-  then the far ones in their prior order.  In a multi-rank job a far particle whose
-  cell is owned by another rank makes every rank take the plain sort;
+  then the far ones in their prior order (arrivals from other ranks after the kept,
+  C-16).  At K = 1 in a multi-rank job a far particle whose cell is owned by another
+  rank makes every rank take the plain sort;
 * the R-rank emulation rule C-16: rank r owns chunk planes
   [floor(r*NCz/R), floor((r+1)*NCz/R)); at a rebin every rank keeps its own
   particles in order, appends arrivals in ascending source rank (each in the
@@ -373,13 +374,16 @@ class Sim:
                 idx = np.nonzero(own == dst)[0]
                 parts[src][dst] = idx
                 M[src, dst] = idx.size
-        # C-15b applies when every rank's store is binned and no far particle leaves its rank
+        # C-15b applies when every rank's store is binned; a far particle that changes rank
+        # is placed in the receiver's far tail when the rebin's counts come from the
+        # in-place step of the call that made it due (K >= 2); at K = 1 (counts from a
+        # separate pass over the store) it makes every rank take the plain sort
         fused = int(self.mesh.chunk_cells) == 8 and all(h is not None for h in self.home)
         if fused:
             for src, s in enumerate(self.stores):
                 f = self.far_mask(self.home[src], s.x) if s.n else np.zeros(0, bool)
                 fars.append(f)
-                if np.any(f & (owners[src] != src)):
+                if self.rebin_interval == 1 and np.any(f & (owners[src] != src)):
                     fused = False
         self.last_far = int(sum(int(f.sum()) for f in fars)) if fused else 0
         new, homes = [], []

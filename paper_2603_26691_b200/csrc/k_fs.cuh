@@ -189,12 +189,17 @@ __global__ void __launch_bounds__(32 * kFsWarps, 2) k_fs(const __grid_constant__
           flags |= ERRF_SCATTER;
           ok = false;
         }
-        int fdest = -1;
+        int fdest = -1, fside = -1;
         if (ok && farp) {   // C-15b: the next slot of the destination bin's tail (k_far_order sorts it)
           const int kz = c[q][2] >> SH;
+          int pl;
           if (a.far_cur && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
             fdest = (int)atomicAdd(a.far_cur + bin_of_cell<SH>(g, a.bg, c[q][0], c[q][1], c[q][2]), 1ULL);
             a.far_src[fdest] = (int32_t)(p0 + r[q]);
+          } else if (VP && a.fs_cur && far_plane(g, c[q][2], fside, pl)) {
+            // a neighbour rank's cell: the far region of the send buffer, keyed by prior index
+            fdest = (int)atomicAdd(a.fs_cur + fside, 1ULL);
+            if ((int64_t)fdest < a.scap) a.fs_key[fside][fdest] = (int32_t)(p0 + r[q]);
           } else {
             flags |= ERRF_SCATTER;
             ok = false;
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(32 * kFsWarps, 2) k_fs(const __grid_constant__
           }
           __syncwarp();
         }
-        if (VP) vside[q] = (farp || e < 0) ? -1 : (int)(e >> 61) - 1;
+        if (VP) vside[q] = farp ? fside : (e < 0 ? -1 : (int)(e >> 61) - 1);
         const long long dl = farp ? (long long)fdest : db + rank;
         if (ok && (uint64_t)dl >= (uint64_t)((VP && vside[q] >= 0) ? a.scap : a.n)) {
           flags |= ERRF_SCATTER;

@@ -331,8 +331,14 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
             atomicAdd(&cnt_s[lb[q] * kSlots + j], 1);
           } else {   // far (C-15b): counted for the bin of its cell when that is on this rank
             const int kz = e2 >> SH;
+            int side, pl;
             if (a.cnt_far_cnt && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
               atomicAdd(a.cnt_far_cnt + bin_of_cell<SH>(g, a.bg, e0, e1, e2), 1);
+              atomicAdd(a.cnt_far_n, 1ULL);
+            } else if (VP && a.cnt_fv[0] && far_plane(g, e2, side, pl)) {
+              // a neighbour rank's cell: counted per cell of its window (k_far_accept there)
+              atomicAdd(a.cnt_fv[side] + ((int64_t)pl * g.n[1] + e1) * g.n[0] + e0, 1);
+              atomicAdd(a.cnt_fs_n + side, 1ULL);
               atomicAdd(a.cnt_far_n, 1ULL);
             } else {
               cfar = 1;

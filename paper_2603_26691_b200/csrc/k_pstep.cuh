@@ -311,12 +311,17 @@ __global__ void __launch_bounds__(32 * pwarps(SCATTER && ADVANCE), (SCATTER && A
           write_ok = false;
         }
         long long fdest = -1;
+        int fside = -1;
         if (valid && farp) {
           // C-15b: a far particle takes the next slot of its destination bin's tail
           const int kz = c2 >> SH;
+          int pl;
           if (a.far_cur && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
             fdest = (long long)atomicAdd(a.far_cur + bin_of_cell<SH>(g, a.bg, c0, c1, c2), 1ULL);
             a.far_src[fdest] = (int32_t)(p0 + r);   // prior index: k_far_order sorts the tail by it
+          } else if (VP && a.fs_cur && far_plane(g, c2, fside, pl)) {
+            fdest = (long long)atomicAdd(a.fs_cur + fside, 1ULL);   // neighbour rank: far send region
+            if (fdest < a.scap) a.fs_key[fside][fdest] = (int32_t)(p0 + r);
           } else {
             flags |= ERRF_SCATTER;
             write_ok = false;
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(32 * pwarps(SCATTER && ADVANCE), (SCATTER && A
           rbase = __shfl_sync(peers, rb0, leader) + __popc(peers & lt);
         }
         __syncwarp();
-        if (VP) vside = (farp || e < 0) ? -1 : (int)(e >> 61) - 1;
+        if (VP) vside = farp ? fside : (e < 0 ? -1 : (int)(e >> 61) - 1);
         dest = farp ? fdest : db + rbase;
         if (write_ok && (uint64_t)dest >= (uint64_t)((VP && vside >= 0) ? a.scap : a.n)) {
           flags |= ERRF_SCATTER;

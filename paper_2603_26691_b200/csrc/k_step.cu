@@ -207,6 +207,29 @@ __device__ __forceinline__ int axis_step(int from, int d, int n, int bc, bool& o
   return t;
 }
 
+// A cell plane beyond this rank's slab within chunk_cells planes (a neighbour's window):
+// side 0 = below z0 (p planes below), side 1 = at / above z1 (p planes above); periodic z
+// wraps.  false: not within reach (the displacement precondition C-23 is violated).
+__device__ __forceinline__ bool far_plane(const Geom& g, int z, int& side, int& p) {
+  const int nz = g.n[2];
+  int below = g.oz0 - 1 - z, above = z - g.oz1;
+  if (g.bc[2] == ST_BC_PERIODIC) {
+    below = ((below % nz) + nz) % nz;
+    above = ((above % nz) + nz) % nz;
+  }
+  if (below >= 0 && below < g.cc) {
+    side = 0;
+    p = below;
+    return true;
+  }
+  if (above >= 0 && above < g.cc) {
+    side = 1;
+    p = above;
+    return true;
+  }
+  return false;
+}
+
 // ---------------------------------------------------------------- warp reductions
 __device__ __forceinline__ void group_sum3(bool member, float& a, float& b, float& c) {
   if (!member) a = b = c = 0.0f;
@@ -959,6 +982,89 @@ int launch_vcombine(const Geom& g, const BinGeom& bg, uint32_t* new_cnt, const u
                     uint32_t* kept_dn, uint32_t* kept_up, int oz0, int oz1, const int* far_cnt, cudaStream_t s) {
   if (bg.nvb <= 0) return 0;
   k_vcombine<<<blocks_for(bg.nvb), 256, 0, s>>>(g, bg, new_cnt, rcnt_dn, rcnt_up, kept_dn, kept_up, oz0, oz1, far_cnt);
+  return 1;
+}
+
+// The receiver of far particles across ranks: counts per cell of my first / last
+// chunk_cells planes (rfv0 from the rank below: planes z0 + p; rfv1 from the rank above:
+// planes z1 - 1 - p) join the far tails of their bins.
+__global__ void k_far_accept(Geom g, BinGeom bg, const int* __restrict__ rfv0, const int* __restrict__ rfv1, int z0,
+                             int z1, uint32_t* __restrict__ new_cnt, int* __restrict__ far_cnt,
+                             unsigned long long* __restrict__ fr_n, int* __restrict__ err) {
+  const int64_t plane = (int64_t)g.n[0] * g.n[1];
+  const int64_t nf = plane * g.cc;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * nf) return;
+  const int side = (int)(i / nf);
+  const int64_t v = i - side * nf;
+  const int cnt = (side ? rfv1 : rfv0)[v];
+  if (!cnt) return;
+  const int p = (int)(v / plane);
+  const int y = (int)((v % plane) / g.n[0]), x = (int)(v % g.n[0]);
+  const int z = side ? z1 - 1 - p : z0 + p;
+  const int kz = z / g.cc;
+  if (z < z0 || z >= z1 || kz < bg.kz0 || kz >= bg.kz0 + bg.nkz) {
+    atomicOr(err, ERRF_SCATTER);
+    return;
+  }
+  const int b = bin_of_cell<0>(g, bg, x, y, z);
+  atomicAdd(new_cnt + b, (uint32_t)cnt);
+  atomicAdd(far_cnt + b, cnt);
+  atomicAdd(fr_n + side, (unsigned long long)cnt);
+}
+
+// Far arrivals of one side (sorted by sender key) into the far tails of B: slot by the
+// bin's cursor, key n_old + rank in (source rank, sender key) order (k_far_order).
+__global__ void k_far_insert(FarInsertArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.count) return;
+  const Store& r = a.r;
+  const int64_t rc = a.rcap;
+  float x[3];
+  int c[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    x[ax] = r.x[ax * rc + i];
+    c[ax] = cell_from_t(cell_coord(x[ax], a.g.lo[ax], a.g.ih[ax]), a.g.n[ax]);
+  }
+  const int kz = c[2] / a.g.cc;
+  if (kz < a.bg.kz0 || kz >= a.bg.kz0 + a.bg.nkz) {
+    atomicOr(a.err, ERRF_SCATTER);
+    return;
+  }
+  const int b = bin_of_cell<0>(a.g, a.bg, c[0], c[1], c[2]);
+  const int64_t slot = (int64_t)atomicAdd(a.far_cur + b, 1ULL);
+  int64_t rank = i;
+  if (a.merge) {   // both sides from the same rank: rank in the merged sender order
+    const int32_t k = a.key[i];
+    int64_t lo = 0, hi = a.other_count;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (a.other_key[mid] < k) lo = mid + 1;
+      else hi = mid;
+    }
+    rank += lo;
+  }
+  a.far_src[slot] = (int32_t)(a.base + rank);
+  const int64_t cap = a.cap;
+  for (int ax = 0; ax < 3; ++ax) {
+    a.B.x[ax * cap + slot] = x[ax];
+    a.B.u[ax * cap + slot] = r.u[ax * rc + i];
+  }
+  a.B.d[slot] = r.d[i];
+  a.B.w[slot] = r.w[i];
+  a.B.id[slot] = r.id[i];
+}
+
+int launch_far_accept(const Geom& g, const BinGeom& bg, const int* rfv0, const int* rfv1, int z0, int z1,
+                      uint32_t* new_cnt, int* far_cnt, unsigned long long* fr_n, int* err, cudaStream_t s) {
+  const int64_t nf = (int64_t)g.n[0] * g.n[1] * g.cc;
+  k_far_accept<<<blocks_for(2 * nf), 256, 0, s>>>(g, bg, rfv0, rfv1, z0, z1, new_cnt, far_cnt, fr_n, err);
+  return 1;
+}
+
+int launch_far_insert(const FarInsertArgs& a, cudaStream_t s) {
+  if (a.count <= 0) return 0;
+  k_far_insert<<<blocks_for(a.count), 256, 0, s>>>(a);
   return 1;
 }
 

@@ -91,6 +91,16 @@ struct st_ctx {
   uint32_t* kept[2] = {nullptr, nullptr};   // [nvb]
   Store sbuf[2], rbuf[2];
   int64_t scap = 0;
+  // far particles across ranks (C-15b): per neighbour-window cell counts (send / received),
+  // d_fs = [counted per side 2 | scatter cursors 2 | received per side 2], keys of the far
+  // region of each send buffer and of each receive buffer (+ a sort ping-pong)
+  int* fv[2] = {nullptr, nullptr};
+  int* rfv[2] = {nullptr, nullptr};
+  int64_t nfv = 0;
+  unsigned long long* d_fs = nullptr;
+  int32_t* fs_key[2] = {nullptr, nullptr};
+  int32_t* fr_key[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int64_t* h_fs = nullptr;   // pinned [4]: far sent lo / hi, far received dn / up
   int64_t* h_tot = nullptr;                 // pinned: send_lo, send_hi, recv_dn, recv_up
   int* h_farg = nullptr;                    // pinned: global far flag
   int* d_farg = nullptr;
@@ -554,6 +564,20 @@ static st_status init_impl(st_ctx* c) {
       if (s2) return s2;
     }
     ST_CUDA(c, cudaHostAlloc(&c->h_tot, 4 * sizeof(int64_t), cudaHostAllocDefault));
+    if (c->dtab) {   // 8^3 chunks: far particles across ranks stay on the fused path
+      c->nfv = (int64_t)g.n[0] * g.n[1] * g.cc;
+      for (int i = 0; i < 2; ++i) {
+        ST_CUDA(c, cudaMalloc(&c->fv[i], c->nfv * sizeof(int)));
+        ST_CUDA(c, cudaMemset(c->fv[i], 0, c->nfv * sizeof(int)));
+        ST_CUDA(c, cudaMalloc(&c->rfv[i], c->nfv * sizeof(int)));
+        ST_CUDA(c, cudaMemset(c->rfv[i], 0, c->nfv * sizeof(int)));   // stays 0 where no neighbour
+        ST_CUDA(c, cudaMalloc(&c->fs_key[i], c->scap * sizeof(int32_t)));
+        for (int k = 0; k < 2; ++k) ST_CUDA(c, cudaMalloc(&c->fr_key[i][k], c->scap * sizeof(int32_t)));
+      }
+      ST_CUDA(c, cudaMalloc(&c->d_fs, 6 * sizeof(unsigned long long)));
+      ST_CUDA(c, cudaMemset(c->d_fs, 0, 6 * sizeof(unsigned long long)));
+      ST_CUDA(c, cudaHostAlloc(&c->h_fs, 4 * sizeof(int64_t), cudaHostAllocDefault));
+    }
     ST_CUDA(c, cudaEventCreateWithFlags(&c->ev_tot, cudaEventDisableTiming));
   }
   ST_CUDA(c, cudaMalloc(&c->item_flag, (nb + 1) * sizeof(uint32_t)));
@@ -633,6 +657,14 @@ st_status st_destroy(st_ctx* c) {
     cudaFree(c->rbuf[i].base);
   }
   if (c->h_tot) cudaFreeHost(c->h_tot);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c->fv[i]);
+    cudaFree(c->rfv[i]);
+    cudaFree(c->fs_key[i]);
+    for (int k = 0; k < 2; ++k) cudaFree(c->fr_key[i][k]);
+  }
+  cudaFree(c->d_fs);
+  if (c->h_fs) cudaFreeHost(c->h_fs);
   if (c->h_farg) cudaFreeHost(c->h_farg);
   cudaFree(c->d_farg);
   if (c->ev_tot) cudaEventDestroy(c->ev_tot);
@@ -969,6 +1001,10 @@ static st_status count_slots(st_ctx* c, bool* far) {
   if (c->comm) {
     ST_CUDA(c, cudaMemsetAsync(c->d_farg, 0, sizeof(int), c->cs));
     ca.far = c->d_farg;
+    if (c->fv[0]) {   // k_count does not place far particles across ranks (they force the general path)
+      for (int i = 0; i < 2; ++i) ST_CUDA(c, cudaMemsetAsync(c->fv[i], 0, c->nfv * sizeof(int), c->cs));
+      ST_CUDA(c, cudaMemsetAsync(c->d_fs, 0, 2 * sizeof(unsigned long long), c->cs));
+    }
   } else if (c->far_cnt) {
     ca.far = c->d_farg;             // never set on one rank with far tails: not read back
   } else {
@@ -1020,8 +1056,13 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     nl = 0;
     std::string why;
     if (comm_rebin_counts(c->comm, c->new_cnt + nb, c->new_cnt + nb + nv, c->rcnt[0], c->rcnt[1], nv, c->d_farg,
-                          g.bc[2] == ST_BC_PERIODIC, c->cs, why))
+                          g.bc[2] == ST_BC_PERIODIC, c->cs, why, c->fv[0], c->fv[1], c->rfv[0], c->rfv[1], c->nfv))
       return fail(c, ST_ERR_NCCL, why);
+    if (c->fv[0]) {   // far arrivals from the neighbours join the far tails of their bins
+      ST_CUDA(c, cudaMemsetAsync(c->d_fs + 4, 0, 2 * sizeof(unsigned long long), c->cs));
+      nl += launch_far_accept(g, c->bg, c->rfv[0], c->rfv[1], c->z0, c->z1, c->new_cnt, c->far_cnt, c->d_fs + 4,
+                              c->d_err, c->cs);
+    }
     nl += launch_vcombine(g, c->bg, c->new_cnt, c->rcnt[0], c->rcnt[1], c->kept[0], c->kept[1], c->z0, c->z1,
                           c->far_cnt, c->cs);
     nl += launch_exclusive_scan_u32(c->new_cnt + nb, nv, c->voff[0], c->sc.partial, c->cs);
@@ -1033,6 +1074,13 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     ST_CUDA(c, cudaMemcpyAsync(c->h_tot + 2, c->roff[0] + nv, sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
     ST_CUDA(c, cudaMemcpyAsync(c->h_tot + 3, c->roff[1] + nv, sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
     ST_CUDA(c, cudaMemcpyAsync(c->h_farg, c->d_farg, sizeof(int), cudaMemcpyDeviceToHost, c->cs));
+    if (c->fv[0]) {
+      // far send cursors start after the near movers of each send buffer
+      for (int i = 0; i < 2; ++i)
+        ST_CUDA(c, cudaMemcpyAsync(c->d_fs + 2 + i, c->voff[i] + nv, sizeof(int64_t), cudaMemcpyDeviceToDevice, c->cs));
+      ST_CUDA(c, cudaMemcpyAsync(c->h_fs, c->d_fs, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
+      ST_CUDA(c, cudaMemcpyAsync(c->h_fs + 2, c->d_fs + 4, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->cs));
+    }
     ST_CUDA(c, cudaEventRecord(c->ev_tot, c->cs));
   }
   nl += launch_exclusive_scan_u32(c->new_cnt, nb, c->off[nlay], c->sc.partial, c->cs);
@@ -1051,10 +1099,13 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
       *fell_back = true;
       return general_rebin(c);
     }
+    const int64_t fs0 = c->fv[0] ? c->h_fs[0] : 0, fs1 = c->fv[0] ? c->h_fs[1] : 0;
+    const int64_t fr0 = c->fv[0] ? c->h_fs[2] : 0, fr1 = c->fv[0] ? c->h_fs[3] : 0;
     int bad = 0;
-    for (int k = 0; k < 4; ++k)
-      if (c->h_tot[k] > c->scap) bad |= 1;
-    n_new = c->n - c->h_tot[0] - c->h_tot[1] + c->h_tot[2] + c->h_tot[3];
+    if (c->h_tot[0] + fs0 > c->scap || c->h_tot[1] + fs1 > c->scap || c->h_tot[2] + fr0 > c->scap ||
+        c->h_tot[3] + fr1 > c->scap)
+      bad |= 1;
+    n_new = c->n - c->h_tot[0] - c->h_tot[1] - fs0 - fs1 + c->h_tot[2] + c->h_tot[3] + fr0 + fr1;
     if (n_new > c->cfg.capacity) bad |= 2;
     // every rank must take the same branch before the payload exchange (else the ranks
     // that did not fail would wait in ncclSend/Recv for ones that returned)
@@ -1064,12 +1115,24 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   }
   StepArgs a = step_args(c, dt, nsteps);
   a.n = n_new;
+  if (c->comm && c->fv[0]) {
+    a.fs_cur = c->d_fs + 2;
+    a.fs_key[0] = c->fs_key[0];
+    a.fs_key[1] = c->fs_key[1];
+  }
   if (advance) ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
   if ((s = check_launch(c, launch_step(a, true, advance, c->cs)))) return s;
   if (c->comm) {
     std::string why;
-    if (comm_rebin_payload(c->comm, c->sbuf, c->scap, c->h_tot[0], c->h_tot[1], c->rbuf, c->scap, c->h_tot[2],
-                           c->h_tot[3], g.bc[2] == ST_BC_PERIODIC, c->cs, why))
+    const int64_t fs0 = c->fv[0] ? c->h_fs[0] : 0, fs1 = c->fv[0] ? c->h_fs[1] : 0;
+    const int64_t fr0 = c->fv[0] ? c->h_fs[2] : 0, fr1 = c->fv[0] ? c->h_fs[3] : 0;
+    // near movers then far movers of each side in one payload (the far region follows)
+    if (comm_rebin_payload(c->comm, c->sbuf, c->scap, c->h_tot[0] + fs0, c->h_tot[1] + fs1, c->rbuf, c->scap,
+                           c->h_tot[2] + fr0, c->h_tot[3] + fr1, g.bc[2] == ST_BC_PERIODIC, c->cs, why))
+      return fail(c, ST_ERR_NCCL, why);
+    if (c->fv[0] && (fs0 + fs1 + fr0 + fr1) > 0 &&
+        comm_far_keys(c->comm, c->fs_key[0] + c->h_tot[0], fs0, c->fs_key[1] + c->h_tot[1], fs1, c->fr_key[0][0], fr0,
+                      c->fr_key[1][0], fr1, g.bc[2] == ST_BC_PERIODIC, c->cs, why))
       return fail(c, ST_ERR_NCCL, why);
     nl = 0;
     for (int side = 0; side < 2; ++side) {
@@ -1091,15 +1154,64 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
       nl += launch_insert(ia, c->cs);
     }
     if ((s = check_launch(c, nl))) return s;
-    c->mig_row.assign(c->cfg.nranks, 0);
     const int G = c->cfg.nranks, r = c->cfg.rank;
     const bool pz = g.bc[2] == ST_BC_PERIODIC;
     const int up = (r + 1 < G) ? r + 1 : (pz ? 0 : -1), dn = (r > 0) ? r - 1 : (pz ? G - 1 : -1);
-    if (up >= 0) c->mig_row[up] += c->h_tot[1];
-    if (dn >= 0) c->mig_row[dn] += c->h_tot[0];
-    c->mig_row[r] = c->n - c->h_tot[0] - c->h_tot[1];
-    c->last_sent = c->h_tot[0] + c->h_tot[1];
-    c->last_recv = c->h_tot[2] + c->h_tot[3];
+    if (fr0 + fr1 > 0) {
+      // far arrivals: each side's block sorted by sender key (the sender's store order),
+      // then into the far tails with keys n_old + rank in (source rank, sender order)
+      Store sorted[2];
+      const int32_t* skey[2] = {c->fr_key[0][0], c->fr_key[1][0]};
+      const int64_t fr[2] = {fr0, fr1};
+      for (int side = 0; side < 2; ++side) {
+        Store a0 = c->rbuf[side], b0 = c->sbuf[side];
+        const int64_t o = c->h_tot[2 + side];   // the far block follows the near arrivals
+        a0.x += o; a0.u += o; a0.d += o; a0.w += o; a0.id += o;
+        sorted[side] = a0;
+        if (fr[side] > 1) {
+          int in_b = 0;
+          const int ns = launch_stable_sort(a0, b0, c->scap, fr[side], c->fr_key[side][0], c->fr_key[side][1], 31,
+                                            c->sc, &in_b, c->cs);
+          if (ns < 0) return fail(c, ST_ERR_CAPACITY, "sort scratch too small (far arrivals)");
+          if ((s = check_launch(c, ns))) return s;
+          if (in_b) {
+            sorted[side] = b0;
+            skey[side] = c->fr_key[side][1];
+          }
+        }
+      }
+      const bool same = dn == up;               // two ranks, periodic: both blocks from one rank
+      nl = 0;
+      for (int side = 0; side < 2; ++side) {
+        if (!fr[side]) continue;
+        FarInsertArgs fa;
+        memset(&fa, 0, sizeof(fa));
+        fa.g = g;
+        fa.bg = c->bg;
+        fa.r = sorted[side];
+        fa.rcap = c->scap;
+        fa.count = fr[side];
+        fa.key = skey[side];
+        fa.other_key = skey[1 - side];
+        fa.other_count = fr[1 - side];
+        fa.merge = same ? 1 : 0;
+        const int src = side == 0 ? dn : up, other = side == 0 ? up : dn;
+        fa.base = c->n + (same ? 0 : (src < other ? 0 : fr[1 - side]));   // ascending source rank (C-16)
+        fa.far_cur = c->far_cur;
+        fa.far_src = c->key[0];
+        fa.B = c->S[1 - c->cur];
+        fa.cap = c->cap;
+        fa.err = c->d_err;
+        nl += launch_far_insert(fa, c->cs);
+      }
+      if ((s = check_launch(c, nl))) return s;
+    }
+    c->mig_row.assign(c->cfg.nranks, 0);
+    if (up >= 0) c->mig_row[up] += c->h_tot[1] + fs1;
+    if (dn >= 0) c->mig_row[dn] += c->h_tot[0] + fs0;
+    c->mig_row[r] = c->n - c->h_tot[0] - c->h_tot[1] - fs0 - fs1;
+    c->last_sent = c->h_tot[0] + c->h_tot[1] + fs0 + fs1;
+    c->last_recv = c->h_tot[2] + c->h_tot[3] + fr0 + fr1;
     c->n = n_new;
   } else {
     c->mig_row[0] = c->n;
@@ -1177,6 +1289,14 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
         ST_CUDA(c, cudaMemsetAsync(c->far_cnt, 0, (size_t)c->bg.nbins * sizeof(int), c->cs));
         if (c->comm) {
           ST_CUDA(c, cudaMemsetAsync(c->d_farg, 0, sizeof(int), c->cs));
+          if (c->fv[0]) {   // far particles into a neighbour's window: counted per cell
+            for (int i = 0; i < 2; ++i) {
+              ST_CUDA(c, cudaMemsetAsync(c->fv[i], 0, c->nfv * sizeof(int), c->cs));
+              a.cnt_fv[i] = c->fv[i];
+            }
+            ST_CUDA(c, cudaMemsetAsync(c->d_fs, 0, 2 * sizeof(unsigned long long), c->cs));
+            a.cnt_fs_n = c->d_fs;
+          }
         }
         a.cnt_far = c->d_farg;      // one rank: never set (8^3 chunks place every far particle)
         a.cnt_hist = c->hist;

@@ -382,7 +382,8 @@ int recv_store(Comm* c, const Store& b, int64_t cap, int64_t n, int peer, std::s
 }  // namespace
 
 int comm_rebin_counts(Comm* c, const uint32_t* vcnt_lo, const uint32_t* vcnt_hi, uint32_t* rcnt_dn, uint32_t* rcnt_up,
-                      int nvb, int* d_far, bool periodic, cudaStream_t s, std::string& why) {
+                      int nvb, int* d_far, bool periodic, cudaStream_t s, std::string& why, const int* fv_lo,
+                      const int* fv_hi, int* rfv_dn, int* rfv_up, int64_t nf) {
   int up, dn;
   neighbours(c, periodic, up, dn);
   if (join_in(c, s, why)) return 1;
@@ -392,6 +393,26 @@ int comm_rebin_counts(Comm* c, const uint32_t* vcnt_lo, const uint32_t* vcnt_hi,
   if (dn >= 0) NCCK(ncclSend(vcnt_lo, nvb, ncclUint32, dn, c->nc, c->ns), why);
   if (dn >= 0) NCCK(ncclRecv(rcnt_dn, nvb, ncclUint32, dn, c->nc, c->ns), why);
   if (up >= 0) NCCK(ncclRecv(rcnt_up, nvb, ncclUint32, up, c->nc, c->ns), why);
+  if (nf > 0) {
+    if (up >= 0) NCCK(ncclSend(fv_hi, nf, ncclInt32, up, c->nc, c->ns), why);
+    if (dn >= 0) NCCK(ncclSend(fv_lo, nf, ncclInt32, dn, c->nc, c->ns), why);
+    if (dn >= 0) NCCK(ncclRecv(rfv_dn, nf, ncclInt32, dn, c->nc, c->ns), why);
+    if (up >= 0) NCCK(ncclRecv(rfv_up, nf, ncclInt32, up, c->nc, c->ns), why);
+  }
+  NCCK(ncclGroupEnd(), why);
+  return join_out(c, s, why);
+}
+
+int comm_far_keys(Comm* c, const int32_t* klo, int64_t send_lo, const int32_t* khi, int64_t send_hi, int32_t* kdn,
+                  int64_t recv_dn, int32_t* kup, int64_t recv_up, bool periodic, cudaStream_t s, std::string& why) {
+  int up, dn;
+  neighbours(c, periodic, up, dn);
+  if (join_in(c, s, why)) return 1;
+  NCCK(ncclGroupStart(), why);
+  if (up >= 0 && send_hi > 0) NCCK(ncclSend(khi, send_hi, ncclInt32, up, c->nc, c->ns), why);
+  if (dn >= 0 && send_lo > 0) NCCK(ncclSend(klo, send_lo, ncclInt32, dn, c->nc, c->ns), why);
+  if (dn >= 0 && recv_dn > 0) NCCK(ncclRecv(kdn, recv_dn, ncclInt32, dn, c->nc, c->ns), why);
+  if (up >= 0 && recv_up > 0) NCCK(ncclRecv(kup, recv_up, ncclInt32, up, c->nc, c->ns), why);
   NCCK(ncclGroupEnd(), why);
   return join_out(c, s, why);
 }

@@ -72,8 +72,15 @@ int comm_migrate(Comm* c, const Geom& g, Store* S, int* cur, int32_t** key, int6
 // plane above) -> upper neighbour, vcnt_lo -> lower neighbour; rcnt_dn receives
 // the lower neighbour's counts for my bottom plane, rcnt_up the upper's for my
 // top plane.  Missing neighbours (walls) leave the receive arrays untouched.
+// fv_lo / fv_hi (nf ints each, or NULL): far particles per cell of the lower / upper
+// neighbour's window, exchanged the same way into rfv_dn / rfv_up.
 int comm_rebin_counts(Comm* c, const uint32_t* vcnt_lo, const uint32_t* vcnt_hi, uint32_t* rcnt_dn, uint32_t* rcnt_up,
-                      int nvb, int* d_far, bool periodic, cudaStream_t s, std::string& why);
+                      int nvb, int* d_far, bool periodic, cudaStream_t s, std::string& why, const int* fv_lo = nullptr,
+                      const int* fv_hi = nullptr, int* rfv_dn = nullptr, int* rfv_up = nullptr, int64_t nf = 0);
+// Keys of the far movers: send_lo keys from klo -> down, send_hi from khi -> up; recv_dn
+// keys <- down into kdn, recv_up <- up into kup.
+int comm_far_keys(Comm* c, const int32_t* klo, int64_t send_lo, const int32_t* khi, int64_t send_hi, int32_t* kdn,
+                  int64_t recv_dn, int32_t* kup, int64_t recv_up, bool periodic, cudaStream_t s, std::string& why);
 // Payload of the movers: sbuf[1] (send_hi particles) -> up, sbuf[0] (send_lo) ->
 // down; rbuf[0] <- down (recv_dn), rbuf[1] <- up (recv_up).  SoA x,u,d,w,id.
 int comm_rebin_payload(Comm* c, const Store* sbuf, int64_t scap, int64_t send_lo, int64_t send_hi, const Store* rbuf,

@@ -44,6 +44,15 @@ struct StepArgs {
   unsigned long long* far_cur;// [nbins] next free slot of each bin's far tail (C-15b), or NULL
   int32_t* far_src;           // [cap] by new-layout slot: old-layout index of a far particle
                               // (k_far_order sorts each tail by it: prior order, C-15b)
+  // multi-GPU far particles whose cell lies in a neighbour rank's slab (C-15b across ranks):
+  // the scatter appends them to the far region of sbuf[side] (after the near movers),
+  // fs_cur[side] = next free slot, fs_key[side][slot] = prior index (the receiver sorts by it)
+  unsigned long long* fs_cur; // [2] or NULL: such a particle is an error (general path taken)
+  int32_t* fs_key[2];
+  // ... and the in-place counting step counts them per cell of the neighbour's first
+  // chunk_cells planes: cnt_fv[side][(p * ny + y) * nx + x], p = planes beyond the slab
+  int* cnt_fv[2];             // or NULL: such a particle sets *cnt_far (general path)
+  unsigned long long* cnt_fs_n;   // [2] totals per side
   // slot histogram produced by an in-place step whose call makes a rebin due (k_count's
   // outputs, same meaning; cnt_hist == NULL: not produced by this launch)
   int* cnt_hist;
@@ -108,6 +117,28 @@ struct CountArgs {
   unsigned long long* movers; // += particles whose current chunk differs from their bin's chunk
   unsigned long long* far_n;  // += far particles placed in bin tails
 };
+// far particles across ranks (see StepArgs::fs_cur): the receiver adds the exchanged
+// per-cell counts to its bins (new_cnt and far_cnt) and totals them per side
+int launch_far_accept(const Geom& g, const BinGeom& bg, const int* rfv0, const int* rfv1, int z0, int z1,
+                      uint32_t* new_cnt, int* far_cnt, unsigned long long* fr_n, int* err, cudaStream_t s);
+// ... and puts the sorted far arrivals of one side into the far tails of B
+struct FarInsertArgs {
+  Geom g;
+  BinGeom bg;
+  Store r;                    // sorted far arrivals of this side (stride rcap)
+  int64_t rcap, count;
+  const int32_t* key;         // their sender keys (sorted), and the other side's
+  const int32_t* other_key;
+  int64_t other_count;
+  int64_t base;               // n_old + position of this side's block in (source rank, key) order
+  int merge;                  // 1: both sides come from the same rank: rank by merging keys
+  unsigned long long* far_cur;
+  int32_t* far_src;
+  Store B;
+  int64_t cap;
+  int* err;
+};
+int launch_far_insert(const FarInsertArgs& a, cudaStream_t s);
 int launch_count(const CountArgs& a, cudaStream_t s);
 // destination table [nbins][27] of k_pstep from the prep bases and the new offsets
 int launch_dbase(const Geom& g, const BinGeom& bg, const int* base, const int64_t* off_new, const int64_t* voff0,
