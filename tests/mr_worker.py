@@ -56,6 +56,13 @@ def main():
     wl_f = synth.Workload("mr", dims, (0, 0, 0), (h, h, h), (1, 1, bcz), 8, 0, (0, 0), "uniform", 1.0,
                           (0, 0, -9.81), 1, 1, 2e-3, steps, "fourier", {"u_rms": 0.3, "modes": 64, "kmax": 6}, 9, 0)
     F = synth.make_field(wl_f)                               # global field [3][nz][ny][nx]
+    if os.environ.get("MR_FIELD") == "xcross":
+        # fast along x everywhere and 2 m/s upwards: far particles (C-15b) also cross the
+        # slab boundaries, so far tails receive far particles from the neighbour ranks
+        F = np.zeros_like(F)
+        F[0] = 20.0
+        F[2] = 2.0
+        F = F.astype(np.float32)
     if os.environ.get("MR_FIELD") == "xshear":
         # fast along x (20 m/s: ~1.3 cells per 4 calls, far particles of C-15b) in the
         # planes from 2 above a slab boundary to 2 below the next, still along x in the
@@ -139,7 +146,7 @@ def main():
         report.update(order_ok=bool(order_ok), worst_x=worst_x, worst_u=worst_u, oracle_last_far=int(emu.last_far),
                       gpu_last_far=[int(gathered[r]["far"]) for r in range(world)],
                       gpu_general=[int(gathered[r]["general"]) for r in range(world)])
-        if os.environ.get("MR_FIELD") == "xshear":
+        if os.environ.get("MR_FIELD") in ("xshear", "xcross"):
             ok &= emu.last_far > 0 and sum(report["gpu_last_far"]) == emu.last_far
             ok &= all(gg == 1 for gg in report["gpu_general"])   # every later rebin fused
         ok &= order_ok and worst_x <= 1e-5 and worst_u <= 1e-5

@@ -78,6 +78,25 @@ def test_sharded_rebalance_equalises_counts():
     assert "MR_REPORT" in out
 
 
+def test_multigpu_far_particles_across_ranks_stay_fused():
+    """K = 4, fast along x everywhere and upwards: far particles (C-15b) also change rank.
+    They are counted per cell of the neighbour's window by the in-place step, sent after
+    the near movers, sorted by the sender's store order and put in the receiver's far
+    tails — the rebin stays fused (no general sort) and the order equals the oracle's
+    (bin, far) sort of kept ++ arrivals."""
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    env = dict(os.environ, MR_K="4", MR_BCZ="1", MR_STEPS="9", MR_FIELD="xcross", MR_OBSERVE="end")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", "29790", os.path.join(ROOT, "tests", "mr_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "MR_REPORT" in out
+
+
 @pytest.mark.parametrize("K", [1, 2])
 def test_sharded_decomposition_matches_one_oracle(K):
     """ST_DECOMP_SHARDED: whole domain per rank, particles stay where
