@@ -244,13 +244,14 @@ st_status st_sync(st_ctx* ctx);
 st_status st_last_timings(st_ctx* ctx, float* advance_ms, float* rebin_ms);
 
 /* Timeline of the asynchronous coupling buffer (SURVEY §8(d6) asks
- * for copy/compute overlap evidence): t[6] receives, in ms since the context was
- * created, the begin and end of the most recent field copy (st_set_fluid_field, copy
- * stream), of the most recent st_advance (compute stream) and of the most recent
- * source readout (st_request_sources .. the copy out in st_wait_sources, readout
- * stream), measured with CUDA events on those streams; -1 where not yet recorded.
- * Blocks on those events. */
-st_status st_last_trace(st_ctx* ctx, double* t);
+ * for copy/compute overlap evidence).  The library records CUDA events on its streams
+ * for every call; t[6] receives, in ms since the context was created, the begin and end
+ * of the k-th field copy (st_set_fluid_field, copy-in stream), of the k-th st_advance
+ * (compute stream) and of the k-th source readout (st_request_sources .. its copy out
+ * in st_wait_sources, readout stream), counted from 0 since st_init; -1 where that
+ * call has not happened or is older than the last 64.  Blocks on those events only,
+ * so it can be read after a run without disturbing it. */
+st_status st_trace(st_ctx* ctx, int64_t k, double* t);
 
 /* Rebalance the particle counts of the ranks (ST_DECOMP_SHARDED; P:356
  * "the partitioning would be regularly checked and ... particles can be exchanged

@@ -131,7 +131,7 @@ SIGNATURES = {
     "st_get_stats": (_i32, [_vp, ctypes.POINTER(StStats)]),
     "st_sync": (_i32, [_vp]),
     "st_last_timings": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
-    "st_last_trace": (_i32, [_vp, _vp]),
+    "st_trace": (_i32, [_vp, ctypes.c_int64, _vp]),
     "st_last_error": (ctypes.c_char_p, [_vp]),
     "st_abi_version": (_i32, []),
     "st_nccl_unique_id": (_i32, [_vp]),

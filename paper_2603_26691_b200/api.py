@@ -310,10 +310,11 @@ class ScaleTrack:
         self._check(self.lib.st_rebalance(self.h, float(tolerance), ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
-    def last_trace(self) -> np.ndarray:
-        """st_last_trace: [copy in begin, end, step begin, end, readout begin, end] in ms."""
+    def trace(self, k: int) -> np.ndarray:
+        """st_trace: [k-th copy in begin, end, k-th step begin, end, k-th readout begin,
+        end] in ms since st_init (-1: not recorded / too old)."""
         t = np.empty(6, np.float64)
-        self._check(self.lib.st_last_trace(self.h, t.ctypes.data))
+        self._check(self.lib.st_trace(self.h, int(k), t.ctypes.data))
         return t
 
     def last_timings(self):

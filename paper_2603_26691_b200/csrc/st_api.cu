@@ -133,10 +133,11 @@ struct st_ctx {
 
   // timing
   cudaEvent_t t_adv0{}, t_adv1{}, t_reb0{}, t_reb1{};
-  // coupling-buffer trace (st_last_trace): [field copy begin/end (xs), step begin/end (cs),
+  // coupling-buffer trace (st_trace): a ring of [field copy begin/end (xs), step begin/end (cs),
   // readout begin/end (xo)] of the most recent calls, against a reference event
-  cudaEvent_t tr_ref{}, tr[6]{};
-  bool tr_set[6] = {false, false, false, false, false, false};
+  static constexpr int kTrace = 64;
+  cudaEvent_t tr_ref{}, tr[kTrace][6]{};
+  int64_t tr_n[3] = {0, 0, 0};   // field copies, advances, readouts so far
   bool timed_adv = false, timed_reb = false;
   bool reb_t0 = false;        // t_reb0 already recorded for the rebin in progress (k_count)
 
@@ -527,7 +528,8 @@ static st_status init_impl(st_ctx* c) {
   ST_CUDA(c, cudaEventCreate(&c->t_reb0));
   ST_CUDA(c, cudaEventCreate(&c->t_reb1));
   ST_CUDA(c, cudaEventCreate(&c->tr_ref));
-  for (int k = 0; k < 6; ++k) ST_CUDA(c, cudaEventCreate(&c->tr[k]));
+  for (int i = 0; i < st_ctx::kTrace; ++i)
+    for (int k = 0; k < 6; ++k) ST_CUDA(c, cudaEventCreate(&c->tr[i][k]));
   {
     st_status ts = make_tensor_maps(c);
     if (ts) return ts;
@@ -680,8 +682,9 @@ st_status st_destroy(st_ctx* c) {
   cudaFree(c->sc.partial);
   for (cudaEvent_t e : {c->ev_readout_done, c->ev_in, c->t_adv0, c->t_adv1, c->t_reb0, c->t_reb1, c->tr_ref})
     if (e) cudaEventDestroy(e);
-  for (int k = 0; k < 6; ++k)
-    if (c->tr[k]) cudaEventDestroy(c->tr[k]);
+  for (int i = 0; i < st_ctx::kTrace; ++i)
+    for (int k = 0; k < 6; ++k)
+      if (c->tr[i][k]) cudaEventDestroy(c->tr[i][k]);
   if (c->own_cs && c->cs) cudaStreamDestroy(c->cs);
   if (c->xs) cudaStreamDestroy(c->xs);
   if (c->xo) cudaStreamDestroy(c->xo);
@@ -735,8 +738,7 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
   // the back buffer may still be read by an advance enqueued earlier
   ST_CUDA(c, cudaStreamWaitEvent(c->xs, c->ev_field_reader[back], 0));
   const Geom& g = c->g;
-  ST_CUDA(c, cudaEventRecord(c->tr[0], c->xs));
-  c->tr_set[0] = true;
+  ST_CUDA(c, cudaEventRecord(c->tr[c->tr_n[0] % st_ctx::kTrace][0], c->xs));
   // cells the caller provides: this rank's slab (ST_DECOMP_SLAB) or its Eulerian
   // partition (ST_DECOMP_SHARDED; the other partitions arrive from their owners)
   const int in_z0 = c->shard ? c->eu_z0 : c->z0, in_z1 = c->shard ? c->eu_z1 : c->z1;
@@ -788,8 +790,8 @@ st_status st_set_fluid_field(st_ctx* c, const float* u) {
   st_status s = check_launch(c, launch_field_ingest(g, src, comp, src_z0, src_nz, c->field[back], c->xs));
   if (s) return s;
   ST_CUDA(c, cudaEventRecord(c->ev_field_ready[back], c->xs));
-  ST_CUDA(c, cudaEventRecord(c->tr[1], c->xs));
-  c->tr_set[1] = true;
+  ST_CUDA(c, cudaEventRecord(c->tr[c->tr_n[0] % st_ctx::kTrace][1], c->xs));
+  c->tr_n[0] += 1;
   c->pending = back;
   return ST_OK;
 }
@@ -1257,8 +1259,7 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
   if (c->front < 0) return fail(c, ST_ERR_STATE, "st_advance before st_set_fluid_field (P:202: first step is synchronous)");
   // the accumulator must be free (its previous readout finished zeroing it)
   ST_CUDA(c, cudaStreamWaitEvent(c->cs, c->ev_acc_free[c->acc_cur], 0));
-  ST_CUDA(c, cudaEventRecord(c->tr[2], c->cs));
-  c->tr_set[2] = true;
+  ST_CUDA(c, cudaEventRecord(c->tr[c->tr_n[1] % st_ctx::kTrace][2], c->cs));
   st_status st = ST_OK;
   bool done = false;
   c->timed_reb = false;
@@ -1318,8 +1319,8 @@ st_status st_advance(st_ctx* c, double dt, int32_t nsteps) {
   }
   ST_CUDA(c, cudaEventRecord(c->ev_field_reader[c->front], c->cs));
   ST_CUDA(c, cudaEventRecord(c->ev_acc_writer[c->acc_cur], c->cs));
-  ST_CUDA(c, cudaEventRecord(c->tr[3], c->cs));
-  c->tr_set[3] = true;
+  ST_CUDA(c, cudaEventRecord(c->tr[c->tr_n[1] % st_ctx::kTrace][3], c->cs));
+  c->tr_n[1] += 1;
   c->T_acc[c->acc_cur] += (double)nsteps * dt;
   c->calls += 1;
   if (c->calls % c->cfg.rebin_interval == 0) {
@@ -1343,8 +1344,7 @@ st_status st_request_sources(st_ctx* c) {
   c->T_acc[old] = 0.0;
   const Geom& g = c->g;
   ST_CUDA(c, cudaStreamWaitEvent(c->xo, c->ev_acc_writer[old], 0));
-  ST_CUDA(c, cudaEventRecord(c->tr[4], c->xo));
-  c->tr_set[4] = true;
+  ST_CUDA(c, cudaEventRecord(c->tr[c->tr_n[2] % st_ctx::kTrace][4], c->xo));
   if (c->comm) {
     std::string why;
     if (comm_source_halo(c->comm, c->acc[old], g, c->z0, c->z1, c->H, c->xo, why)) return fail(c, ST_ERR_NCCL, why);
@@ -1376,8 +1376,8 @@ st_status st_wait_sources(st_ctx* c, float* S, double* interval_s) {
     ST_CUDA(c, cudaMemcpyAsync(S, c->S_dev, 3 * out_cells * sizeof(float),
                                dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->xo));
   }
-  ST_CUDA(c, cudaEventRecord(c->tr[5], c->xo));
-  c->tr_set[5] = true;
+  ST_CUDA(c, cudaEventRecord(c->tr[c->tr_n[2] % st_ctx::kTrace][5], c->xo));
+  c->tr_n[2] += 1;
   ST_CUDA(c, cudaStreamSynchronize(c->xo));
   if (interval_s) *interval_s = c->readout_T;
   return consume_flags(c);
@@ -1686,16 +1686,20 @@ st_status st_rebalance(st_ctx* c, double tolerance, int64_t* sent, int64_t* rece
   return ST_OK;
 }
 
-st_status st_last_trace(st_ctx* c, double* t) {
+st_status st_trace(st_ctx* c, int64_t k, double* t) {
   ST_ALIVE(c);
   if (!t) return fail(c, ST_ERR_INVALID_ARG, "t is NULL");
-  for (int k = 0; k < 6; ++k) {
-    t[k] = -1.0;
-    if (!c->tr_set[k]) continue;
-    float ms = 0.0f;
-    ST_CUDA(c, cudaEventSynchronize(c->tr[k]));
-    ST_CUDA(c, cudaEventElapsedTime(&ms, c->tr_ref, c->tr[k]));
-    t[k] = ms;
+  for (int j = 0; j < 3; ++j) {   // j: 0 field copy, 1 advance, 2 readout
+    t[2 * j] = t[2 * j + 1] = -1.0;
+    const int64_t done = c->tr_n[j];
+    if (k < 0 || k >= done || k < done - st_ctx::kTrace) continue;
+    for (int e = 0; e < 2; ++e) {
+      cudaEvent_t ev = c->tr[k % st_ctx::kTrace][2 * j + e];
+      float ms = 0.0f;
+      ST_CUDA(c, cudaEventSynchronize(ev));
+      ST_CUDA(c, cudaEventElapsedTime(&ms, c->tr_ref, ev));
+      t[2 * j + e] = ms;
+    }
   }
   return ST_OK;
 }

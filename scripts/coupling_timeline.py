@@ -3,7 +3,7 @@
 field copies in and source readouts out must run under the particle step, not between
 steps.  Drives C3 (BASELINE.json configs[2]: 1e8 particles, 256^3 periodic, two-way,
 a new field every step) through the C-ABI with pinned host buffers in the paper's
-one-step-skew pattern and reads st_last_trace after every step: CUDA-event intervals on
+one-step-skew pattern and reads the st_trace event ring after the run: CUDA-event intervals on
 the copy-in stream, the compute stream and the readout stream.
 
   python scripts/coupling_timeline.py [--workload C3] [--particles 1e8] [--steps 12] [--out f.json]
@@ -71,12 +71,13 @@ def main():
         st.advance(wl.dt, 1)
         if s > 0:
             st.wait_sources(Sh)
-        t = st.last_trace()      # copy-in s, step s, readout s-1
         st.request_sources()
-        if s >= 4:               # after the first sort and a full rebin cycle
-            rows.append({"step": s - 4, "copy_in": [t[0], t[1]], "step_ms": [t[2], t[3]],
-                         "readout_prev": [t[4], t[5]]})
     st.wait_sources(Sh)
+    # read the event ring after the run (reading it inside the loop would block the host)
+    for s in range(4, a.steps + 4):   # after the first sort and a full rebin cycle
+        ci, sp, ro = st.trace(s), st.trace(s), st.trace(s - 1)
+        rows.append({"step": s - 4, "copy_in": [ci[0], ci[1]], "step_ms": [sp[2], sp[3]],
+                     "readout_prev": [ro[4], ro[5]]})
     t0 = rows[0]["copy_in"][0]
     steps = [r["step_ms"] for r in rows]
     cov_in = cov_out = len_in = len_out = 0.0
