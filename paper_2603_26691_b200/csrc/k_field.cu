@@ -144,6 +144,14 @@ int launch_fill_u64_seq(uint64_t* dst, int64_t n, uint64_t start, cudaStream_t s
   return 1;
 }
 
+// take the device error flags (read and clear in one atomic step) into host-mapped memory
+__global__ void k_take_flags(int* err, int* out) { *out = atomicExch(err, 0); }
+
+int launch_take_flags(int* err, int* out, cudaStream_t s) {
+  k_take_flags<<<1, 1, 0, s>>>(err, out);
+  return 1;
+}
+
 int launch_fill_f32(float* dst, int64_t n, float v, cudaStream_t s) {
   if (n <= 0) return 0;
   k_fill_f32<<<grid_for(n), 256, 0, s>>>(dst, n, v);

@@ -127,6 +127,8 @@ struct st_ctx {
 
   // errors and counters
   int* d_err = nullptr;
+  int* h_flags = nullptr;     // mapped pinned: consume_flags' atomic take of d_err
+  int* d_flags = nullptr;
   int64_t calls = 0, rebins = 0, launches = 0, fused_rebins = 0, last_movers = 0;
   std::vector<int64_t> mig_row;
   int64_t last_sent = 0, last_recv = 0;
@@ -200,12 +202,19 @@ static st_status check_launch(st_ctx* c, int nl) {
   return ST_OK;
 }
 
-// Read and clear the device error flags (call only after the producing stream synced).
-static st_status consume_flags(st_ctx* c) {
-  int h = 0;
-  ST_CUDA(c, cudaMemcpy(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+// Read and clear the device error flags, ordered on stream s (NULL: the compute stream):
+// one atomic exchange into host-mapped memory, so nothing runs on the legacy default
+// stream (a cudaMemcpy there would wait for the running step on the blocking compute
+// stream and serialise the coupling buffer).  Flags raised by work still running on
+// another stream are reported by a later call.
+static st_status consume_flags(st_ctx* c, cudaStream_t s = nullptr) {
+  if (!s) s = c->cs;
+  *(volatile int*)c->h_flags = 0;
+  st_status st = check_launch(c, launch_take_flags(c->d_err, c->d_flags, s));
+  if (st) return st;
+  ST_CUDA(c, cudaStreamSynchronize(s));
+  const int h = *(volatile int*)c->h_flags;
   if (!h) return ST_OK;
-  ST_CUDA(c, cudaMemset(c->d_err, 0, sizeof(int)));
   if (h & ERRF_CFL) return fail(c, ST_ERR_CFL, "displacement precondition violated (C-11/C-12: one wrap or bounce)");
   if (h & ERRF_WINDOW)
     return fail(c, ST_ERR_CFL, "a particle left this rank's field/source window between rebins (C-16)");
@@ -538,6 +547,8 @@ static st_status init_impl(st_ctx* c) {
   ST_CUDA(c, cudaMalloc(&c->S_dev, (size_t)3 * (c->local_cells > 0 ? c->local_cells : 1) * sizeof(float)));
   ST_CUDA(c, cudaMalloc(&c->d_err, sizeof(int)));
   ST_CUDA(c, cudaMemset(c->d_err, 0, sizeof(int)));
+  ST_CUDA(c, cudaHostAlloc(&c->h_flags, sizeof(int), cudaHostAllocMapped));
+  ST_CUDA(c, cudaHostGetDevicePointer(&c->d_flags, c->h_flags, 0));
   const size_t nb = (size_t)c->bg.nbins;
   for (int i = 0; i < 2; ++i) {
     ST_CUDA(c, cudaMalloc(&c->off[i], (nb + 1) * sizeof(int64_t)));
@@ -640,6 +651,7 @@ st_status st_destroy(st_ctx* c) {
   cudaFree(c->field_stage);
   cudaFree(c->S_dev);
   cudaFree(c->d_err);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
   for (int i = 0; i < 2; ++i) {
     cudaFree(c->off[i]);
     cudaFree(c->items[i]);
@@ -1378,9 +1390,8 @@ st_status st_wait_sources(st_ctx* c, float* S, double* interval_s) {
   }
   ST_CUDA(c, cudaEventRecord(c->tr[c->tr_n[2] % st_ctx::kTrace][5], c->xo));
   c->tr_n[2] += 1;
-  ST_CUDA(c, cudaStreamSynchronize(c->xo));
   if (interval_s) *interval_s = c->readout_T;
-  return consume_flags(c);
+  return consume_flags(c, c->xo);   // syncs the readout stream only, not the running step
 }
 
 st_status st_get_sources(st_ctx* c, float* S, double* interval_s) {

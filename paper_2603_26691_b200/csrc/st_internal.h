@@ -77,6 +77,7 @@ int launch_source_readout(const Geom& g, float4* acc, int z0, int z1, float scal
                           cudaStream_t s);
 int launch_fill_u64_seq(uint64_t* dst, int64_t n, uint64_t start, cudaStream_t s);
 int launch_fill_f32(float* dst, int64_t n, float v, cudaStream_t s);
+int launch_take_flags(int* err, int* out, cudaStream_t s);
 int launch_keys(const Geom& g, const float* x, int64_t xstride, int64_t n, int32_t* key,
                 cudaStream_t s);
 
