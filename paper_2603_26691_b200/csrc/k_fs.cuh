@@ -196,10 +196,15 @@ __global__ void __launch_bounds__(32 * kFsWarps, 2) k_fs(const __grid_constant__
           if (a.far_cur && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
             fdest = (int)atomicAdd(a.far_cur + bin_of_cell<SH>(g, a.bg, c[q][0], c[q][1], c[q][2]), 1ULL);
             a.far_src[fdest] = (int32_t)(p0 + r[q]);
+            a.far_src_hi[fdest] = 0;
           } else if (VP && a.fs_cur && far_plane(g, c[q][2], fside, pl)) {
-            // a neighbour rank's cell: the far region of the send buffer, keyed by prior index
+            // a neighbour rank's cell: the far region of the send buffer, with its prior
+            // index (the receiver's tail key) and the cell it was counted for
             fdest = (int)atomicAdd(a.fs_cur + fside, 1ULL);
-            if ((int64_t)fdest < a.scap) a.fs_key[fside][fdest] = (int32_t)(p0 + r[q]);
+            if ((int64_t)fdest < a.scap) {
+              a.fs_key[fside][fdest] = (int32_t)(p0 + r[q]);
+              a.fs_cell[fside][fdest] = (c[q][2] * g.n[1] + c[q][1]) * g.n[0] + c[q][0];
+            }
           } else {
             flags |= ERRF_SCATTER;
             ok = false;

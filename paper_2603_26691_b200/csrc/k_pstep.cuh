@@ -319,9 +319,13 @@ __global__ void __launch_bounds__(32 * pwarps(SCATTER && ADVANCE), (SCATTER && A
           if (a.far_cur && kz >= a.bg.kz0 && kz < a.bg.kz0 + a.bg.nkz) {
             fdest = (long long)atomicAdd(a.far_cur + bin_of_cell<SH>(g, a.bg, c0, c1, c2), 1ULL);
             a.far_src[fdest] = (int32_t)(p0 + r);   // prior index: k_far_order sorts the tail by it
+            a.far_src_hi[fdest] = 0;
           } else if (VP && a.fs_cur && far_plane(g, c2, fside, pl)) {
             fdest = (long long)atomicAdd(a.fs_cur + fside, 1ULL);   // neighbour rank: far send region
-            if (fdest < a.scap) a.fs_key[fside][fdest] = (int32_t)(p0 + r);
+            if (fdest < a.scap) {
+              a.fs_key[fside][fdest] = (int32_t)(p0 + r);
+              a.fs_cell[fside][fdest] = (c2 * g.n[1] + c1) * g.n[0] + c0;
+            }
           } else {
             flags |= ERRF_SCATTER;
             write_ok = false;

@@ -633,19 +633,21 @@ __global__ void k_vcombine(Geom g, BinGeom bg, uint32_t* __restrict__ new_cnt, c
   new_cnt[dt] += rcnt_up[v];
 }
 
-// C-15b, deterministic: the fused scatter placed bin d's F far particles in the last F
-// slots of d in atomic order and recorded each one's old-layout index in far_src; one
-// thread per bin sorts that tail by it (insertion sort, payload moved with the key), so
-// the far tail is in prior store order — the (bin, far)-stable sort of the oracle.
+// C-15b, deterministic: the fused scatter (and, across ranks, k_far_insert) placed bin
+// d's F far particles in the last F slots of d in atomic order, each with its key
+// (hi, lo) = (0, old-layout index) or (1 + source-rank order, sender's index); one thread
+// per bin sorts that tail by the key (insertion sort, payload moved with it), so the far
+// tail is kept ++ arrivals in prior store order — the (bin, far)-stable sort of the oracle.
 __global__ void k_far_order(int nbins, const int* __restrict__ far_cnt, const int64_t* __restrict__ off_new,
-                            int32_t* __restrict__ far_src, Store B, int64_t cap) {
+                            int32_t* __restrict__ far_src, int32_t* __restrict__ far_hi, Store B, int64_t cap) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nbins) return;
   const int F = far_cnt[d];
   if (F < 2) return;
   const int64_t t0 = off_new[d + 1] - F;
+  auto key_of = [&](int64_t t) { return ((int64_t)far_hi[t] << 32) | (uint32_t)far_src[t]; };
   for (int i = 1; i < F; ++i) {
-    const int32_t key = far_src[t0 + i];
+    const int64_t key = key_of(t0 + i);
     float v[8];
     for (int a = 0; a < 3; ++a) {
       v[a] = B.x[a * cap + t0 + i];
@@ -655,9 +657,10 @@ __global__ void k_far_order(int nbins, const int* __restrict__ far_cnt, const in
     v[7] = B.w[t0 + i];
     const uint64_t id = B.id[t0 + i];
     int j = i - 1;
-    for (; j >= 0 && far_src[t0 + j] > key; --j) {
+    for (; j >= 0 && key_of(t0 + j) > key; --j) {
       const int64_t s = t0 + j, t = s + 1;
       far_src[t] = far_src[s];
+      far_hi[t] = far_hi[s];
       for (int a = 0; a < 3; ++a) {
         B.x[a * cap + t] = B.x[a * cap + s];
         B.u[a * cap + t] = B.u[a * cap + s];
@@ -668,7 +671,8 @@ __global__ void k_far_order(int nbins, const int* __restrict__ far_cnt, const in
     }
     const int64_t t = t0 + j + 1;
     if (t != t0 + i) {
-      far_src[t] = key;
+      far_src[t] = (int32_t)(uint32_t)key;
+      far_hi[t] = (int32_t)(key >> 32);
       for (int a = 0; a < 3; ++a) {
         B.x[a * cap + t] = v[a];
         B.u[a * cap + t] = v[3 + a];
@@ -1013,41 +1017,28 @@ __global__ void k_far_accept(Geom g, BinGeom bg, const int* __restrict__ rfv0, c
   atomicAdd(fr_n + side, (unsigned long long)cnt);
 }
 
-// Far arrivals of one side (sorted by sender key) into the far tails of B: slot by the
-// bin's cursor, key n_old + rank in (source rank, sender key) order (k_far_order).
+// Far arrivals of one side into the far tails of B: bin = the cell the sender counted
+// them for (their position has advanced since, in the sender's fused launch), slot by
+// the bin's cursor, key (1 + source-rank order, sender's index) for k_far_order.
 __global__ void k_far_insert(FarInsertArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.count) return;
   const Store& r = a.r;
   const int64_t rc = a.rcap;
-  float x[3];
-  int c[3];
-  for (int ax = 0; ax < 3; ++ax) {
-    x[ax] = r.x[ax * rc + i];
-    c[ax] = cell_from_t(cell_coord(x[ax], a.g.lo[ax], a.g.ih[ax]), a.g.n[ax]);
-  }
-  const int kz = c[2] / a.g.cc;
+  const int cl = a.cell[i];
+  const int cx = cl % a.g.n[0], cy = (cl / a.g.n[0]) % a.g.n[1], cz = cl / (a.g.n[0] * a.g.n[1]);
+  const int kz = cz / a.g.cc;
   if (kz < a.bg.kz0 || kz >= a.bg.kz0 + a.bg.nkz) {
     atomicOr(a.err, ERRF_SCATTER);
     return;
   }
-  const int b = bin_of_cell<0>(a.g, a.bg, c[0], c[1], c[2]);
+  const int b = bin_of_cell<0>(a.g, a.bg, cx, cy, cz);
   const int64_t slot = (int64_t)atomicAdd(a.far_cur + b, 1ULL);
-  int64_t rank = i;
-  if (a.merge) {   // both sides from the same rank: rank in the merged sender order
-    const int32_t k = a.key[i];
-    int64_t lo = 0, hi = a.other_count;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (a.other_key[mid] < k) lo = mid + 1;
-      else hi = mid;
-    }
-    rank += lo;
-  }
-  a.far_src[slot] = (int32_t)(a.base + rank);
+  a.far_src[slot] = a.key[i];
+  a.far_src_hi[slot] = a.hi;
   const int64_t cap = a.cap;
   for (int ax = 0; ax < 3; ++ax) {
-    a.B.x[ax * cap + slot] = x[ax];
+    a.B.x[ax * cap + slot] = r.x[ax * rc + i];
     a.B.u[ax * cap + slot] = r.u[ax * rc + i];
   }
   a.B.d[slot] = r.d[i];
@@ -1068,10 +1059,11 @@ int launch_far_insert(const FarInsertArgs& a, cudaStream_t s) {
   return 1;
 }
 
-int launch_far_order(const BinGeom& bg, const int* far_cnt, const int64_t* off_new, const int32_t* far_src, Store B,
-                     int64_t cap, cudaStream_t s) {
+int launch_far_order(const BinGeom& bg, const int* far_cnt, const int64_t* off_new, const int32_t* far_src,
+                     const int32_t* far_src_hi, Store B, int64_t cap, cudaStream_t s) {
   if (!far_cnt || !far_src || bg.nbins <= 0) return 0;
-  k_far_order<<<blocks_for(bg.nbins), 256, 0, s>>>(bg.nbins, far_cnt, off_new, const_cast<int32_t*>(far_src), B, cap);
+  k_far_order<<<blocks_for(bg.nbins), 256, 0, s>>>(bg.nbins, far_cnt, off_new, const_cast<int32_t*>(far_src),
+                                                   const_cast<int32_t*>(far_src_hi), B, cap);
   return 1;
 }
 

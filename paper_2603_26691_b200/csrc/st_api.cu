@@ -98,8 +98,10 @@ struct st_ctx {
   int* rfv[2] = {nullptr, nullptr};
   int64_t nfv = 0;
   unsigned long long* d_fs = nullptr;
-  int32_t* fs_key[2] = {nullptr, nullptr};
-  int32_t* fr_key[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int32_t* fs_key[2] = {nullptr, nullptr};    // sender's store index of each far mover
+  int32_t* fs_cell[2] = {nullptr, nullptr};   // the cell it was counted for
+  int32_t* fr_key[2] = {nullptr, nullptr};    // received
+  int32_t* fr_cell[2] = {nullptr, nullptr};
   int64_t* h_fs = nullptr;   // pinned [4]: far sent lo / hi, far received dn / up
   int64_t* h_tot = nullptr;                 // pinned: send_lo, send_hi, recv_dn, recv_up
   int* h_farg = nullptr;                    // pinned: global far flag
@@ -585,7 +587,9 @@ static st_status init_impl(st_ctx* c) {
         ST_CUDA(c, cudaMalloc(&c->rfv[i], c->nfv * sizeof(int)));
         ST_CUDA(c, cudaMemset(c->rfv[i], 0, c->nfv * sizeof(int)));   // stays 0 where no neighbour
         ST_CUDA(c, cudaMalloc(&c->fs_key[i], c->scap * sizeof(int32_t)));
-        for (int k = 0; k < 2; ++k) ST_CUDA(c, cudaMalloc(&c->fr_key[i][k], c->scap * sizeof(int32_t)));
+        ST_CUDA(c, cudaMalloc(&c->fs_cell[i], c->scap * sizeof(int32_t)));
+        ST_CUDA(c, cudaMalloc(&c->fr_key[i], c->scap * sizeof(int32_t)));
+        ST_CUDA(c, cudaMalloc(&c->fr_cell[i], c->scap * sizeof(int32_t)));
       }
       ST_CUDA(c, cudaMalloc(&c->d_fs, 6 * sizeof(unsigned long long)));
       ST_CUDA(c, cudaMemset(c->d_fs, 0, 6 * sizeof(unsigned long long)));
@@ -675,7 +679,9 @@ st_status st_destroy(st_ctx* c) {
     cudaFree(c->fv[i]);
     cudaFree(c->rfv[i]);
     cudaFree(c->fs_key[i]);
-    for (int k = 0; k < 2; ++k) cudaFree(c->fr_key[i][k]);
+    cudaFree(c->fs_cell[i]);
+    cudaFree(c->fr_key[i]);
+    cudaFree(c->fr_cell[i]);
   }
   cudaFree(c->d_fs);
   if (c->h_fs) cudaFreeHost(c->h_fs);
@@ -902,7 +908,8 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.tm_win[1] = c->tmap_win[c->front < 0 ? 0 : c->front][1];
   a.dtab = c->dtab;
   a.far_cur = c->far_cur;
-  a.far_src = c->key[0];      // the radix keys are free outside the general sort
+  a.far_src = c->key[0];      // the radix keys are free outside the general sort: the far
+  a.far_src_hi = c->key[1];   // tails' (hi, lo) sort keys
   a.cap = c->cap;
   a.n = c->n;
   a.off = c->off[c->lay];
@@ -1131,8 +1138,10 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   a.n = n_new;
   if (c->comm && c->fv[0]) {
     a.fs_cur = c->d_fs + 2;
-    a.fs_key[0] = c->fs_key[0];
-    a.fs_key[1] = c->fs_key[1];
+    for (int i = 0; i < 2; ++i) {
+      a.fs_key[i] = c->fs_key[i];
+      a.fs_cell[i] = c->fs_cell[i];
+    }
   }
   if (advance) ST_CUDA(c, cudaEventRecord(c->t_adv0, c->cs));
   if ((s = check_launch(c, launch_step(a, true, advance, c->cs)))) return s;
@@ -1145,8 +1154,10 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
                            c->h_tot[2] + fr0, c->h_tot[3] + fr1, g.bc[2] == ST_BC_PERIODIC, c->cs, why))
       return fail(c, ST_ERR_NCCL, why);
     if (c->fv[0] && (fs0 + fs1 + fr0 + fr1) > 0 &&
-        comm_far_keys(c->comm, c->fs_key[0] + c->h_tot[0], fs0, c->fs_key[1] + c->h_tot[1], fs1, c->fr_key[0][0], fr0,
-                      c->fr_key[1][0], fr1, g.bc[2] == ST_BC_PERIODIC, c->cs, why))
+        (comm_far_keys(c->comm, c->fs_key[0] + c->h_tot[0], fs0, c->fs_key[1] + c->h_tot[1], fs1, c->fr_key[0], fr0,
+                       c->fr_key[1], fr1, g.bc[2] == ST_BC_PERIODIC, c->cs, why) ||
+         comm_far_keys(c->comm, c->fs_cell[0] + c->h_tot[0], fs0, c->fs_cell[1] + c->h_tot[1], fs1, c->fr_cell[0], fr0,
+                       c->fr_cell[1], fr1, g.bc[2] == ST_BC_PERIODIC, c->cs, why)))
       return fail(c, ST_ERR_NCCL, why);
     nl = 0;
     for (int side = 0; side < 2; ++side) {
@@ -1172,29 +1183,11 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     const bool pz = g.bc[2] == ST_BC_PERIODIC;
     const int up = (r + 1 < G) ? r + 1 : (pz ? 0 : -1), dn = (r > 0) ? r - 1 : (pz ? G - 1 : -1);
     if (fr0 + fr1 > 0) {
-      // far arrivals: each side's block sorted by sender key (the sender's store order),
-      // then into the far tails with keys n_old + rank in (source rank, sender order)
-      Store sorted[2];
-      const int32_t* skey[2] = {c->fr_key[0][0], c->fr_key[1][0]};
+      // far arrivals into the far tails: bin of the cell they were counted for, key
+      // (1 + order of the source rank, sender's store index) — k_far_order sorts them after
+      // the kept far particles, by source rank, in sender order (C-16, C-15b)
       const int64_t fr[2] = {fr0, fr1};
-      for (int side = 0; side < 2; ++side) {
-        Store a0 = c->rbuf[side], b0 = c->sbuf[side];
-        const int64_t o = c->h_tot[2 + side];   // the far block follows the near arrivals
-        a0.x += o; a0.u += o; a0.d += o; a0.w += o; a0.id += o;
-        sorted[side] = a0;
-        if (fr[side] > 1) {
-          int in_b = 0;
-          const int ns = launch_stable_sort(a0, b0, c->scap, fr[side], c->fr_key[side][0], c->fr_key[side][1], 31,
-                                            c->sc, &in_b, c->cs);
-          if (ns < 0) return fail(c, ST_ERR_CAPACITY, "sort scratch too small (far arrivals)");
-          if ((s = check_launch(c, ns))) return s;
-          if (in_b) {
-            sorted[side] = b0;
-            skey[side] = c->fr_key[side][1];
-          }
-        }
-      }
-      const bool same = dn == up;               // two ranks, periodic: both blocks from one rank
+      const int src[2] = {dn, up};
       nl = 0;
       for (int side = 0; side < 2; ++side) {
         if (!fr[side]) continue;
@@ -1202,17 +1195,19 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
         memset(&fa, 0, sizeof(fa));
         fa.g = g;
         fa.bg = c->bg;
-        fa.r = sorted[side];
+        Store rb = c->rbuf[side];
+        const int64_t o = c->h_tot[2 + side];   // the far block follows the near arrivals
+        rb.x += o; rb.u += o; rb.d += o; rb.w += o; rb.id += o;
+        fa.r = rb;
         fa.rcap = c->scap;
         fa.count = fr[side];
-        fa.key = skey[side];
-        fa.other_key = skey[1 - side];
-        fa.other_count = fr[1 - side];
-        fa.merge = same ? 1 : 0;
-        const int src = side == 0 ? dn : up, other = side == 0 ? up : dn;
-        fa.base = c->n + (same ? 0 : (src < other ? 0 : fr[1 - side]));   // ascending source rank (C-16)
+        fa.key = c->fr_key[side];
+        fa.cell = c->fr_cell[side];
+        const int other = src[1 - side];
+        fa.hi = 1 + ((other >= 0 && other < src[side]) ? 1 : 0);   // one source rank: both sides 1
         fa.far_cur = c->far_cur;
         fa.far_src = c->key[0];
+        fa.far_src_hi = c->key[1];
         fa.B = c->S[1 - c->cur];
         fa.cap = c->cap;
         fa.err = c->d_err;
@@ -1231,8 +1226,8 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     c->mig_row[0] = c->n;
   }
   // C-15b: far tails into prior store order (after the arrivals: they precede the tail)
-  if ((s = check_launch(c, launch_far_order(c->bg, c->far_cnt, c->off[nlay], c->key[0], c->S[1 - c->cur], c->cap,
-                                            c->cs))))
+  if ((s = check_launch(c, launch_far_order(c->bg, c->far_cnt, c->off[nlay], c->key[0], c->key[1], c->S[1 - c->cur],
+                                            c->cap, c->cs))))
     return s;
   if (advance) {
     ST_CUDA(c, cudaEventRecord(c->t_adv1, c->cs));

@@ -42,13 +42,15 @@ struct StepArgs {
   const int* slot_base;       // [27][nbins] base[j][s] (scatter; rebin_prep output; k_step)
   const long long* dtab;      // [nbins][27] destination table (scatter; k_dbase output; k_pstep)
   unsigned long long* far_cur;// [nbins] next free slot of each bin's far tail (C-15b), or NULL
-  int32_t* far_src;           // [cap] by new-layout slot: old-layout index of a far particle
-                              // (k_far_order sorts each tail by it: prior order, C-15b)
+  int32_t* far_src;           // [cap] by new-layout slot: the tail sort key (hi, lo) of a far
+  int32_t* far_src_hi;        // particle: (0, old-layout index) for this rank's own, (1 + order of
+                              // the source rank, sender's index) for arrivals (k_far_order, C-15b)
   // multi-GPU far particles whose cell lies in a neighbour rank's slab (C-15b across ranks):
   // the scatter appends them to the far region of sbuf[side] (after the near movers),
   // fs_cur[side] = next free slot, fs_key[side][slot] = prior index (the receiver sorts by it)
   unsigned long long* fs_cur; // [2] or NULL: such a particle is an error (general path taken)
   int32_t* fs_key[2];
+  int32_t* fs_cell[2];        // [scap] per side: the global cell it was counted for (its bin there)
   // ... and the in-place counting step counts them per cell of the neighbour's first
   // chunk_cells planes: cnt_fv[side][(p * ny + y) * nx + x], p = planes beyond the slab
   int* cnt_fv[2];             // or NULL: such a particle sets *cnt_far (general path)
@@ -79,7 +81,8 @@ int launch_vcombine(const Geom& g, const BinGeom& bg, uint32_t* new_cnt, const u
                     const uint32_t* rcnt_up, uint32_t* kept_dn, uint32_t* kept_up, int oz0, int oz1,
                     const int* far_cnt, cudaStream_t s);
 // C-15b: sort every bin's far tail of the new layout B by the old-layout index (far_src)
-int launch_far_order(const BinGeom& bg, const int* far_cnt, const int64_t* off_new, const int32_t* far_src, Store B,
+int launch_far_order(const BinGeom& bg, const int* far_cnt, const int64_t* off_new, const int32_t* far_src,
+                     const int32_t* far_src_hi, Store B,
                      int64_t cap, cudaStream_t s);
 struct InsertArgs {
   Geom g;
@@ -121,19 +124,18 @@ struct CountArgs {
 // per-cell counts to its bins (new_cnt and far_cnt) and totals them per side
 int launch_far_accept(const Geom& g, const BinGeom& bg, const int* rfv0, const int* rfv1, int z0, int z1,
                       uint32_t* new_cnt, int* far_cnt, unsigned long long* fr_n, int* err, cudaStream_t s);
-// ... and puts the sorted far arrivals of one side into the far tails of B
+// ... and puts the far arrivals of one side into the far tails of B
 struct FarInsertArgs {
   Geom g;
   BinGeom bg;
-  Store r;                    // sorted far arrivals of this side (stride rcap)
+  Store r;                    // far arrivals of this side (stride rcap), any order
   int64_t rcap, count;
-  const int32_t* key;         // their sender keys (sorted), and the other side's
-  const int32_t* other_key;
-  int64_t other_count;
-  int64_t base;               // n_old + position of this side's block in (source rank, key) order
-  int merge;                  // 1: both sides come from the same rank: rank by merging keys
+  const int32_t* key;         // their sender store indices
+  const int32_t* cell;        // the global cells they were counted for
+  int32_t hi;                 // 1 + order of the source rank among this rank's sources (C-16)
   unsigned long long* far_cur;
   int32_t* far_src;
+  int32_t* far_src_hi;
   Store B;
   int64_t cap;
   int* err;
