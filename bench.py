@@ -497,11 +497,18 @@ def run_ours(args):
     alg = algorithmic_bytes_per_update(wl.coupling == 1) * n_local + 80 * movers * (1.0 / K) + 24 * cells_win
     kms = adv_ms
     achieved = alg / (kms / 1e3) / 1e9
-    traffic = None
+    # DRAM bytes per step launch from the committed ncu capture of THESE kernels at this
+    # workload (profiles/ncu_traffic.json: per-launch dram__bytes_read + write of the fused
+    # k_fs and the in-place k_ip at C5 1e9), mixed as the timed launches are: one fused
+    # launch per K; null when no capture matches the workload / particle count
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(kname.split()[0])
+            tj = json.load(open(tp))
+            if tj.get("workload") == wl.name and abs(tj.get("particles", 0) - n_local) <= 0.01 * n_local:
+                traffic = (tj["k_fs"] + (K - 1) * tj["k_ip"]) / K
+                traffic_src = tj.get("source")
         except Exception:
             traffic = None
 
@@ -565,6 +572,7 @@ def run_ours(args):
                               if args.cluster > 0 else {})),
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "alg_bytes_per_launch": alg, "kernel_ms": kms},
             "step_kernel_ms": adv_ms, "rebin_prep_ms": reb_ms, "rebins_in_timed_region": len(reb_list),
             "f_move_chunk": f_move, "fused_rebins": st_stats["fused_rebins"],

@@ -191,9 +191,25 @@ int comm_source_halo(Comm* c, float4* acc, const Geom& g, int z0, int z1, int H,
   return join_out(c, s, why);
 }
 
+static bool equal_slabs(const std::vector<int>& zb) {
+  for (size_t r = 1; r + 1 < zb.size(); ++r)
+    if (zb[r + 1] - zb[r] != zb[1] - zb[0]) return false;
+  return true;
+}
+
 int comm_shard_field(Comm* c, float* stage, int64_t comp, int64_t plane, int plane0, const std::vector<int>& zb,
                      cudaStream_t s, std::string& why) {
   if (join_in(c, s, why)) return 1;
+  if (equal_slabs(zb)) {   // equal partitions: one all-gather per component (NVLS-capable)
+    const size_t cnt = (size_t)(zb[1] - zb[0]) * plane;
+    NCCK(ncclGroupStart(), why);
+    for (int k = 0; k < 3; ++k) {
+      float* base = stage + k * comp + (int64_t)plane0 * plane;
+      NCCK(ncclAllGather(base + (int64_t)zb[c->rank] * plane, base, cnt, ncclFloat, c->nc, c->ns), why);
+    }
+    NCCK(ncclGroupEnd(), why);
+    return join_out(c, s, why);
+  }
   NCCK(ncclGroupStart(), why);
   for (int r = 0; r < c->nranks; ++r) {
     const size_t cnt = (size_t)(zb[r + 1] - zb[r]) * plane;
@@ -210,6 +226,12 @@ int comm_shard_field(Comm* c, float* stage, int64_t comp, int64_t plane, int pla
 int comm_shard_sources(Comm* c, float4* acc, int64_t plane, const std::vector<int>& zb, cudaStream_t s,
                        std::string& why) {
   if (join_in(c, s, why)) return 1;
+  if (equal_slabs(zb)) {   // equal partitions: one reduce-scatter, in place (NVLS-capable)
+    const size_t cnt = (size_t)(zb[1] - zb[0]) * plane * 4;
+    float* base = reinterpret_cast<float*>(acc);
+    NCCK(ncclReduceScatter(base, base + (int64_t)zb[c->rank] * plane * 4, cnt, ncclFloat, ncclSum, c->nc, c->ns), why);
+    return join_out(c, s, why);
+  }
   NCCK(ncclGroupStart(), why);
   for (int r = 0; r < c->nranks; ++r) {
     const size_t cnt = (size_t)(zb[r + 1] - zb[r]) * plane * 4;

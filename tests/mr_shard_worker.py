@@ -33,7 +33,7 @@ def main():
     uid = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
 
-    dims, h = (32, 24, 40), 1 / 16
+    dims, h = (32, 24, int(os.environ.get("MR_DZ", "40"))), 1 / 16   # 16 * world: equal slabs (all-gather path)
     L = [d * h for d in dims]
     cfg = Config(dims=dims, cell_size=(h, h, h), chunk_cells=8, bc=(1, 1, 1), gravity=(0, 0, -9.81),
                  rebin_interval=K, capacity=100_000, device=local, rank=rank, nranks=world,

@@ -97,17 +97,17 @@ def test_multigpu_far_particles_across_ranks_stay_fused():
     assert "MR_REPORT" in out
 
 
-@pytest.mark.parametrize("K", [1, 2])
-def test_sharded_decomposition_matches_one_oracle(K):
+@pytest.mark.parametrize("K,equal", [(1, False), (2, False), (2, True)])
+def test_sharded_decomposition_matches_one_oracle(K, equal):
     """ST_DECOMP_SHARDED: whole domain per rank, particles stay where
     injected, sources all-reduced — equal to one oracle run holding all particles."""
     n = _ngpu()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(n, 4)
-    env = dict(os.environ, MR_K=str(K), MR_STEPS="6")
+    env = dict(os.environ, MR_K=str(K), MR_STEPS="6", MR_DZ=str(16 * world if equal else 40))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29700 + K),
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + K + (10 if equal else 0)),
            os.path.join(ROOT, "tests", "mr_shard_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
