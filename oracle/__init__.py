@@ -26,9 +26,9 @@ inject -> set fluid field -> advance(dt, nsteps) -> get sources, with
   sender's order), then stable-sorts by bin key; M[src][dst] counts movers.
 * source readout C-13: S = acc / (V_cell * T_acc) in N/m^3, acc in float64.
 
-Parity status: every function here is pinned by tests/test_oracle_pins.py except
-where DESIGN.md §5 says "parity unpinned" (trajectory values in a non-uniform
-field beyond the invariants of pin P-10).
+Parity status: every function here is pinned by tests/test_oracle_pins.py (the
+C-15b rule by a pure-Python brute force, P-9b) except where DESIGN.md §5 says "parity
+unpinned" (trajectory values in a non-uniform field beyond the invariants of pin P-10).
 """
 from __future__ import annotations
 
