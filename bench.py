@@ -528,6 +528,7 @@ def run_ours(args):
         # field goes in (H2D) and step s-1's sources come out (D2H) while step s runs;
         # every step's copies are inside the timed region
         torch.cuda.synchronize()
+        k0 = st.stats()["calls"]      # index of the first e2e call in the library's trace ring
         t_host0 = time.perf_counter()
         h0.record(stream)
         for s in range(k_e2e):
@@ -548,6 +549,19 @@ def run_ours(args):
         e2e = {"value": n_total * k_e2e / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(Fh[0].numel() * 4), "d2h_bytes_per_step": int(Sh.numel() * 4),
                "steps": k_e2e, "ms_per_step": ems / k_e2e}
+        try:   # where the e2e time goes: the library's CUDA-event ring (st_trace) of these calls
+            tr = [st.trace(k0 + k) for k in range(k_e2e)]
+            stp = [(t[2], t[3]) for t in tr]
+            gaps = [stp[k + 1][0] - stp[k][1] for k in range(k_e2e - 1)]
+            cin = [(t[0], t[1]) for t in tr[1:]]
+            hid = sum(max(0.0, min(b, stp[k][1]) - max(a, stp[k][0])) for k, (a, b) in enumerate(cin))
+            e2e["trace"] = {"steps_ms": float(np.mean([b - a for a, b in stp])),
+                            "mean_gap_between_steps_ms": float(np.mean(gaps)) if gaps else 0.0,
+                            "first_copy_to_last_step_end_ms": float(stp[-1][1] - tr[0][0]),
+                            "copy_in_ms": float(np.mean([b - a for a, b in cin])) if cin else 0.0,
+                            "copy_in_under_previous_step_frac": hid / max(1e-9, sum(b - a for a, b in cin))}
+        except Exception as ex:      # diagnostics never sink the line
+            e2e["trace"] = {"error": str(ex)[:200]}
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
