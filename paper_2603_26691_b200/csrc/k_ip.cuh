@@ -67,7 +67,6 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
   const int nbins = a.nbins;
   const bool two_way = a.p.two_way != 0;
   const float dt = a.dt;
-  unsigned cmov = 0;
   int cfar = 0, flags = 0;
   uint32_t phase = 0, iphase = 0;
   if (lane == 0) {
@@ -344,7 +343,6 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
               cfar = 1;
             }
           }
-          cmov += ((e0 >> SH) != (sx >> SH)) | ((e1 >> SH) != (ry >> SH)) | ((e2 >> SH) != (rz >> SH));
         }
         const int64_t i = p0 + r[q];
         __stcs(a.A.x + i, x[q][0]); __stcs(a.A.x + cap + i, x[q][1]); __stcs(a.A.x + 2 * cap + i, x[q][2]);
@@ -362,12 +360,8 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
       __syncwarp();
     }
   }
-  if (COUNT) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cmov += __shfl_xor_sync(kFull, cmov, o);
-    if (lane == 0 && cmov) atomicAdd(a.cnt_movers, (unsigned long long)cmov);
-    if (cfar) *(volatile int*)a.cnt_far = 1;
-  }
+  // (the chunk movers of the statistics are summed from the histogram by k_rebin_prep)
+  if (COUNT && cfar) *(volatile int*)a.cnt_far = 1;
   if (flags) atomicOr(a.err, flags);
 }
 

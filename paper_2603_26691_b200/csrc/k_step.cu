@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
 // d = nbins + side * nvb + v.
 template <int SH>
 __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cnt_base, uint32_t* __restrict__ new_cnt,
-                             const int* __restrict__ far_cnt) {
+                             const int* __restrict__ far_cnt, unsigned long long* __restrict__ movers) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nbins + 2 * bg.nvb) return;
   int dx, dy, dz;
@@ -548,6 +548,22 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
     }
     key[j] = ok ? bin_of_cell<SH>(g, bg, sx, sy, sz) : 0x7fffffff;
     cnt[j] = ok ? cnt_base[(int64_t)j * nbins + key[j]] : 0;
+  }
+  // statistics (movers != NULL): particles arriving from another chunk
+  if (movers) {
+    unsigned long long mv = 0;
+    const int dk = dcc<SH>(dx, g.cc) + g.NC[0] * (dcc<SH>(dy, g.cc) + g.NC[1] * dcc<SH>(dz, g.cc));
+#pragma unroll
+    for (int j = 0; j < 27; ++j) {
+      if (key[j] == 0x7fffffff) continue;
+      const int sk = key[j] / bg.cc3;   // local chunk of the source bin
+      const int dkl = dk - bg.kz0 * g.NC[0] * g.NC[1];
+      mv += (sk != dkl) ? (unsigned long long)cnt[j] : 0ull;
+    }
+    // lanes of this warp that returned early (ragged chunks, the tail) are not in the mask
+    const unsigned m = __activemask();
+    const unsigned sum = __reduce_add_sync(m, (unsigned)mv);
+    if ((threadIdx.x & 31) == __ffs(m) - 1 && sum) atomicAdd(movers, (unsigned long long)sum);
   }
   // stable order = ascending source bin: base of source q = sum of the counts of
   // the sources with a smaller bin (keys are distinct), all in registers
@@ -972,13 +988,13 @@ int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s) {
 }
 
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, const int* far_cnt,
-                      cudaStream_t s) {
+                      unsigned long long* movers, cudaStream_t s) {
   if (g.cc == 8)
     k_rebin_prep<3><<<blocks_for((int64_t)bg.nbins + 2 * bg.nvb, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt,
-                                                                                  far_cnt);
+                                                                                  far_cnt, movers);
   else
     k_rebin_prep<0><<<blocks_for((int64_t)bg.nbins + 2 * bg.nvb, 128), 128, 0, s>>>(g, bg, bg.nbins, cnt_base, new_cnt,
-                                                                                  far_cnt);
+                                                                                  far_cnt, movers);
   return 1;
 }
 

@@ -56,6 +56,7 @@ struct st_ctx {
   unsigned long long* d_far_n = nullptr;  // far particles placed by the last count (C-15b)
   int64_t general_rebins = 0;
   bool hist_ready = false;    // the last in-place step produced the next rebin's counts
+  bool counts_from_ip = false; // the pending rebin's counts came from that step (not k_count)
   Comm* shard = nullptr;      // ST_DECOMP_SHARDED: communicator of the source all-reduce
   std::vector<int32_t> slab_copy;   // cfg.slab_planes, owned (the caller's array is read at init only)
   int shard_rank = 0, shard_nranks = 1;
@@ -988,6 +989,7 @@ static st_status general_rebin(st_ctx* c) {
 static st_status count_slots(st_ctx* c, bool* far) {
   *far = true;
   if (!c->binned) return ST_OK;
+  c->counts_from_ip = c->hist_ready;
   if (c->hist_ready) {   // counted by the in-place step that made this rebin due
     c->hist_ready = false;
     ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
@@ -1070,7 +1072,10 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   const int nb = c->bg.nbins, nv = c->bg.nvb;
   if (!c->reb_t0) ST_CUDA(c, cudaEventRecord(c->t_reb0, c->cs));
   c->reb_t0 = false;
-  int nl = launch_rebin_prep(g, c->bg, c->hist, c->new_cnt, c->far_cnt, c->cs);
+  // chunk movers of the statistics: counted here when the in-place step produced the
+  // counts (k_count counts them itself)
+  int nl = launch_rebin_prep(g, c->bg, c->hist, c->new_cnt, c->far_cnt, c->counts_from_ip ? c->d_movers : nullptr,
+                             c->cs);
   st_status s;
   if (c->comm) {
     if ((s = check_launch(c, nl))) return s;

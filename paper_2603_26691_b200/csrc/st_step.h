@@ -101,8 +101,10 @@ struct InsertArgs {
 int launch_insert(const InsertArgs& a, cudaStream_t s);
 
 int launch_step(const StepArgs& a, bool scatter, bool advance, cudaStream_t s);
+// movers != NULL: add the particles arriving from another chunk (statistics; the counts
+// came from the in-place step, which no longer counts them itself)
 int launch_rebin_prep(const Geom& g, const BinGeom& bg, int* cnt_base, uint32_t* new_cnt, const int* far_cnt,
-                      cudaStream_t s);
+                      unsigned long long* movers, cudaStream_t s);
 // Slot histogram of the current layout (k_count): input of the next neighbour-slot rebin
 struct CountArgs {
   Geom g;
