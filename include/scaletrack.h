@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 2
+#define ST_ABI_VERSION 3   /* 3: st_micro_config.arithmetic */
 
 typedef struct st_ctx st_ctx;   /* opaque; owns the particle store, fields, sources */
 typedef int32_t st_status;
@@ -366,8 +366,10 @@ const char* st_ec_last_error(const st_ec* ec);
  *   sign C-31); d' = (6 m'/(pi rho_p))^(1/3); into the cell of the start position add
  *   acc_u -= w (m'u' - m u - m g dt), acc_rv -= w (m' - m), acc_e -= w C_p (m'T' - m T)
  *   (Eq. 8, 11, 13; C-8, C-33); reflect / wrap at the walls (C-11, C-12).
- * State fp32, arithmetic fp64, accumulators fp64 (C-28).  Test oracle:
- * oracle/microphysics.py.
+ * State fp32, accumulators fp64; arithmetic fp64 by default (C-28) or fp32 when
+ * cfg->arithmetic == ST_ARITH_FP32 (reading C-36: the same operations in the same order,
+ * each rounded to binary32; each droplet's deposit is still added in fp64).  Test
+ * oracle: oracle/microphysics.py (micro_advance(..., arith=np.float64 | np.float32)).
  * ------------------------------------------------------------------------------- */
 typedef struct {
   int32_t abi_version;   /* ST_ABI_VERSION */
@@ -386,7 +388,10 @@ typedef struct {
   double s_vp;           /* surface saturation S_v,p */
   int32_t device;        /* CUDA device ordinal */
   void* stream;          /* cudaStream_t, NULL = the legacy default stream */
+  int32_t arithmetic;    /* ST_ARITH_FP64 (default, C-28) | ST_ARITH_FP32 (C-36) */
 } st_micro_config;
+
+enum { ST_ARITH_FP64 = 0, ST_ARITH_FP32 = 1 };
 
 /* Fill *cfg with the DESIGN.md C-30 constants (air / water, 1 m cells, reflecting). */
 void st_micro_config_default(st_micro_config* cfg);

@@ -26,8 +26,12 @@ What it follows (PAPER.md = P, SPEC.md = S; readings C-28..C-33 in DESIGN.md §3
 
 Storage (C-28): the state (x, u, d, T, w) and the 5-component field are stored in
 ``store`` precision (float32 for the GPU parity tests, float64 for the pins); every
-operation of the step is computed in float64 from the stored values and the results
-are rounded to ``store`` at the end of each sub-step.
+operation of the step is computed in ``arith`` precision from the stored values —
+float64 by default (reading C-28), or float32 (the kernel's fp32 mode, reading C-36:
+the same operations in the same order, each rounded to binary32) — and the results are
+rounded to ``store`` at the end of each sub-step.  The fluid-side accumulators are
+float64 in both modes (each sub-step's deposit is computed in ``arith`` and added in
+float64).
 
 Parity status: pinned by tests/test_oracle_micro.py (SPEC worked examples, d^2-law
 closed form and first-order convergence, the exact discrete temperature relaxation,
@@ -74,38 +78,38 @@ class MicroMesh:
 
 # ---- closures (one function per equation) -------------------------------------------
 
-def saturation_vapor_density(T):
+def saturation_vapor_density(T, arith=np.float64):
     """C-30: Magnus saturation pressure over water, ideal-gas conversion."""
-    T = np.asarray(T, dtype=np.float64)
+    T = np.asarray(T, dtype=arith)
     tc = T - 273.15
     e_s = 610.94 * np.exp(17.625 * tc / (tc + 243.04))
     return e_s / (R_V * T)
 
 
-def mass_transfer_rate(d, rho_v, T_f, props: MicroProps):
+def mass_transfer_rate(d, rho_v, T_f, props: MicroProps, arith=np.float64):
     """Eq. 7: dm/dt = 2 pi D_v d rho_v,sat (S_v,f - S_v,p), kg/s."""
-    rs = saturation_vapor_density(T_f)
-    s_vf = np.asarray(rho_v, dtype=np.float64) / rs
-    return 2.0 * math.pi * props.D_v * np.asarray(d, dtype=np.float64) * rs * (s_vf - props.s_vp)
+    rs = saturation_vapor_density(T_f, arith)
+    s_vf = np.asarray(rho_v, dtype=arith) / rs
+    return 2.0 * math.pi * props.D_v * np.asarray(d, dtype=arith) * rs * (s_vf - props.s_vp)
 
 
-def heat_transfer_rate(d, m, T_p, T_f, dm_dt, props: MicroProps):
+def heat_transfer_rate(d, m, T_p, T_f, dm_dt, props: MicroProps, arith=np.float64):
     """Eq. 12, literal sign (C-31): dT_p/dt in K/s."""
-    d = np.asarray(d, dtype=np.float64)
-    q = math.pi * props.nusselt * props.kappa_f * d * (np.asarray(T_f, np.float64) - T_p)
-    return (q - props.latent * np.asarray(dm_dt, np.float64)) / (np.asarray(m, np.float64) * props.cp_p)
+    d = np.asarray(d, dtype=arith)
+    q = math.pi * props.nusselt * props.kappa_f * d * (np.asarray(T_f, arith) - T_p)
+    return (q - props.latent * np.asarray(dm_dt, arith)) / (np.asarray(m, arith) * props.cp_p)
 
 
-def drag_factor(Re, law):
+def drag_factor(Re, law, arith=np.float64):
     """f = C_D Re / 24 (Schiller-Naumann; 0.44 Re/24 above Re = 1000), Stokes f = 1."""
-    Re = np.asarray(Re, dtype=np.float64)
+    Re = np.asarray(Re, dtype=arith)
     if law == DRAG_STOKES:
         return np.ones_like(Re)
     return np.where(Re <= 1000.0, 1.0 + 0.15 * np.power(Re, 0.687), 0.44 * Re / 24.0)
 
 
-def droplet_mass(d, rho_p):
-    return math.pi / 6.0 * rho_p * np.asarray(d, np.float64) ** 3
+def droplet_mass(d, rho_p, arith=np.float64):
+    return math.pi / 6.0 * rho_p * np.asarray(d, arith) ** 3
 
 
 # ---- geometry (C-5, C-6, C-11, C-12) -------------------------------------------------
@@ -114,7 +118,8 @@ def cell_index(x, mesh: MicroMesh):
     """C-6: per axis clamp(floor((x - o) / h), 0, n - 1); returns flat cell ids."""
     c = []
     for a in range(3):
-        t = (x[a] - mesh.origin[a]) * (1.0 / mesh.cell_size[a])
+        # Python-float constants act as weak scalars: rounded to x's dtype at use
+        t = (x[a] - float(mesh.origin[a])) * (1.0 / float(mesh.cell_size[a]))
         f = np.floor(t)
         f = np.where(f >= 0, f, 0)
         f = np.where(f >= mesh.dims[a], mesh.dims[a] - 1, f)
@@ -129,14 +134,14 @@ def _ghost(i, n, bc):
     return np.clip(i, 0, n - 1)
 
 
-def trilinear(F, x, mesh: MicroMesh):
+def trilinear(F, x, mesh: MicroMesh, arith=np.float64):
     """C-5: cell-centred field F[k][nz][ny][nx] at x (3 x n), weights from
-    s = (x - o)/h - 1/2, ghost cells by the boundary rule.  Returns k x n (float64)."""
-    F = np.asarray(F, dtype=np.float64)
+    s = (x - o)/h - 1/2, ghost cells by the boundary rule.  Returns k x n (arith)."""
+    F = np.asarray(F, dtype=arith)
     K = F.shape[0]
     i0, fr = [], []
     for a in range(3):
-        t = (x[a] - mesh.origin[a]) * (1.0 / mesh.cell_size[a])
+        t = (x[a] - float(mesh.origin[a])) * (1.0 / float(mesh.cell_size[a]))
         s = t - 0.5
         fl = np.floor(s)
         i = fl.astype(np.int64)
@@ -146,7 +151,7 @@ def trilinear(F, x, mesh: MicroMesh):
         f = np.where(lowm, 0.0, np.where(highm, 1.0, f))
         i0.append(i)
         fr.append(f)
-    out = np.zeros((K, x.shape[1]))
+    out = np.zeros((K, x.shape[1]), arith)
     for c in range(2):
         for b in range(2):
             for a in range(2):
@@ -172,7 +177,7 @@ def _apply_bc(xa, ua, lo, hi, bc):
 # ---- the step ------------------------------------------------------------------------
 
 def micro_advance(mesh: MicroMesh, props: MicroProps, x, u, d, T, w, F, dt, nsteps, acc=None,
-                  store=np.float32):
+                  store=np.float32, arith=np.float64):
     """``nsteps`` sub-steps of length dt for every droplet, field F frozen (C-7).
 
     x, u: 3 x n; d, T, w: n; F: 5 x nz x ny x nx = (u_x, u_y, u_z, T_f, rho_v).
@@ -184,39 +189,40 @@ def micro_advance(mesh: MicroMesh, props: MicroProps, x, u, d, T, w, F, dt, nste
     u = np.array(u, dtype=store)
     d = np.array(d, dtype=store)
     T = np.array(T, dtype=store)
-    w64 = np.asarray(w, dtype=store).astype(np.float64)
+    w64 = np.asarray(w, dtype=store).astype(arith)
     F = np.asarray(F, dtype=store)
     ncell = int(np.prod(mesh.dims))
     if acc is None:
         acc = np.zeros((5, ncell))
-    g = np.asarray(props.gravity, dtype=np.float64)[:, None]
+    g = np.asarray(props.gravity, dtype=arith)[:, None]
+    dt = arith(dt)
     lo = [float(mesh.origin[a]) for a in range(3)]
     hi = [float(mesh.origin[a] + mesh.dims[a] * mesh.cell_size[a]) for a in range(3)]
     n_clamped = 0
     for _ in range(nsteps):
-        xp, up = x.astype(np.float64), u.astype(np.float64)
-        dp, Tp = d.astype(np.float64), T.astype(np.float64)
+        xp, up = x.astype(arith), u.astype(arith)
+        dp, Tp = d.astype(arith), T.astype(arith)
         # 1 deposit cell = cell of the start position (C-10)
         cell = cell_index(xp, mesh)
         # 2 fluid state at x_p: velocity, temperature, vapour density (C-5)
-        f = trilinear(F, xp, mesh)
+        f = trilinear(F, xp, mesh, arith)
         uf, Tf, rv = f[0:3], f[3], f[4]
         # 3 drag, semi-implicit Euler (Eq. 9-10)
         slip = uf - up
         Re = np.sqrt(np.sum(slip * slip, axis=0)) * dp / props.nu_f
         tau = props.rho_p * dp * dp / (18.0 * props.rho_f * props.nu_f)
-        h = dt / (tau / drag_factor(Re, props.drag_law))
+        h = dt / (tau / drag_factor(Re, props.drag_law, arith))
         un = (up + h * uf + dt * g) / (1.0 + h)
         xn = xp + dt * un
         # 4 mass (Eq. 7) and temperature (Eq. 12), explicit Euler from the start state
-        m = droplet_mass(dp, props.rho_p)
-        mdot = mass_transfer_rate(dp, rv, Tf, props)
+        m = droplet_mass(dp, props.rho_p, arith)
+        mdot = mass_transfer_rate(dp, rv, Tf, props, arith)
         mn = m + dt * mdot
         floor = 0.01 * m
         clamp = mn < floor
         n_clamped += int(np.count_nonzero(clamp))
         mn = np.where(clamp, floor, mn)
-        Tn = Tp + dt * heat_transfer_rate(dp, m, Tp, Tf, mdot, props)
+        Tn = Tp + dt * heat_transfer_rate(dp, m, Tp, Tf, mdot, props, arith)
         dn = np.cbrt(6.0 * mn / (math.pi * props.rho_p))
         # 5 fluid-side sources into the start cell (Eq. 8, 11, 13; C-8)
         for a in range(3):

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libscaletrack.so")
 
-ST_ABI_VERSION = 2
+ST_ABI_VERSION = 3
 
 ST_OK = 0
 STATUS_NAMES = {
@@ -105,8 +105,12 @@ class StMicroConfig(ctypes.Structure):
         ("latent", ctypes.c_double), ("nusselt", ctypes.c_double), ("s_vp", ctypes.c_double),
         ("device", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
+        ("arithmetic", ctypes.c_int32),
     ]
 
+
+ARITH_FP64 = 0
+ARITH_FP32 = 1
 
 SIGNATURES = {
     "st_config_default": (None, [ctypes.POINTER(StConfig)]),

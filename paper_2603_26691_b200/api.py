@@ -411,6 +411,7 @@ class MicroConfig:
     s_vp: float = 1.0
     device: int = 0
     stream: int | None = None
+    arithmetic: str = "fp64"     # "fp64" (C-28, default) | "fp32" (C-36)
 
     def to_c(self) -> N.StMicroConfig:
         c = N.StMicroConfig()
@@ -421,6 +422,9 @@ class MicroConfig:
         for f in ("rho_f", "nu_f", "rho_p", "D_v", "kappa_f", "cp_p", "latent", "nusselt", "s_vp"):
             setattr(c, f, float(getattr(self, f)))
         c.drag_law, c.device, c.stream = int(self.drag_law), int(self.device), self.stream
+        if self.arithmetic not in ("fp64", "fp32"):
+            raise ValueError(f"arithmetic must be 'fp64' or 'fp32', not {self.arithmetic!r}")
+        c.arithmetic = N.ARITH_FP32 if self.arithmetic == "fp32" else N.ARITH_FP64
         return c
 
 

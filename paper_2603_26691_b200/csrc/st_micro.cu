@@ -50,20 +50,53 @@ __device__ __forceinline__ int ghost(int i, int n, int bc) {
   return i < 0 ? 0 : (i > n - 1 ? n - 1 : i);
 }
 
-__device__ __forceinline__ int cell_axis(double x, double lo, double ih, int n) {
-  double f = floor((x - lo) * ih);
-  if (!(f >= 0.0)) return 0;
-  if (f >= (double)n) return n - 1;
+// Arithmetic-precision overloads: fp64 is the default mode (C-28), fp32 the opt-in mode
+// (reading C-36): the same operations in the same order, each rounded to binary32.
+__device__ __forceinline__ double m_floor(double v) { return floor(v); }
+__device__ __forceinline__ float m_floor(float v) { return floorf(v); }
+__device__ __forceinline__ double m_sqrt(double v) { return sqrt(v); }
+__device__ __forceinline__ float m_sqrt(float v) { return sqrtf(v); }
+__device__ __forceinline__ double m_exp(double v) { return exp(v); }
+__device__ __forceinline__ float m_exp(float v) { return expf(v); }
+__device__ __forceinline__ double m_cbrt(double v) { return cbrt(v); }
+__device__ __forceinline__ float m_cbrt(float v) { return cbrtf(v); }
+// Re^0.687: fp64 via exp2/log2 (within a few fp64 ulp of libm pow), fp32 via powf
+__device__ __forceinline__ double m_pow0687(double v) { return exp2(0.687 * log2(v)); }
+__device__ __forceinline__ float m_pow0687(float v) { return powf(v, 0.687f); }
+
+template <typename R>
+__device__ __forceinline__ int cell_axis(R x, R lo, R ih, int n) {
+  R f = m_floor((x - lo) * ih);
+  if (!(f >= R(0))) return 0;
+  if (f >= (R)n) return n - 1;
   return (int)f;
 }
 
-__global__ void __launch_bounds__(256, 4) k_micro(MicroArgs a) {
+// One thread per droplet (whole warps iterate together: the deposit reduction is
+// warp-collective).  R = arithmetic type; the state is fp32 storage in both modes and
+// the per-droplet deposits are summed in fp64 (the accumulators are fp64, C-28).
+template <typename R>
+__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 4) k_micro(MicroArgs a) {
   const int64_t ncell = (int64_t)a.nx * a.ny * a.nz;
   const int dims[3] = {a.nx, a.ny, a.nz};
+  // every host-folded fp64 constant rounded once to R (as numpy rounds a Python float
+  // operand to the array's dtype)
+  R lo[3], hi[3], L[3], ih[3], lo2[3], hi2[3], g[3];
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = (R)a.lo[k];
+    hi[k] = (R)a.hi[k];
+    L[k] = (R)a.L[k];
+    ih[k] = (R)a.ih[k];
+    lo2[k] = (R)(2.0 * a.lo[k]);
+    hi2[k] = (R)(2.0 * a.hi[k]);
+    g[k] = (R)a.g[k];
+  }
+  const R dt = (R)a.dt, rho_p = (R)a.rho_p, nu_f = (R)a.nu_f, c18 = (R)a.c18, c_m = (R)a.c_m, c_q = (R)a.c_q,
+          c_d = (R)a.c_d, c_m6 = (R)a.c_m6, s_vp = (R)a.s_vp, latent = (R)a.latent, cp_p = (R)a.cp_p;
+  const R one = 1, half = 0.5;
   unsigned long long clamps = 0, cfl = 0;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // whole warps iterate together (the deposit reduction below is warp-collective)
   const int64_t n_round = (a.n + 31) & ~(int64_t)31;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
     const bool valid = i < a.n;
@@ -71,25 +104,25 @@ __global__ void __launch_bounds__(256, 4) k_micro(MicroArgs a) {
     float xs[3] = {a.x[j], a.x[a.n + j], a.x[2 * a.n + j]};
     float us[3] = {a.u[j], a.u[a.n + j], a.u[2 * a.n + j]};
     float ds = a.d[j], Ts = a.T[j];
-    const double wn = valid ? -(double)a.w[j] : 0.0;
+    const R wn = valid ? -(R)a.w[j] : R(0);
     for (int s = 0; s < a.nsteps; ++s) {
-      double xp[3] = {xs[0], xs[1], xs[2]}, up[3] = {us[0], us[1], us[2]};
-      const double dp = ds, Tp = Ts;
+      R xp[3] = {xs[0], xs[1], xs[2]}, up[3] = {us[0], us[1], us[2]};
+      const R dp = ds, Tp = Ts;
       // 1 deposit cell = cell of the start position (C-10)
       int c[3];
-      for (int k = 0; k < 3; ++k) c[k] = cell_axis(xp[k], a.lo[k], a.ih[k], dims[k]);
+      for (int k = 0; k < 3; ++k) c[k] = cell_axis<R>(xp[k], lo[k], ih[k], dims[k]);
       const int64_t cell = ((int64_t)c[2] * a.ny + c[1]) * a.nx + c[0];
       // 2 trilinear (u_f, T_f, rho_v) at x_p (C-5), loop order z, y, x as the oracle
       int i0[3];
-      double fr[3];
+      R fr[3];
       for (int k = 0; k < 3; ++k) {
-        double t = (xp[k] - a.lo[k]) * a.ih[k];
-        double sv = t - 0.5;
-        double fl = floor(sv);
+        R t = (xp[k] - lo[k]) * ih[k];
+        R sv = t - half;
+        R fl = m_floor(sv);
         int ii = (int)fl;
-        double f = sv - fl;
-        if (ii < -1) { ii = -1; f = 0.0; }
-        if (ii > dims[k] - 1) { ii = dims[k] - 1; f = 1.0; }
+        R f = sv - fl;
+        if (ii < -1) { ii = -1; f = R(0); }
+        if (ii > dims[k] - 1) { ii = dims[k] - 1; f = one; }
         i0[k] = ii;
         fr[k] = f;
       }
@@ -98,50 +131,51 @@ __global__ void __launch_bounds__(256, 4) k_micro(MicroArgs a) {
         gi[k][0] = ghost(i0[k], dims[k], a.bc[k]);
         gi[k][1] = ghost(i0[k] + 1, dims[k], a.bc[k]);
       }
-      double fv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      R fv[5] = {0, 0, 0, 0, 0};
 #pragma unroll
       for (int cz = 0; cz < 2; ++cz)
 #pragma unroll
         for (int cy = 0; cy < 2; ++cy)
 #pragma unroll
           for (int cx = 0; cx < 2; ++cx) {
-            double wt = ((cx ? fr[0] : 1.0 - fr[0]) * (cy ? fr[1] : 1.0 - fr[1])) * (cz ? fr[2] : 1.0 - fr[2]);
+            R wt = ((cx ? fr[0] : one - fr[0]) * (cy ? fr[1] : one - fr[1])) * (cz ? fr[2] : one - fr[2]);
             const int64_t cc = ((int64_t)gi[2][cz] * a.ny + gi[1][cy]) * a.nx + gi[0][cx];
 #pragma unroll
-            for (int k = 0; k < 5; ++k) fv[k] = fv[k] + wt * (double)__ldg(a.F + k * ncell + cc);
+            for (int k = 0; k < 5; ++k) fv[k] = fv[k] + wt * (R)__ldg(a.F + k * ncell + cc);
           }
-      const double Tf = fv[3], rv = fv[4];
+      const R Tf = fv[3], rv = fv[4];
       // 3 drag, semi-implicit Euler (Eq. 9-10)
-      double sl[3] = {fv[0] - up[0], fv[1] - up[1], fv[2] - up[2]};
-      const double Re = sqrt((sl[0] * sl[0] + sl[1] * sl[1]) + sl[2] * sl[2]) * dp / a.nu_f;
-      double fdr = 1.0;
-      if (a.drag_law == ST_DRAG_SCHILLER_NAUMANN)
-        fdr = Re <= 1000.0 ? 1.0 + 0.15 * exp2(0.687 * log2(Re)) : 0.44 * Re / 24.0;   // Re = 0 -> 1 (C-22)
-      const double tau = a.rho_p * dp * dp / a.c18;
-      const double h = a.dt / (tau / fdr);
-      double un[3], xn[3];
+      R sl[3] = {fv[0] - up[0], fv[1] - up[1], fv[2] - up[2]};
+      const R Re = m_sqrt((sl[0] * sl[0] + sl[1] * sl[1]) + sl[2] * sl[2]) * dp / nu_f;
+      R fdr = one;
+      if (a.drag_law == ST_DRAG_SCHILLER_NAUMANN)   // Re = 0 -> 1 (C-22)
+        fdr = Re <= R(1000) ? one + R(0.15) * m_pow0687(Re) : R(0.44) * Re / R(24);
+      const R tau = rho_p * dp * dp / c18;
+      const R h = dt / (tau / fdr);
+      R un[3], xn[3];
       for (int k = 0; k < 3; ++k) {
-        un[k] = ((up[k] + h * fv[k]) + a.dt * a.g[k]) / (1.0 + h);
-        xn[k] = xp[k] + a.dt * un[k];
+        un[k] = ((up[k] + h * fv[k]) + dt * g[k]) / (one + h);
+        xn[k] = xp[k] + dt * un[k];
       }
       // 4 mass (Eq. 7, Magnus C-30) and temperature (Eq. 12), explicit Euler
-      const double m = a.c_m6 * (dp * dp * dp);     // d^3 to <= 1.5 fp64 ulp of the oracle's pow
-      const double tc = Tf - 273.15;
-      const double es = 610.94 * exp(17.625 * tc / (tc + 243.04));
-      const double rs = es / (461.5 * Tf);
-      const double svf = rv / rs;
-      const double mdot = a.c_m * dp * rs * (svf - a.s_vp);
-      double mn = m + a.dt * mdot;
-      const double mfloor = 0.01 * m;
+      const R m = c_m6 * (dp * dp * dp);     // d^3 to <= 1.5 ulp of the oracle's pow
+      const R tc = Tf - R(273.15);
+      const R es = R(610.94) * m_exp(R(17.625) * tc / (tc + R(243.04)));
+      const R rs = es / (R(461.5) * Tf);
+      const R svf = rv / rs;
+      const R mdot = c_m * dp * rs * (svf - s_vp);
+      R mn = m + dt * mdot;
+      const R mfloor = R(0.01) * m;
       if (mn < mfloor) { mn = mfloor; clamps += valid; }
-      const double q = a.c_q * dp * (Tf - Tp);
-      const double Tn = Tp + a.dt * ((q - a.latent * mdot) / (m * a.cp_p));
-      const double dn = cbrt(6.0 * mn / a.c_d);
-      // 5 fluid-side sources into the start cell (Eq. 8, 11, 13; C-8, C-33)
+      const R q = c_q * dp * (Tf - Tp);
+      const R Tn = Tp + dt * ((q - latent * mdot) / (m * cp_p));
+      const R dn = m_cbrt(R(6) * mn / c_d);
+      // 5 fluid-side sources into the start cell (Eq. 8, 11, 13; C-8, C-33), each
+      // droplet's deposit computed in R, summed in fp64
       double dep[5];
-      for (int k = 0; k < 3; ++k) dep[k] = wn * ((mn * un[k] - m * up[k]) - m * a.g[k] * a.dt);
-      dep[3] = wn * (mn - m);
-      dep[4] = wn * a.cp_p * (mn * Tn - m * Tp);
+      for (int k = 0; k < 3; ++k) dep[k] = (double)(wn * ((mn * un[k] - m * up[k]) - m * g[k] * dt));
+      dep[3] = (double)(wn * (mn - m));
+      dep[4] = (double)(wn * cp_p * (mn * Tn - m * Tp));
       // Runs of lanes with the same start cell (contiguous in a binned store) are summed
       // into the run's first lane by a segmented suffix scan; one fp64 reduction per run.
       const int key = valid ? (int)cell : -1 - lane;
@@ -149,26 +183,28 @@ __global__ void __launch_bounds__(256, 4) k_micro(MicroArgs a) {
       const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != key);
       const unsigned above = lane == 31 ? 0u : heads & (0xffffffffu << (lane + 1));
       const int end = above ? __ffs(above) - 1 : 32;
+      if (__any_sync(0xffffffffu, end - lane > 1)) {   // skip the scan when every run is one lane
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
+        for (int off = 1; off < 32; off <<= 1) {
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {
-          const double o = __shfl_down_sync(0xffffffffu, dep[k], off);
-          if (lane + off < end) dep[k] = dep[k] + o;
+          for (int k = 0; k < 5; ++k) {
+            const double o = __shfl_down_sync(0xffffffffu, dep[k], off);
+            if (lane + off < end) dep[k] = dep[k] + o;
+          }
         }
       }
       if (valid && ((heads >> lane) & 1u))
         for (int k = 0; k < 5; ++k) atomicAdd(a.acc + k * ncell + cell, dep[k]);
       // 6 walls / periodic (C-11, C-12), round the state to fp32
       for (int k = 0; k < 3; ++k) {
-        double v = xn[k];
+        R v = xn[k];
         if (a.bc[k] == ST_BC_PERIODIC) {
-          if (v < a.lo[k]) v = v + a.L[k];
-          else if (v >= a.hi[k]) v = v - a.L[k];
-          if (v < a.lo[k] || v >= a.hi[k]) cfl += valid;
+          if (v < lo[k]) v = v + L[k];
+          else if (v >= hi[k]) v = v - L[k];
+          if (v < lo[k] || v >= hi[k]) cfl += valid;
         } else {
-          if (v < a.lo[k]) { v = 2.0 * a.lo[k] - v; un[k] = -un[k]; if (v > a.hi[k]) cfl += valid; }
-          else if (v > a.hi[k]) { v = 2.0 * a.hi[k] - v; un[k] = -un[k]; if (v < a.lo[k]) cfl += valid; }
+          if (v < lo[k]) { v = lo2[k] - v; un[k] = -un[k]; if (v > hi[k]) cfl += valid; }
+          else if (v > hi[k]) { v = hi2[k] - v; un[k] = -un[k]; if (v < lo[k]) cfl += valid; }
         }
         xs[k] = (float)v;
         // C-12 fix-up in storage precision: a wrap that rounds onto hi is stored as lo
@@ -232,6 +268,7 @@ extern "C" st_status st_micro_advance(const st_micro_config* c, int64_t n, float
     if (c->dims[k] < 1 || !(c->cell_size[k] > 0.0) || (c->bc[k] != ST_BC_PERIODIC && c->bc[k] != ST_BC_REFLECT))
       return ST_ERR_INVALID_ARG;
   if ((int64_t)c->dims[0] * c->dims[1] * c->dims[2] >= (1ll << 31)) return ST_ERR_INVALID_ARG;
+  if (c->arithmetic != ST_ARITH_FP64 && c->arithmetic != ST_ARITH_FP32) return ST_ERR_INVALID_ARG;
   if (c->drag_law != ST_DRAG_STOKES && c->drag_law != ST_DRAG_SCHILLER_NAUMANN) return ST_ERR_INVALID_ARG;
   if (!(c->rho_p > 0.0) || !(c->rho_f > 0.0) || !(c->nu_f > 0.0) || !(c->cp_p > 0.0)) return ST_ERR_INVALID_ARG;
   if (n_clamped) *n_clamped = 0;
@@ -325,7 +362,10 @@ extern "C" st_status st_micro_advance(const st_micro_config* c, int64_t n, float
   const int64_t need = (n + 255) / 256;   // block size 256 = 8 whole warps
   const int64_t cap = (int64_t)nsm * 8;            // 8 resident 256-thread CTAs per SM
   const int grid = (int)(need < cap ? need : cap);
-  k_micro<<<grid, 256, 0, s>>>(a);
+  if (c->arithmetic == ST_ARITH_FP32)
+    k_micro<float><<<grid, 256, 0, s>>>(a);
+  else
+    k_micro<double><<<grid, 256, 0, s>>>(a);
   unsigned long long h[2] = {0, 0};
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s);

@@ -119,8 +119,9 @@ def test_micro_config_layout_default_and_validation(lib):
 #include <stddef.h>
 #include "scaletrack.h"
 int main(void){
-  printf("%zu %zu %zu %zu\n", sizeof(st_micro_config), offsetof(st_micro_config, D_v),
-         offsetof(st_micro_config, device), offsetof(st_micro_config, stream));
+  printf("%zu %zu %zu %zu %zu %d %d\n", sizeof(st_micro_config), offsetof(st_micro_config, D_v),
+         offsetof(st_micro_config, device), offsetof(st_micro_config, stream),
+         offsetof(st_micro_config, arithmetic), (int)ST_ARITH_FP64, (int)ST_ARITH_FP32);
   return 0;
 }'''
     tmp = os.path.join(ROOT, "build")
@@ -130,7 +131,8 @@ int main(void){
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", exe, c_src])
     vals = [int(v) for v in subprocess.check_output([exe]).split()]
     M = N.StMicroConfig
-    assert vals == [ctypes.sizeof(M), M.D_v.offset, M.device.offset, M.stream.offset]
+    assert vals == [ctypes.sizeof(M), M.D_v.offset, M.device.offset, M.stream.offset, M.arithmetic.offset,
+                    N.ARITH_FP64, N.ARITH_FP32]
     c = M()
     lib.st_micro_config_default(ctypes.byref(c))
     py = MicroConfig().to_c()
@@ -149,3 +151,9 @@ int main(void){
     lib.st_micro_config_default(ctypes.byref(bad))
     bad.cell_size[1] = 0.0
     assert lib.st_micro_advance(ctypes.byref(bad), 0, None, None, None, None, None, None, 1e-3, 1, None, None) == 1
+    bad.cell_size[1] = 1.0
+    bad.arithmetic = 2                                # neither fp64 nor fp32
+    assert lib.st_micro_advance(ctypes.byref(bad), 0, None, None, None, None, None, None, 1e-3, 1, None, None) == 1
+    assert MicroConfig(arithmetic="fp32").to_c().arithmetic == N.ARITH_FP32
+    with pytest.raises(ValueError):
+        MicroConfig(arithmetic="bf16").to_c()

@@ -22,12 +22,12 @@ def _setup(n, dims=(24, 20, 12), h=0.125, bc=(0, 0, 1), seed=11, field_kw=None, 
     return mesh, F, x, u, d, T, w
 
 
-def _gpu_run(mesh, props, F, x, u, d, T, w, dt, calls):
+def _gpu_run(mesh, props, F, x, u, d, T, w, dt, calls, arithmetic="fp64"):
     from paper_2603_26691_b200 import MicroConfig, micro_advance
     cfg = MicroConfig(dims=mesh.dims, origin=mesh.origin, cell_size=mesh.cell_size, bc=mesh.bc,
                       rho_f=props.rho_f, nu_f=props.nu_f, rho_p=props.rho_p, gravity=props.gravity,
                       drag_law=props.drag_law, D_v=props.D_v, kappa_f=props.kappa_f, cp_p=props.cp_p,
-                      latent=props.latent, nusselt=props.nusselt, s_vp=props.s_vp)
+                      latent=props.latent, nusselt=props.nusselt, s_vp=props.s_vp, arithmetic=arithmetic)
     dev = torch.device("cuda:0")
     tx, tu, td, tT, tw = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, u, d, T, w))
     tF = torch.from_numpy(np.ascontiguousarray(F)).to(dev)
@@ -200,3 +200,73 @@ def test_micro_deposit_start_cell_gpu():
     for k in (0, 2, 3, 4):
         assert np.flatnonzero(g[4][k]).tolist() == [start], k
     _compare(g, o, mesh, "start-cell")
+
+
+# ---- fp32 arithmetic mode (reading C-36; bounds in tests/micro_bounds.py) -------------
+
+def _stable(n, bc=(0, 0, 1), seed=11, binned=False):
+    mesh, F, x, u, d, T, w = _setup(n, bc=bc, seed=seed, drop_kw={"d_range": (10e-6, 30e-6)})
+    if binned:
+        c = np.floor(x.astype(np.float64) / 0.125).astype(np.int64)
+        o = np.lexsort((c[0], c[1], c[2]))
+        x, u, d, T, w = x[:, o].copy(), u[:, o].copy(), d[o].copy(), T[o].copy(), w[o].copy()
+    return mesh, F, x, u, d, T, w
+
+
+@pytest.mark.parametrize("n,calls,bc,binned", [
+    (20_000, (3, 2), (0, 0, 1), False),     # many tiles + ragged tail, two calls accumulate
+    (8 * 24 * 20 * 12 + 77, (2, 3), (0, 0, 1), True),   # binned: long same-cell lane runs
+    (257, (4,), (1, 1, 1), False),          # one full CTA + 1, all walls reflecting
+    (1, (6,), (0, 0, 0), False),            # a single droplet, fully periodic
+])
+def test_micro_fp32_parity(n, calls, bc, binned):
+    """The fp32 kernel against the fp32 oracle (same operations, both binary32; only the
+    libm-vs-CUDA exp / pow / cbrt ulps differ) and against the fp64 oracle, each within
+    the binary32 rounding bound of tests/micro_bounds.py.  dt = 1 ms, 10-30 um droplets:
+    the explicit Eq. 7 / Eq. 12 updates are contractive (test_oracle_micro._stable_cloud)."""
+    from tests.micro_bounds import check_fp32, run_with_gross
+    mesh, F, x, u, d, T, w = _stable(n, bc=bc, binned=binned)
+    props = M.MicroProps()
+    dt, ns = 1e-3, sum(calls)
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, dt, calls, arithmetic="fp32")
+    r32 = run_with_gross(mesh, props, x, u, d, T, w, F, dt, ns, arith=np.float32)
+    r64 = run_with_gross(mesh, props, x, u, d, T, w, F, dt, ns)
+    u_scale = float(np.max(np.abs(F[:3]))) + 9.81 * dt * ns
+    check_fp32(g, r32[:6], r64[6], mesh, ns, u_scale, f"vs fp32 oracle n={n}")
+    check_fp32(g, r64[:6], r64[6], mesh, ns, u_scale, f"vs fp64 oracle n={n}")
+    assert g[5] == r32[5] == r64[5]
+
+
+def test_micro_fp32_mass_floor_clamps_match():
+    """C-32 in fp32 mode: the clamp decision is taken in binary32 on both sides."""
+    mesh, F, x, u, d, T, w = _setup(3000, field_kw={"T0": 300.0, "rho_v0": 1e-4},
+                                    drop_kw={"d_range": (0.5e-6, 3e-6)})
+    props = M.MicroProps()
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 0.2, (1,), arithmetic="fp32")
+    o = M.micro_advance(mesh, props, x, u, d, T, w, F, 0.2, 1, arith=np.float32)
+    assert o[5] > 0 and g[5] == o[5]
+    np.testing.assert_allclose(g[2], o[2], rtol=8 * 1.2e-7)
+
+
+def test_micro_fp32_full_size_sampled():
+    """2e7 droplets on the bench grid in fp32 mode: sampled droplet states against the
+    fp32 oracle run on those droplets alone (droplets are independent given the frozen
+    field); the vapour ledger of the whole field closes to the binary32 bound."""
+    from tests.micro_bounds import C_ACC, EPS32, STATE_ULPS
+    dims, h = (192, 192, 72), 1.0 / 32
+    mesh = M.MicroMesh(dims=dims, origin=(0.0, 0.0, 0.0), cell_size=(h,) * 3, bc=(0, 0, 1))
+    F = synth.micro_field(dims, mesh.origin, mesh.cell_size, seed=4)
+    n = 20_000_000
+    x, u, d, T, w = synth.droplets_np(n, (0.0, 0.0, 0.0), (6.0, 6.0, 2.25), seed=9, d_range=(10e-6, 30e-6))
+    props = M.MicroProps()
+    g = _gpu_run(mesh, props, F, x, u, d, T, w, 1e-3, (2,), arithmetic="fp32")
+    idx = np.random.default_rng(0).choice(n, 2000, replace=False)
+    o = M.micro_advance(mesh, props, x[:, idx], u[:, idx], d[idx], T[idx], w[idx], F, 1e-3, 2, arith=np.float32)
+    tol = STATE_ULPS * 2 * EPS32
+    assert np.max(np.abs(g[0][:, idx].astype(np.float64) - o[0])) <= tol * 6.0
+    assert np.max(np.abs(g[2][idx] / o[2] - 1)) <= tol
+    assert np.max(np.abs(g[3][idx] / o[3] - 1)) <= tol
+    m0 = M.droplet_mass(d.astype(np.float64), props.rho_p)
+    m1 = M.droplet_mass(g[2].astype(np.float64), props.rho_p)
+    dM = np.sum(w * (m1 - m0))
+    assert abs(g[4][3].sum() + dM) <= C_ACC * EPS32 * np.sum(w * (m0 + m1)) * 2

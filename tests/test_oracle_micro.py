@@ -269,3 +269,79 @@ def test_periodic_wrap_stays_half_open_fp32(side):
     if side == "lo":
         assert xn[0, 0] == np.float32(0.0)
     assert un[0, 0] == np.float32(u[0, 0])                 # a wrap keeps the velocity
+
+
+# ---- fp32 arithmetic mode (reading C-36) ----------------------------------------------
+
+def _stable_cloud(n=20_000):
+    """Droplets of 10-30 um with dt = 1 ms: dt / tau_T <= 0.71 and dt / tau_p <= 3.3 under
+    the semi-implicit drag, so the explicit Eq. 7 / Eq. 12 updates are contractive and an
+    fp32 rounding is not amplified from step to step."""
+    dims, h = (24, 20, 12), 0.125
+    mesh = M.MicroMesh(dims=dims, origin=(0.0, 0.0, 0.0), cell_size=(h,) * 3, bc=(0, 0, 1))
+    F = synth.micro_field(dims, mesh.origin, mesh.cell_size, seed=11)
+    x, u, d, T, w = synth.droplets_np(n, (0.0, 0.0, 0.0), (3.0, 2.5, 1.5), seed=12, d_range=(10e-6, 30e-6))
+    return mesh, F, x, u, d, T, w
+
+
+def test_fp32_mode_rounds_every_operation_to_binary32():
+    """C-36: the closures and the interpolation compute in float32 (no silent promotion
+    through a float64 constant), and the fp32 step is not the fp64 step."""
+    d = np.array([12e-6, 25e-6], np.float32)
+    Tf = np.array([282.0, 284.5], np.float32)
+    rv = np.array([9e-3, 8e-3], np.float32)
+    f32 = np.float32
+    assert M.saturation_vapor_density(Tf, f32).dtype == f32
+    assert M.mass_transfer_rate(d, rv, Tf, P, f32).dtype == f32
+    assert M.droplet_mass(d, P.rho_p, f32).dtype == f32
+    assert M.drag_factor(np.array([0.0, 3.0, 2e3], f32), M.DRAG_SCHILLER_NAUMANN, f32).dtype == f32
+    m = M.droplet_mass(d, P.rho_p, f32)
+    assert M.heat_transfer_rate(d, m, Tf, Tf, m, P, f32).dtype == f32
+    mesh, F, x, u, d, T, w = _stable_cloud(2000)
+    assert M.trilinear(F, x, mesh, f32).dtype == f32
+    r64 = M.micro_advance(mesh, P, x, u, d, T, w, F, 1e-3, 3)
+    r32 = M.micro_advance(mesh, P, x, u, d, T, w, F, 1e-3, 3, arith=f32)
+    assert np.mean(r32[2] == r64[2]) < 0.9           # d: the modes really differ
+    assert r32[4].dtype == np.float64                # accumulators stay fp64
+
+
+@pytest.mark.parametrize("nsteps", [1, 5, 20])
+def test_fp32_mode_within_rounding_bound_of_fp64(nsteps):
+    """The fp32 oracle stays within the binary32 rounding bound of the fp64 oracle
+    (tests/micro_bounds.py) on a 2e4-droplet stable cloud."""
+    from tests.micro_bounds import check_fp32, run_with_gross
+    mesh, F, x, u, d, T, w = _stable_cloud()
+    ref = run_with_gross(mesh, P, x, u, d, T, w, F, 1e-3, nsteps)
+    got = M.micro_advance(mesh, P, x, u, d, T, w, F, 1e-3, nsteps, arith=np.float32)
+    u_scale = float(np.max(np.abs(F[:3]))) + 9.81 * 1e-3 * nsteps
+    check_fp32(got, ref[:6], ref[6], mesh, nsteps, u_scale, f"n={nsteps}")
+    assert got[5] == ref[5]
+
+
+def test_fp32_temperature_relaxation_closed_form():
+    """Eq. 12 closed form (test_temperature_relaxation_exact_discrete) in fp32 mode:
+    T_n - T_f = (1 - dt/tau_T)^n (T_0 - T_f) to the binary32 rounding of 25 sub-steps."""
+    mesh = _box()
+    props = M.MicroProps(gravity=(0.0, 0.0, 0.0))
+    Tf, T0, d0, dt, n = 285.0, 281.0, 20e-6, 2e-3, 25
+    F = _uniform_field(mesh, Tf=Tf, rv=float(M.saturation_vapor_density(Tf)))
+    m = math.pi / 6 * props.rho_p * d0 ** 3
+    tau_T = m * props.cp_p / (math.pi * 2.0 * props.kappa_f * d0)
+    x, u, d, T, w = _one(d=d0, T=T0)
+    _, _, _, Tn, _, _ = M.micro_advance(mesh, props, x, u, d, T, w, F, dt, n, arith=np.float32)
+    want = Tf + (1 - dt / tau_T) ** n * (T0 - Tf)
+    assert abs(float(Tn[0]) - want) <= 4 * n * np.finfo(np.float32).eps * Tf
+    assert float(Tn[0]) != pytest.approx(T0, abs=0.5)
+
+
+def test_fp32_vapour_ledger_closes():
+    """S:186 in fp32 mode: the droplets' mass gain plus the vapour source is zero to the
+    binary32 rounding of the per-droplet mass differences."""
+    from tests.micro_bounds import C_ACC, EPS32
+    mesh, F, x, u, d, T, w = _stable_cloud(5000)
+    _, _, dn, _, acc, _ = M.micro_advance(mesh, P, x, u, d, T, w, F, 1e-3, 4, arith=np.float32)
+    m0 = M.droplet_mass(d.astype(np.float64), P.rho_p)
+    m1 = M.droplet_mass(dn.astype(np.float64), P.rho_p)
+    dM = np.sum(w * (m1 - m0))
+    assert dM != 0
+    assert abs(dM + acc[3].sum()) <= C_ACC * EPS32 * np.sum(w * (m0 + m1)) * 4
