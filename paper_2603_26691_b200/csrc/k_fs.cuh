@@ -34,7 +34,7 @@ constexpr int kFsWarps = ST_FS_WARPS;
 constexpr uint32_t kFsTx = 8u * kIpBoxF * 4u + kFsBoxI * 8u;
 
 template <int BCM, int SPEC>
-__global__ void __launch_bounds__(32 * kFsWarps, 2) k_fs(const __grid_constant__ StepArgs a) {
+__global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(const __grid_constant__ StepArgs a) {
   constexpr int SH = 3;
   constexpr bool VP = (SPEC & kSpecVP) != 0;
   constexpr bool SUB = (SPEC & kSpecSub) != 0;

@@ -20,6 +20,8 @@ ap.add_argument("--n", type=int, default=200_000_000)
 ap.add_argument("--nsteps", type=int, default=1)
 ap.add_argument("--calls", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=3)
+ap.add_argument("--arith", choices=("fp64", "fp32"), default="fp64", help="arithmetic mode (C-28 / C-36)")
+ap.add_argument("--dt", type=float, default=1e-3)
 ap.add_argument("--unsorted", action="store_true", help="random order instead of the binned (cell-sorted) store")
 a = ap.parse_args()
 
@@ -37,25 +39,26 @@ if not a.unsorted:     # the binned store (C-15): droplets ordered by their cell
     x = x[:, torch.argsort(key)].contiguous()
     del c, key
 u = torch.zeros((3, n), device=dev)
-d = 5e-6 + 25e-6 * torch.rand(n, generator=g, device=dev)
+d = 10e-6 + 20e-6 * torch.rand(n, generator=g, device=dev)   # dt / tau_T <= 0.71 at dt = 1 ms
 T = 281.0 + 4.0 * torch.rand(n, generator=g, device=dev)
 w = torch.full((n,), 100.0, device=dev)
 acc = torch.zeros((5, 72, 192, 192), dtype=torch.float64, device=dev)
-cfg = MicroConfig(dims=dims, cell_size=(h,) * 3, bc=(0, 0, 1))
+cfg = MicroConfig(dims=dims, cell_size=(h,) * 3, bc=(0, 0, 1), arithmetic=a.arith)
 s = torch.cuda.current_stream()
 cfg.stream = s.cuda_stream
 for _ in range(a.warmup):
-    micro_advance(cfg, x, u, d, T, w, F, 5e-3, a.nsteps, acc)
+    micro_advance(cfg, x, u, d, T, w, F, a.dt, a.nsteps, acc)
 torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record(s)
-for _ in range(a.calls):
-    micro_advance(cfg, x, u, d, T, w, F, 5e-3, a.nsteps, acc)
-e1.record(s)
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.calls + 1)]
+ev[0].record(s)
+for k in range(a.calls):
+    micro_advance(cfg, x, u, d, T, w, F, a.dt, a.nsteps, acc)
+    ev[k + 1].record(s)
 torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / a.calls
+per = [ev[k].elapsed_time(ev[k + 1]) for k in range(a.calls)]
+ms = ev[0].elapsed_time(ev[-1]) / a.calls
 peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
 alg = n * (52 + 40 * a.nsteps)
 print(json.dumps({"metric": "droplet-updates/s (microphysics step, f3)", "value": n * a.nsteps / (ms * 1e-3),
-                  "n": n, "nsteps": a.nsteps, "binned": not a.unsorted, "ms_per_call": ms, "alg_bytes_per_call": alg,
+                  "n": n, "nsteps": a.nsteps, "arith": a.arith, "dt": a.dt, "binned": not a.unsorted, "ms_per_call": ms, "per_call_ms": per, "alg_bytes_per_call": alg,
                   "achieved_GBs": alg / (ms * 1e-3) / 1e9, "peaks": peaks}))
