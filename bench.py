@@ -103,7 +103,7 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -112,13 +112,14 @@ class ClockSampler:
             try:
                 sm.append(float(f[1]))
                 smax = float(f[2])
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for nm, v in zip(names, f[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": statistics.median(pw) if pw else None}
 
 
 def make_workload(name, G, particles):
@@ -538,6 +539,9 @@ def run_ours(args):
         # every step's copies are inside the timed region
         torch.cuda.synchronize()
         k0 = st.stats()["calls"]      # index of the first e2e call in the library's trace ring
+        esampler = ClockSampler(local)
+        esampler.start()
+        time.sleep(0.3)
         t_host0 = time.perf_counter()
         h0.record(stream)
         for s in range(k_e2e):
@@ -550,6 +554,15 @@ def run_ours(args):
         h1.record(stream)
         torch.cuda.synchronize()
         t_host1 = time.perf_counter()
+        # the device-resident loop again, right after (same thermal / power state): the
+        # e2e gap that is not the copies shows up as a difference of the two step times
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for s in range(k_e2e):
+            step(s, fields, S)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        eclocks = esampler.stop()
         ems = max(h0.elapsed_time(h1), 1e3 * (t_host1 - t_host0))   # host-blocking copies: wall clock bounds it
         if G > 1:
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
@@ -557,7 +570,8 @@ def run_ours(args):
             ems = float(t.item())
         e2e = {"value": n_total * k_e2e / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(Fh[0].numel() * 4), "d2h_bytes_per_step": int(Sh.numel() * 4),
-               "steps": k_e2e, "ms_per_step": ems / k_e2e}
+               "steps": k_e2e, "ms_per_step": ems / k_e2e, "clocks": eclocks,
+               "device_ms_per_step_after": d0.elapsed_time(d1) / k_e2e}
         try:   # where the e2e time goes: the library's CUDA-event ring (st_trace) of these calls
             tr = [st.trace(k0 + k) for k in range(k_e2e)]
             stp = [(t[2], t[3]) for t in tr]
