@@ -611,7 +611,7 @@ def run_ours(args):
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
                          "alg_bytes_per_launch": alg, "kernel_ms": kms},
-            "step_kernel_ms": adv_ms, "rebin_prep_ms": reb_ms, "rebins_in_timed_region": len(reb_list),
+            "step_kernel_ms": adv_ms, "step_kernel_ms_series": [round(v, 3) for v in adv], "rebin_prep_ms": reb_ms, "rebins_in_timed_region": len(reb_list),
             "f_move_chunk": f_move, "fused_rebins": st_stats["fused_rebins"],
             "general_rebins": st_stats["general_rebins"], "far_last_rebin": st_stats["last_far"],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,

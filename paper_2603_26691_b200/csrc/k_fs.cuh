@@ -72,13 +72,31 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
     tma_ids(st + kFsOffId, &a.tm_id66, (int)(first & ~1LL), bar + k);
   };
 
-  for (int item = blockIdx.x * kFsWarps + wib; item < n_items; item += warps_total) {
-    const int b0 = a.item_bin0[item];
-    const int b1 = (item + 1 < n_items) ? a.item_bin0[item + 1] : nbins;
+  const bool dyn = ST_DYN_ITEMS && a.item_ctr != nullptr;   // items as in k_ip
+  int item = blockIdx.x * kFsWarps + wib;
+  int hb0 = 0, hb1 = 0, hrel = 0;
+  int64_t hp0 = 0;
+  auto header = [&](int it) {
+    hb0 = a.item_bin0[it];
+    hb1 = (it + 1 < n_items) ? a.item_bin0[it + 1] : nbins;
+    hp0 = a.off[hb0];
+    hrel = (lane <= hb1 - hb0) ? (int)(a.off[hb0 + lane] - hp0) : 0;
+  };
+  if (item < n_items) header(item);
+  while (item < n_items) {
+    const int b0 = hb0, b1 = hb1;
     const int nb = b1 - b0;
-    const int64_t p0 = a.off[b0];
-    const int np = (int)(a.off[b1] - p0);
+    const int64_t p0 = hp0;
+    const int myrel = hrel;
+    const int np = __shfl_sync(kFull, myrel, nb);
     const int nbatch = (np + 63) >> 6;
+    int tk = 0;
+    if (dyn && lane == 0) tk = atomicAdd(a.item_ctr, 1);
+    int next = item + warps_total;
+    auto prefetch = [&]() {
+      if (dyn) next = warps_total + __shfl_sync(kFull, tk, 0);
+      if (next < n_items) header(next);
+    };
     int rx, ry, rz;
     cell_of_bin(g, a.bg, b0, rx, ry, rz);
     if (lane == 0) {
@@ -89,7 +107,7 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
       for (int k = 0; k < kFsStages && k < nbatch; ++k) issue(k, p0 + 64 * k);
     }
     __syncwarp();
-    if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
+    if (lane <= nb) rel[lane] = myrel;
     for (int k = lane; k < kTable; k += 32) run[k] = 0;
     mbar_wait(ibar, iphase);
     iphase ^= 1u;
@@ -401,10 +419,13 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
         issue(sk, p0 + base + 64 * kFsStages);
       }
       __syncwarp();
+      if (bi == 0) prefetch();
     }
+    if (nbatch == 0) prefetch();
     __syncwarp();
     flush();
     __syncwarp();
+    item = next;
   }
   if (flags) atomicOr(a.err, flags);
 }
@@ -421,6 +442,7 @@ int launch_fs_variant(const StepArgs& a, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fs<BCM, SPEC>, 32 * kFsWarps, smem);
     grid = nsm * (per > 0 ? per : 1);
   }
+  if (ST_DYN_ITEMS && a.item_ctr) cudaMemsetAsync(a.item_ctr, 0, sizeof(int), s);
   k_fs<BCM, SPEC><<<grid, 32 * kFsWarps, smem, s>>>(a);
   return 1;
 }

@@ -31,6 +31,10 @@ __device__ __forceinline__ float lg2_ftz(float x) {
   return r;
 }
 
+#ifndef ST_DYN_ITEMS
+#define ST_DYN_ITEMS 1   // step kernels take their items from a counter (k_ip, k_fs)
+#endif
+
 constexpr int kIpStages = 3;
 constexpr int kIpBoxF = 68;                          // 64 particles + 4 floats of 16-B alignment slack
 constexpr int kIpStageBytes = 8 * kIpBoxF * 4;       // 2176 = 17 x 128
@@ -75,13 +79,34 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
   }
   __syncwarp();
 
-  for (int item = blockIdx.x * kIpWarps + wib; item < n_items; item += warps_total) {
-    const int b0 = a.item_bin0[item];
-    const int b1 = (item + 1 < n_items) ? a.item_bin0[item + 1] : nbins;
+  // items: the first one per warp is static, the rest are handed out by a counter
+  // (ST_DYN_ITEMS; clustered loads make item sizes uneven) and their headers are
+  // fetched one item ahead, while the current item's batches run
+  const bool dyn = ST_DYN_ITEMS && a.item_ctr != nullptr;
+  int item = blockIdx.x * kIpWarps + wib;
+  int hb0 = 0, hb1 = 0, hrel = 0;
+  int64_t hp0 = 0;
+  auto header = [&](int it) {
+    hb0 = a.item_bin0[it];
+    hb1 = (it + 1 < n_items) ? a.item_bin0[it + 1] : nbins;
+    hp0 = a.off[hb0];
+    hrel = (lane <= hb1 - hb0) ? (int)(a.off[hb0 + lane] - hp0) : 0;
+  };
+  if (item < n_items) header(item);
+  while (item < n_items) {
+    const int b0 = hb0, b1 = hb1;
     const int nb = b1 - b0;                       // <= 8, one chunk row along +x
-    const int64_t p0 = a.off[b0];
-    const int np = (int)(a.off[b1] - p0);
+    const int64_t p0 = hp0;
+    const int myrel = hrel;
+    const int np = __shfl_sync(kFull, myrel, nb);
     const int nbatch = (np + 63) >> 6;
+    int tk = 0;
+    if (dyn && lane == 0) tk = atomicAdd(a.item_ctr, 1);   // consumed after the first batch
+    int next = item + warps_total;
+    auto prefetch = [&]() {
+      if (dyn) next = warps_total + __shfl_sync(kFull, tk, 0);
+      if (next < n_items) header(next);
+    };
     int rx, ry, rz;
     cell_of_bin(g, a.bg, b0, rx, ry, rz);
     if (lane == 0) {
@@ -94,7 +119,7 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
       }
     }
     __syncwarp();
-    if (lane <= nb) rel[lane] = (int)(a.off[b0 + lane] - p0);
+    if (lane <= nb) rel[lane] = myrel;
     if (COUNT)
       for (int k = lane; k < kTable; k += 32) cnt_s[k] = 0;
     mbar_wait(ibar, iphase);
@@ -348,7 +373,9 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
         __stcs(a.A.x + i, x[q][0]); __stcs(a.A.x + cap + i, x[q][1]); __stcs(a.A.x + 2 * cap + i, x[q][2]);
         __stcs(a.A.u + i, u[q][0]); __stcs(a.A.u + cap + i, u[q][1]); __stcs(a.A.u + 2 * cap + i, u[q][2]);
       }
+      if (bi == 0) prefetch();
     }
+    if (nbatch == 0) prefetch();
     __syncwarp();
     flush();
     __syncwarp();
@@ -359,6 +386,7 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
       }
       __syncwarp();
     }
+    item = next;
   }
   // (the chunk movers of the statistics are summed from the histogram by k_rebin_prep)
   if (COUNT && cfar) *(volatile int*)a.cnt_far = 1;
@@ -377,6 +405,7 @@ int launch_ip_variant(const StepArgs& a, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ip<BCM, SPEC, COUNT>, 32 * kIpWarps, smem);
     grid = nsm * (per > 0 ? per : 1);
   }
+  if (ST_DYN_ITEMS && a.item_ctr) cudaMemsetAsync(a.item_ctr, 0, sizeof(int), s);
   k_ip<BCM, SPEC, COUNT><<<grid, 32 * kIpWarps, smem, s>>>(a);
   return 1;
 }

@@ -130,6 +130,7 @@ struct st_ctx {
 
   // errors and counters
   int* d_err = nullptr;
+  int* item_ctr = nullptr;                  // dynamic item counter of the step kernels (reset per launch)
   int* h_flags = nullptr;     // mapped pinned: consume_flags' atomic take of d_err
   int* d_flags = nullptr;
   int64_t calls = 0, rebins = 0, launches = 0, fused_rebins = 0, last_movers = 0;
@@ -550,6 +551,7 @@ static st_status init_impl(st_ctx* c) {
   ST_CUDA(c, cudaMalloc(&c->S_dev, (size_t)3 * (c->local_cells > 0 ? c->local_cells : 1) * sizeof(float)));
   ST_CUDA(c, cudaMalloc(&c->d_err, sizeof(int)));
   ST_CUDA(c, cudaMemset(c->d_err, 0, sizeof(int)));
+  ST_CUDA(c, cudaMalloc(&c->item_ctr, sizeof(int)));
   ST_CUDA(c, cudaHostAlloc(&c->h_flags, sizeof(int), cudaHostAllocMapped));
   ST_CUDA(c, cudaHostGetDevicePointer(&c->d_flags, c->h_flags, 0));
   const size_t nb = (size_t)c->bg.nbins;
@@ -662,6 +664,7 @@ st_status st_destroy(st_ctx* c) {
     cudaFree(c->items[i]);
     cudaFree(c->n_items[i]);
   }
+  cudaFree(c->item_ctr);
   cudaFree(c->new_cnt);
   cudaFree(c->item_flag);
   cudaFree(c->item_pos);
@@ -918,6 +921,7 @@ static StepArgs step_args(st_ctx* c, float dt, int nsteps) {
   a.slot_base = c->hist;
   a.item_bin0 = c->items[c->lay];
   a.n_items = c->n_items[c->lay];
+  a.item_ctr = c->item_ctr;
   a.nbins = c->bg.nbins;
   a.field = c->front >= 0 ? c->field[c->front] : nullptr;
   a.acc = c->acc[c->acc_cur];

@@ -64,6 +64,7 @@ struct StepArgs {
   unsigned long long* cnt_far_n;
   const int* item_bin0;       // warp items of A
   const int* n_items;
+  int* item_ctr;              // or NULL: items handed out dynamically (k_ip / k_fs; zeroed per launch)
   int nbins;
   const float4* field;
   float4* acc;
