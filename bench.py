@@ -466,6 +466,7 @@ def run_ours(args):
     sampler.start()
     time.sleep(0.3)
     l0 = st.stats()["kernel_launches"]
+    c0 = st.stats()["calls"]          # first timed call in the library's trace ring
     adv, reb = [], []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -479,6 +480,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = st.stats()["kernel_launches"] - l0
+    timeline = None
+    try:   # where the step time goes between the step kernels (library event ring, st_trace)
+        tr = [st.trace(c0 + k) for k in range(min(args.steps, 60))]
+        if all(t[2] >= 0 and t[3] >= 0 for t in tr):
+            timeline = {"calls": len(tr),
+                        "advance_call_ms": float(np.mean([t[3] - t[2] for t in tr])),
+                        "gap_to_next_advance_ms": float(np.mean([tr[k + 1][2] - tr[k][3] for k in range(len(tr) - 1)]))
+                        if len(tr) > 1 else 0.0,
+                        "field_in_ms": float(np.mean([t[1] - t[0] for t in tr])),
+                        "readout_ms": float(np.mean([t[5] - t[4] for t in tr]))}
+    except Exception as ex:
+        timeline = {"error": str(ex)[:200]}
     ms = e0.elapsed_time(e1)
     n_local = st.count()
     tot = torch.tensor([ms, float(n_local)], dtype=torch.float64, device=dev)
@@ -611,6 +624,7 @@ def run_ours(args):
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
                          "alg_bytes_per_launch": alg, "kernel_ms": kms},
+            "timeline": timeline,
             "step_kernel_ms": adv_ms, "step_kernel_ms_series": [round(v, 3) for v in adv], "rebin_prep_ms": reb_ms, "rebins_in_timed_region": len(reb_list),
             "f_move_chunk": f_move, "fused_rebins": st_stats["fused_rebins"],
             "general_rebins": st_stats["general_rebins"], "far_last_rebin": st_stats["last_far"],

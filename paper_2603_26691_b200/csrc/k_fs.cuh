@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
   const int nbins = a.nbins;
   const bool two_way = a.p.two_way != 0;
   const float dt = a.dt;
+  const float2 nlo = f2(-g.lo[0], -g.lo[1]), ihv = f2(g.ih[0], g.ih[1]);
   int flags = 0;
   uint32_t phase = 0, iphase = 0;
   const unsigned lt = lanemask_lt();
@@ -191,11 +192,14 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
       bool wok[2];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          t[q][k] = cell_coord(x[q][k], g.lo[k], g.ih[k]);
-          c[q][k] = cell_from_t(t[q][k], g.n[k]);
+        {
+          const float2 txy = cell_coord2(x[q][0], x[q][1], nlo, ihv);
+          t[q][0] = txy.x;
+          t[q][1] = txy.y;
+          t[q][2] = cell_coord(x[q][2], g.lo[2], g.ih[2]);
         }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) c[q][k] = cell_from_t(t[q][k], g.n[k]);
         const int sx = rx + lb[q];
         const int j = slot_of<BCM>(g, sx, ry, rz, c[q][0], c[q][1], c[q][2]);
         const int key = lb[q] * kSlots + (j < 0 ? kStay : j);
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
 
       // ---- advance (a3-a7) ----
       const float gx = a.p.g[0], gy = a.p.g[1], gz = a.p.g[2];
+      const float2 gxy = f2(gx, gy), ngdt = f2(-gx * dt, -gy * dt);
       float tau[2], inv_tau[2], mw[2];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -283,20 +288,21 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
       }
       const int nsub = SUB ? a.nsteps : 1;
       for (int sub = 0; sub < nsub; ++sub) {
-        float4 ufq[2];
+        V3 ufq[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           if (sub > 0) {
+            const float2 txy = cell_coord2(x[q][0], x[q][1], nlo, ihv);
+            t[q][0] = txy.x;
+            t[q][1] = txy.y;
+            t[q][2] = cell_coord(x[q][2], g.lo[2], g.ih[2]);
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              t[q][k] = cell_coord(x[q][k], g.lo[k], g.ih[k]);
-              c[q][k] = cell_from_t(t[q][k], g.n[k]);
-            }
+            for (int k = 0; k < 3; ++k) c[q][k] = cell_from_t(t[q][k], g.n[k]);
           }
           int i0[3];
           float f[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) stencil_lo(t[q][k], i0[k], f[k]);
+          stencil_lo2(f2(t[q][0], t[q][1]), i0[0], i0[1], f[0], f[1]);
+          stencil_lo(t[q][2], i0[2], f[2]);
           float4 q8[8];
           const bool inw = (unsigned)(i0[0] - rx + 2) <= 10u && (unsigned)(i0[1] - ry + 2) <= 3u &&
                            (unsigned)(i0[2] - rz + 2) <= 3u;
@@ -321,42 +327,46 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
             q8[4] = ld4(fb + oz); q8[5] = ld4(fb + oz + 1); q8[6] = ld4(fb + oz + oy);
             q8[7] = ld4(fb + oz + oy + 1);
           }
-          ufq[q] = trilerp(q8, f[0], f[1], f[2]);
+          ufq[q] = trilerp3(q8, f[0], f[1], f[2]);
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const float4 uf = ufq[q];
-          const float s0 = uf.x - u[q][0], s1 = uf.y - u[q][1], s2 = uf.z - u[q][2];
+          const V3 uf = ufq[q];
+          const float2 sxy = __fadd2_rn(uf.xy, f2(-u[q][0], -u[q][1]));
+          const float s0 = sxy.x, s1 = sxy.y, s2 = uf.z - u[q][2];
           const float Re = sqrt_approx(fmaf(s0, s0, fmaf(s1, s1, s2 * s2))) * dp[q] * a.p.inv_nu;
           float fd = fmaf(0.15f, ex2_ftz(0.687f * lg2_ftz(Re)), 1.0f);
           fd = (Re <= 1000.0f) ? fd : (0.44f / 24.0f) * Re;
           fd = (a.p.drag_law == ST_DRAG_STOKES) ? 1.0f : fd;
           const float taue = tau[q] * rcp_approx(fd);
           const float h = dt * fd * inv_tau[q];
-          float du0, du1, du2;
+          float2 duxy;
+          float du2;
           if (a.p.integrator == ST_INT_EXPONENTIAL) {
             const float E = ex2_ftz(-1.44269504088896341f * h);
             const float Ms = h * (1.0f - h * (0.5f - h * (1.0f / 6.0f - h * (1.0f / 24.0f - h * (1.0f / 120.0f - h * (1.0f / 720.0f))))));
             const float M = h < 0.125f ? Ms : 1.0f - E;
             const float tM = taue * M;
-            const float us0 = fmaf(gx, taue, uf.x), us1 = fmaf(gy, taue, uf.y), us2 = fmaf(gz, taue, uf.z);
-            const float r0 = u[q][0] - us0, r1 = u[q][1] - us1, r2 = u[q][2] - us2;
-            du0 = fmaf(-M, r0, -gx * dt);
-            du1 = fmaf(-M, r1, -gy * dt);
+            const float2 usxy = __ffma2_rn(gxy, bc2(taue), uf.xy);
+            const float us2 = fmaf(gz, taue, uf.z);
+            const float2 rxy = __fadd2_rn(f2(u[q][0], u[q][1]), neg2(usxy));
+            const float r2 = u[q][2] - us2;
+            duxy = __ffma2_rn(bc2(-M), rxy, ngdt);
             du2 = fmaf(-M, r2, -gz * dt);
-            x[q][0] = fmaf(tM, r0, fmaf(us0, dt, x[q][0]));
-            x[q][1] = fmaf(tM, r1, fmaf(us1, dt, x[q][1]));
+            const float2 xn = __ffma2_rn(bc2(tM), rxy, __ffma2_rn(usxy, bc2(dt), f2(x[q][0], x[q][1])));
+            x[q][0] = xn.x;
+            x[q][1] = xn.y;
             x[q][2] = fmaf(tM, r2, fmaf(us2, dt, x[q][2]));
-            u[q][0] = fmaf(E, r0, us0);
-            u[q][1] = fmaf(E, r1, us1);
+            const float2 un = __ffma2_rn(bc2(E), rxy, usxy);
+            u[q][0] = un.x;
+            u[q][1] = un.y;
             u[q][2] = fmaf(E, r2, us2);
           } else {
             const float inv1h = rcp_approx(1.0f + h);
-            const float un0 = (u[q][0] + h * uf.x + dt * gx) * inv1h;
-            const float un1 = (u[q][1] + h * uf.y + dt * gy) * inv1h;
+            const float un0 = (u[q][0] + h * uf.xy.x + dt * gx) * inv1h;
+            const float un1 = (u[q][1] + h * uf.xy.y + dt * gy) * inv1h;
             const float un2 = (u[q][2] + h * uf.z + dt * gz) * inv1h;
-            du0 = (un0 - u[q][0]) - gx * dt;
-            du1 = (un1 - u[q][1]) - gy * dt;
+            duxy = f2((un0 - u[q][0]) - gx * dt, (un1 - u[q][1]) - gy * dt);
             du2 = (un2 - u[q][2]) - gz * dt;
             x[q][0] = fmaf(dt, un0, x[q][0]);
             x[q][1] = fmaf(dt, un1, x[q][1]);
@@ -366,10 +376,12 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
             u[q][2] = un2;
           }
           if (two_way) {
-            const float ja = -mw[q] * du0, jb = -mw[q] * du1, jc = -mw[q] * du2;
+            const float2 jxy = __fmul2_rn(bc2(-mw[q]), duxy);
+            const float ja = jxy.x, jb = jxy.y, jc = -mw[q] * du2;
             if (valid[q] && c[q][0] == rx + acb && c[q][1] == ry && c[q][2] == rz) {
-              da0 += ja;
-              da1 += jb;
+              const float2 dn = __fadd2_rn(f2(da0, da1), jxy);
+              da0 = dn.x;
+              da1 = dn.y;
               da2 += jc;
             } else if (valid[q]) {
               const int az = VP ? acc_z(g, c[q][2]) : c[q][2] - g.az0;

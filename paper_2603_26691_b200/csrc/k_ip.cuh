@@ -35,6 +35,49 @@ __device__ __forceinline__ float lg2_ftz(float x) {
 #define ST_DYN_ITEMS 1   // step kernels take their items from a counter (k_ip, k_fs)
 #endif
 
+
+// Packed fp32 pairs (FADD2 / FMUL2 / FFMA2 of sm_100): the x and y components of a
+// particle's vectors travel as one float2 and z alone, so each 3-vector operation is two
+// instructions instead of three.  Every packed operation rounds each half exactly like
+// the scalar one it replaces (same operands, same order, RN), so results are unchanged.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
+struct V3 {
+  float2 xy;
+  float z;
+};
+__device__ __forceinline__ V3 lerp3(const float4& a, const float4& b, float f) {
+  V3 r;
+  r.xy = __ffma2_rn(bc2(f), __fadd2_rn(f2(b.x, b.y), f2(-a.x, -a.y)), f2(a.x, a.y));
+  r.z = fmaf(f, b.z - a.z, a.z);
+  return r;
+}
+__device__ __forceinline__ V3 lerp3(const V3& a, const V3& b, float f) {
+  V3 r;
+  r.xy = __ffma2_rn(bc2(f), __fadd2_rn(b.xy, neg2(a.xy)), a.xy);
+  r.z = fmaf(f, b.z - a.z, a.z);
+  return r;
+}
+// C-5: the trilinear of trilerp() (same lerp tree, x then y then z)
+__device__ __forceinline__ V3 trilerp3(const float4 (&q)[8], float fx, float fy, float fz) {
+  return lerp3(lerp3(lerp3(q[0], q[1], fx), lerp3(q[2], q[3], fx), fy),
+               lerp3(lerp3(q[4], q[5], fx), lerp3(q[6], q[7], fx), fy), fz);
+}
+// C-6 cell coordinates of (x, y): (x - lo) * ih per component, each rounded (cell_coord)
+__device__ __forceinline__ float2 cell_coord2(float x, float y, float2 nlo, float2 ih) {
+  return __fmul2_rn(__fadd2_rn(f2(x, y), nlo), ih);
+}
+// stencil_lo() of (tx, ty)
+__device__ __forceinline__ void stencil_lo2(float2 t, int& i0, int& i1, float& f0, float& f1) {
+  const float2 sh = __fadd2_rn(t, bc2(-0.5f));
+  i0 = __float2int_rd(sh.x);
+  i1 = __float2int_rd(sh.y);
+  const float2 f = __fadd2_rn(sh, f2(-(float)i0, -(float)i1));
+  f0 = f.x;
+  f1 = f.y;
+}
+
 constexpr int kIpStages = 3;
 constexpr int kIpBoxF = 68;                          // 64 particles + 4 floats of 16-B alignment slack
 constexpr int kIpStageBytes = 8 * kIpBoxF * 4;       // 2176 = 17 x 128
@@ -216,6 +259,8 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
       __syncwarp();
 
       const float gx = a.p.g[0], gy = a.p.g[1], gz = a.p.g[2];
+      const float2 gxy = f2(gx, gy), ngdt = f2(-gx * dt, -gy * dt);
+      const float2 nlo = f2(-g.lo[0], -g.lo[1]), ihv = f2(g.ih[0], g.ih[1]);
       float tau[2], inv_tau[2], mw[2];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -226,16 +271,19 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
       const int nsub = SUB ? a.nsteps : 1;
       for (int sub = 0; sub < nsub; ++sub) {
         int c[2][3];
-        float4 ufq[2];
+        V3 ufq[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           int i0[3];
           float f[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const float t = cell_coord(x[q][k], g.lo[k], g.ih[k]);
-            c[q][k] = cell_from_t(t, g.n[k]);
-            stencil_lo(t, i0[k], f[k]);
+          {
+            const float2 txy = cell_coord2(x[q][0], x[q][1], nlo, ihv);
+            const float tz = cell_coord(x[q][2], g.lo[2], g.ih[2]);
+            c[q][0] = cell_from_t(txy.x, g.n[0]);
+            c[q][1] = cell_from_t(txy.y, g.n[1]);
+            c[q][2] = cell_from_t(tz, g.n[2]);
+            stencil_lo2(txy, i0[0], i0[1], f[0], f[1]);
+            stencil_lo(tz, i0[2], f[2]);
           }
           float4 q8[8];
           const bool inw = (unsigned)(i0[0] - rx + 2) <= 10u && (unsigned)(i0[1] - ry + 2) <= 3u &&
@@ -261,42 +309,46 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
             q8[4] = ld4(fb + oz); q8[5] = ld4(fb + oz + 1); q8[6] = ld4(fb + oz + oy);
             q8[7] = ld4(fb + oz + oy + 1);
           }
-          ufq[q] = trilerp(q8, f[0], f[1], f[2]);
+          ufq[q] = trilerp3(q8, f[0], f[1], f[2]);
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const float4 uf = ufq[q];
-          const float s0 = uf.x - u[q][0], s1 = uf.y - u[q][1], s2 = uf.z - u[q][2];
+          const V3 uf = ufq[q];
+          const float2 sxy = __fadd2_rn(uf.xy, f2(-u[q][0], -u[q][1]));
+          const float s0 = sxy.x, s1 = sxy.y, s2 = uf.z - u[q][2];
           const float Re = sqrt_approx(fmaf(s0, s0, fmaf(s1, s1, s2 * s2))) * dp[q] * a.p.inv_nu;
           float fd = fmaf(0.15f, ex2_ftz(0.687f * lg2_ftz(Re)), 1.0f);   // Re = 0: lg2 -> -inf, ex2 -> 0
           fd = (Re <= 1000.0f) ? fd : (0.44f / 24.0f) * Re;
           fd = (a.p.drag_law == ST_DRAG_STOKES) ? 1.0f : fd;
           const float taue = tau[q] * rcp_approx(fd);
           const float h = dt * fd * inv_tau[q];
-          float du0, du1, du2;
+          float2 duxy;
+          float du2;
           if (a.p.integrator == ST_INT_EXPONENTIAL) {
             const float E = ex2_ftz(-1.44269504088896341f * h);
             const float Ms = h * (1.0f - h * (0.5f - h * (1.0f / 6.0f - h * (1.0f / 24.0f - h * (1.0f / 120.0f - h * (1.0f / 720.0f))))));
             const float M = h < 0.125f ? Ms : 1.0f - E;
             const float tM = taue * M;
-            const float us0 = fmaf(gx, taue, uf.x), us1 = fmaf(gy, taue, uf.y), us2 = fmaf(gz, taue, uf.z);
-            const float r0 = u[q][0] - us0, r1 = u[q][1] - us1, r2 = u[q][2] - us2;
-            du0 = fmaf(-M, r0, -gx * dt);
-            du1 = fmaf(-M, r1, -gy * dt);
+            const float2 usxy = __ffma2_rn(gxy, bc2(taue), uf.xy);
+            const float us2 = fmaf(gz, taue, uf.z);
+            const float2 rxy = __fadd2_rn(f2(u[q][0], u[q][1]), neg2(usxy));
+            const float r2 = u[q][2] - us2;
+            duxy = __ffma2_rn(bc2(-M), rxy, ngdt);
             du2 = fmaf(-M, r2, -gz * dt);
-            x[q][0] = fmaf(tM, r0, fmaf(us0, dt, x[q][0]));
-            x[q][1] = fmaf(tM, r1, fmaf(us1, dt, x[q][1]));
+            const float2 xn = __ffma2_rn(bc2(tM), rxy, __ffma2_rn(usxy, bc2(dt), f2(x[q][0], x[q][1])));
+            x[q][0] = xn.x;
+            x[q][1] = xn.y;
             x[q][2] = fmaf(tM, r2, fmaf(us2, dt, x[q][2]));
-            u[q][0] = fmaf(E, r0, us0);
-            u[q][1] = fmaf(E, r1, us1);
+            const float2 un = __ffma2_rn(bc2(E), rxy, usxy);
+            u[q][0] = un.x;
+            u[q][1] = un.y;
             u[q][2] = fmaf(E, r2, us2);
           } else {
             const float inv1h = rcp_approx(1.0f + h);
-            const float un0 = (u[q][0] + h * uf.x + dt * gx) * inv1h;
-            const float un1 = (u[q][1] + h * uf.y + dt * gy) * inv1h;
+            const float un0 = (u[q][0] + h * uf.xy.x + dt * gx) * inv1h;
+            const float un1 = (u[q][1] + h * uf.xy.y + dt * gy) * inv1h;
             const float un2 = (u[q][2] + h * uf.z + dt * gz) * inv1h;
-            du0 = (un0 - u[q][0]) - gx * dt;
-            du1 = (un1 - u[q][1]) - gy * dt;
+            duxy = f2((un0 - u[q][0]) - gx * dt, (un1 - u[q][1]) - gy * dt);
             du2 = (un2 - u[q][2]) - gz * dt;
             x[q][0] = fmaf(dt, un0, x[q][0]);
             x[q][1] = fmaf(dt, un1, x[q][1]);
@@ -309,10 +361,12 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
             // reaction into the sub-step start cell (Eq. 11, C-10): the warp's accumulator
             // cell in registers, any other cell by one red.global.add.v4
             const bool v = valid[q];
-            const float ja = -mw[q] * du0, jb = -mw[q] * du1, jc = -mw[q] * du2;
+            const float2 jxy = __fmul2_rn(bc2(-mw[q]), duxy);
+            const float ja = jxy.x, jb = jxy.y, jc = -mw[q] * du2;
             if (v && c[q][0] == rx + acb && c[q][1] == ry && c[q][2] == rz) {
-              da0 += ja;
-              da1 += jb;
+              const float2 dn = __fadd2_rn(f2(da0, da1), jxy);
+              da0 = dn.x;
+              da1 = dn.y;
               da2 += jc;
             } else if (v) {
               const int az = VP ? acc_z(g, c[q][2]) : c[q][2] - g.az0;
@@ -345,8 +399,9 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
         if (COUNT) {
           // slot of the end cell relative to the particle's bin (the next rebin's input)
           const int sx = rx + lb[q];
-          const int e0 = cell_from_t(cell_coord(x[q][0], g.lo[0], g.ih[0]), g.n[0]);
-          const int e1 = cell_from_t(cell_coord(x[q][1], g.lo[1], g.ih[1]), g.n[1]);
+          const float2 exy = cell_coord2(x[q][0], x[q][1], nlo, ihv);
+          const int e0 = cell_from_t(exy.x, g.n[0]);
+          const int e1 = cell_from_t(exy.y, g.n[1]);
           const int e2 = cell_from_t(cell_coord(x[q][2], g.lo[2], g.ih[2]), g.n[2]);
           const int j = slot_of<BCM>(g, sx, ry, rz, e0, e1, e2);
           if (j == kStay && lb[q] == acb) {

@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(kDbaseBlock) k_dbase(Geom g, BinGeom bg, int n
     int sx, sy, sz;
     cell_of_bin(g, bg, s, sx, sy, sz);
     const bool cell_ok = sx < g.n[0] && sy < g.n[1] && sz < g.n[2];
+#pragma unroll
     for (int j = 0; j < kSlots; ++j) {
       bool ok = cell_ok;
       const int dx = axis_step(sx, j % 3 - 1, g.n[0], g.bc[0], ok);
@@ -651,51 +652,173 @@ __global__ void k_vcombine(Geom g, BinGeom bg, uint32_t* __restrict__ new_cnt, c
 
 // C-15b, deterministic: the fused scatter (and, across ranks, k_far_insert) placed bin
 // d's F far particles in the last F slots of d in atomic order, each with its key
-// (hi, lo) = (0, old-layout index) or (1 + source-rank order, sender's index); one thread
-// per bin sorts that tail by the key (insertion sort, payload moved with it), so the far
-// tail is kept ++ arrivals in prior store order — the (bin, far)-stable sort of the oracle.
-__global__ void k_far_order(int nbins, const int* __restrict__ far_cnt, const int64_t* __restrict__ off_new,
-                            int32_t* __restrict__ far_src, int32_t* __restrict__ far_hi, Store B, int64_t cap) {
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= nbins) return;
-  const int F = far_cnt[d];
-  if (F < 2) return;
-  const int64_t t0 = off_new[d + 1] - F;
-  auto key_of = [&](int64_t t) { return ((int64_t)far_hi[t] << 32) | (uint32_t)far_src[t]; };
-  for (int i = 1; i < F; ++i) {
-    const int64_t key = key_of(t0 + i);
-    float v[8];
-    for (int a = 0; a < 3; ++a) {
-      v[a] = B.x[a * cap + t0 + i];
-      v[3 + a] = B.u[a * cap + t0 + i];
-    }
-    v[6] = B.d[t0 + i];
-    v[7] = B.w[t0 + i];
-    const uint64_t id = B.id[t0 + i];
-    int j = i - 1;
-    for (; j >= 0 && key_of(t0 + j) > key; --j) {
-      const int64_t s = t0 + j, t = s + 1;
-      far_src[t] = far_src[s];
-      far_hi[t] = far_hi[s];
-      for (int a = 0; a < 3; ++a) {
-        B.x[a * cap + t] = B.x[a * cap + s];
-        B.u[a * cap + t] = B.u[a * cap + s];
+// (hi, lo) = (0, old-layout index) or (1 + source-rank order, sender's index); k_far_order_w
+// sorts that tail by the key (payload moved with it), so the far tail is kept ++ arrivals
+// in prior store order — the (bin, far)-stable sort of the oracle.
+// Far-tail ordering in two kernels.  k_far_order_w: persistent warps scan the bins 32 at a
+// time; a tail of F <= 32 kFarR entries is ordered by its warp — every entry's rank is the
+// number of smaller keys in the tail (keys are distinct: (0, own old index) or (1 + source
+// order, sender index)), then each entry moves once, from registers, to t0 + rank.  Longer
+// tails go to a list for k_far_order_b: one CTA per tail sorts (key, entry) pairs in shared
+// memory (bitonic), copies the tail's payload to the same indices of the old layout (free
+// after the scatter) and gathers it back in key order.  (The round-2 thread-per-bin
+// insertion sort moved O(F^2) payload per bin; at C5, K = 4, dense bins collect hundreds of
+// far particles.)
+constexpr int kFarR = 4;
+constexpr int kFarBlockMax = 4096;   // longest tail sorted in shared memory (8 + 4 B per entry)
+__device__ __forceinline__ int64_t far_key(const int32_t* far_src, const int32_t* far_hi, int64_t t) {
+  return ((int64_t)far_hi[t] << 32) | (uint32_t)far_src[t];
+}
+__device__ __forceinline__ void move_payload(const Store& from, int64_t s, const Store& to, int64_t t, int64_t cap) {
+  for (int a = 0; a < 3; ++a) {
+    to.x[a * cap + t] = from.x[a * cap + s];
+    to.u[a * cap + t] = from.u[a * cap + s];
+  }
+  to.d[t] = from.d[s];
+  to.w[t] = from.w[s];
+  to.id[t] = from.id[s];
+}
+__global__ void __launch_bounds__(256) k_far_order_w(int nbins, const int* __restrict__ far_cnt,
+                                                     const int64_t* __restrict__ off_new, int32_t* __restrict__ far_src,
+                                                     int32_t* __restrict__ far_hi, Store B, int64_t cap,
+                                                     int* __restrict__ long_list, int* __restrict__ long_n) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  for (int64_t d0 = (int64_t)gw * 32; d0 < nbins; d0 += (int64_t)nw * 32) {
+    const int64_t dl = d0 + lane;
+    const int Fl = dl < nbins ? far_cnt[dl] : 0;
+    unsigned todo = __ballot_sync(0xffffffffu, Fl >= 2);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int d = (int)(d0 + l);
+      const int F = __shfl_sync(0xffffffffu, Fl, l);
+      if (F > 32 * kFarR) {
+        if (lane == 0) long_list[atomicAdd(long_n, 1)] = d;
+        continue;
       }
-      B.d[t] = B.d[s];
-      B.w[t] = B.w[s];
-      B.id[t] = B.id[s];
-    }
-    const int64_t t = t0 + j + 1;
-    if (t != t0 + i) {
-      far_src[t] = (int32_t)(uint32_t)key;
-      far_hi[t] = (int32_t)(key >> 32);
-      for (int a = 0; a < 3; ++a) {
-        B.x[a * cap + t] = v[a];
-        B.u[a * cap + t] = v[3 + a];
+      const int64_t t0 = off_new[d + 1] - F;
+      int64_t key[kFarR];
+      int rank[kFarR];
+#pragma unroll
+      for (int r = 0; r < kFarR; ++r) {
+        const int i = lane + 32 * r;
+        key[r] = i < F ? far_key(far_src, far_hi, t0 + i) : INT64_MAX;
+        rank[r] = 0;
       }
-      B.d[t] = v[6];
-      B.w[t] = v[7];
-      B.id[t] = id;
+#pragma unroll
+      for (int r2 = 0; r2 < kFarR; ++r2) {
+        if (32 * r2 >= F) break;
+        const int m = min(32, F - 32 * r2);
+        for (int j = 0; j < m; ++j) {
+          const int64_t kj = __shfl_sync(0xffffffffu, key[r2], j);
+#pragma unroll
+          for (int r = 0; r < kFarR; ++r) rank[r] += kj < key[r];
+        }
+      }
+      float v[kFarR][8];
+      uint64_t id[kFarR];
+#pragma unroll
+      for (int r = 0; r < kFarR; ++r) {
+        const int64_t t = t0 + lane + 32 * r;
+        if (lane + 32 * r < F) {
+          for (int a = 0; a < 3; ++a) {
+            v[r][a] = B.x[a * cap + t];
+            v[r][3 + a] = B.u[a * cap + t];
+          }
+          v[r][6] = B.d[t];
+          v[r][7] = B.w[t];
+          id[r] = B.id[t];
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < kFarR; ++r) {
+        if (lane + 32 * r < F) {
+          const int64_t t = t0 + rank[r];
+          far_src[t] = (int32_t)(uint32_t)key[r];
+          far_hi[t] = (int32_t)(key[r] >> 32);
+          for (int a = 0; a < 3; ++a) {
+            B.x[a * cap + t] = v[r][a];
+            B.u[a * cap + t] = v[r][3 + a];
+          }
+          B.d[t] = v[r][6];
+          B.w[t] = v[r][7];
+          B.id[t] = id[r];
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_far_order_b(const int* __restrict__ far_cnt, const int64_t* __restrict__ off_new,
+                                                     int32_t* __restrict__ far_src, int32_t* __restrict__ far_hi,
+                                                     Store B, Store A, int64_t cap, const int* __restrict__ long_list,
+                                                     const int* __restrict__ long_n) {
+  __shared__ long long skey[kFarBlockMax];
+  __shared__ int sidx[kFarBlockMax];
+  const int nl = *long_n;
+  for (int li = blockIdx.x; li < nl; li += gridDim.x) {
+    const int d = long_list[li];
+    const int F = far_cnt[d];
+    const int64_t t0 = off_new[d + 1] - F;
+    // the tail's payload to the same indices of the old layout (scratch)
+    for (int i = threadIdx.x; i < F; i += blockDim.x) move_payload(B, t0 + i, A, t0 + i, cap);
+    if (F <= kFarBlockMax) {
+      int P = 1;
+      while (P < F) P <<= 1;
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        skey[i] = i < F ? far_key(far_src, far_hi, t0 + i) : INT64_MAX;
+        sidx[i] = i;
+      }
+      __syncthreads();
+      for (int k = 2; k <= P; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+          for (int i = threadIdx.x; i < P; i += blockDim.x) {
+            const int o = i ^ jj;
+            if (o > i) {
+              const bool up = (i & k) == 0;
+              const long long a = skey[i], b = skey[o];
+              if ((a > b) == up) {
+                skey[i] = b;
+                skey[o] = a;
+                const int t = sidx[i];
+                sidx[i] = sidx[o];
+                sidx[o] = t;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int p = threadIdx.x; p < F; p += blockDim.x) {
+        far_src[t0 + p] = (int32_t)(uint32_t)skey[p];
+        far_hi[t0 + p] = (int32_t)(skey[p] >> 32);
+        move_payload(A, t0 + sidx[p], B, t0 + p, cap);
+      }
+      __syncthreads();
+    } else {
+      // beyond the shared-memory sort: rank of every entry by counting smaller keys
+      __syncthreads();
+      for (int i = threadIdx.x; i < F; i += blockDim.x) {
+        const int64_t ki = far_key(far_src, far_hi, t0 + i);
+        int rank = 0;
+        for (int j = 0; j < F; ++j) rank += far_key(far_src, far_hi, t0 + j) < ki;
+        move_payload(A, t0 + i, B, t0 + rank, cap);
+        A.id[t0 + i] = (uint64_t)ki;   // keys kept beside the payload until every rank is known
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < F; i += blockDim.x) {
+        // the keys in rank order: re-rank from the saved copies
+        const int64_t ki = (int64_t)A.id[t0 + i];
+        int rank = 0;
+        for (int j = 0; j < F; ++j) rank += (int64_t)A.id[t0 + j] < ki;
+        far_src[t0 + rank] = (int32_t)(uint32_t)ki;
+        far_hi[t0 + rank] = (int32_t)(ki >> 32);
+      }
+      __syncthreads();
     }
   }
 }
@@ -1035,7 +1158,7 @@ __global__ void k_far_accept(Geom g, BinGeom bg, const int* __restrict__ rfv0, c
 
 // Far arrivals of one side into the far tails of B: bin = the cell the sender counted
 // them for (their position has advanced since, in the sender's fused launch), slot by
-// the bin's cursor, key (1 + source-rank order, sender's index) for k_far_order.
+// the bin's cursor, key (1 + source-rank order, sender's index) for k_far_order_w.
 __global__ void k_far_insert(FarInsertArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.count) return;
@@ -1076,11 +1199,22 @@ int launch_far_insert(const FarInsertArgs& a, cudaStream_t s) {
 }
 
 int launch_far_order(const BinGeom& bg, const int* far_cnt, const int64_t* off_new, const int32_t* far_src,
-                     const int32_t* far_src_hi, Store B, int64_t cap, cudaStream_t s) {
+                     const int32_t* far_src_hi, Store B, Store A, int64_t cap, int* long_list, int* long_n,
+                     cudaStream_t s) {
   if (!far_cnt || !far_src || bg.nbins <= 0) return 0;
-  k_far_order<<<blocks_for(bg.nbins), 256, 0, s>>>(bg.nbins, far_cnt, off_new, const_cast<int32_t*>(far_src),
-                                                   const_cast<int32_t*>(far_src_hi), B, cap);
-  return 1;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  cudaMemsetAsync(long_n, 0, sizeof(int), s);
+  const int grid = (int)std::min<int64_t>((int64_t)nsm * 8, blocks_for((int64_t)bg.nbins, 256));
+  k_far_order_w<<<grid, 256, 0, s>>>(bg.nbins, far_cnt, off_new, const_cast<int32_t*>(far_src),
+                                      const_cast<int32_t*>(far_src_hi), B, cap, long_list, long_n);
+  k_far_order_b<<<nsm, 256, 0, s>>>(far_cnt, off_new, const_cast<int32_t*>(far_src), const_cast<int32_t*>(far_src_hi),
+                                     B, A, cap, long_list, long_n);
+  return 2;
 }
 
 int launch_insert(const InsertArgs& a, cudaStream_t s) {

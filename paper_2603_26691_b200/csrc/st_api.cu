@@ -131,6 +131,8 @@ struct st_ctx {
   // errors and counters
   int* d_err = nullptr;
   int* item_ctr = nullptr;                  // dynamic item counter of the step kernels (reset per launch)
+  int* far_long = nullptr;                  // [nbins] bins whose far tail is sorted by a CTA (k_far_order_b)
+  int* far_long_n = nullptr;
   int* h_flags = nullptr;     // mapped pinned: consume_flags' atomic take of d_err
   int* d_flags = nullptr;
   int64_t calls = 0, rebins = 0, launches = 0, fused_rebins = 0, last_movers = 0;
@@ -565,6 +567,8 @@ static st_status init_impl(st_ctx* c) {
     ST_CUDA(c, cudaMalloc(&c->dtab, nb * 27 * sizeof(long long)));
     ST_CUDA(c, cudaMalloc(&c->far_cnt, nb * sizeof(int)));
     ST_CUDA(c, cudaMalloc(&c->far_cur, nb * sizeof(unsigned long long)));
+    ST_CUDA(c, cudaMalloc(&c->far_long, nb * sizeof(int)));
+    ST_CUDA(c, cudaMalloc(&c->far_long_n, sizeof(int)));
   }
   ST_CUDA(c, cudaMalloc(&c->new_cnt, (nb + 2 * (size_t)c->bg.nvb + 1) * sizeof(uint32_t)));
   if (c->bg.nvb > 0) {
@@ -665,6 +669,8 @@ st_status st_destroy(st_ctx* c) {
     cudaFree(c->n_items[i]);
   }
   cudaFree(c->item_ctr);
+  cudaFree(c->far_long);
+  cudaFree(c->far_long_n);
   cudaFree(c->new_cnt);
   cudaFree(c->item_flag);
   cudaFree(c->item_pos);
@@ -1193,7 +1199,7 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
     const int up = (r + 1 < G) ? r + 1 : (pz ? 0 : -1), dn = (r > 0) ? r - 1 : (pz ? G - 1 : -1);
     if (fr0 + fr1 > 0) {
       // far arrivals into the far tails: bin of the cell they were counted for, key
-      // (1 + order of the source rank, sender's store index) — k_far_order sorts them after
+      // (1 + order of the source rank, sender's store index) — k_far_order_w sorts them after
       // the kept far particles, by source rank, in sender order (C-16, C-15b)
       const int64_t fr[2] = {fr0, fr1};
       const int src[2] = {dn, up};
@@ -1236,7 +1242,7 @@ static st_status scatter_rebin(st_ctx* c, bool advance, float dt, int nsteps, bo
   }
   // C-15b: far tails into prior store order (after the arrivals: they precede the tail)
   if ((s = check_launch(c, launch_far_order(c->bg, c->far_cnt, c->off[nlay], c->key[0], c->key[1], c->S[1 - c->cur],
-                                            c->cap, c->cs))))
+                                            c->S[c->cur], c->cap, c->far_long, c->far_long_n, c->cs))))
     return s;
   if (advance) {
     ST_CUDA(c, cudaEventRecord(c->t_adv1, c->cs));

@@ -44,7 +44,7 @@ struct StepArgs {
   unsigned long long* far_cur;// [nbins] next free slot of each bin's far tail (C-15b), or NULL
   int32_t* far_src;           // [cap] by new-layout slot: the tail sort key (hi, lo) of a far
   int32_t* far_src_hi;        // particle: (0, old-layout index) for this rank's own, (1 + order of
-                              // the source rank, sender's index) for arrivals (k_far_order, C-15b)
+                              // the source rank, sender's index) for arrivals (k_far_order_w, C-15b)
   // multi-GPU far particles whose cell lies in a neighbour rank's slab (C-15b across ranks):
   // the scatter appends them to the far region of sbuf[side] (after the near movers),
   // fs_cur[side] = next free slot, fs_key[side][slot] = prior index (the receiver sorts by it)
@@ -83,8 +83,8 @@ int launch_vcombine(const Geom& g, const BinGeom& bg, uint32_t* new_cnt, const u
                     const int* far_cnt, cudaStream_t s);
 // C-15b: sort every bin's far tail of the new layout B by the old-layout index (far_src)
 int launch_far_order(const BinGeom& bg, const int* far_cnt, const int64_t* off_new, const int32_t* far_src,
-                     const int32_t* far_src_hi, Store B,
-                     int64_t cap, cudaStream_t s);
+                     const int32_t* far_src_hi, Store B, Store A, int64_t cap, int* long_list, int* long_n,
+                     cudaStream_t s);
 struct InsertArgs {
   Geom g;
   BinGeom bg;

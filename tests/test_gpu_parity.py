@@ -161,6 +161,45 @@ def test_far_movers_placed_in_bin_tails():
     assert st["general_rebins"] == gen0
 
 
+def test_far_tails_long_dense_bins():
+    """C-15b with long far tails (k_far_order_w / k_far_order_b): two dense cells of
+    particles (3000 and 12000) move 2.5 cells between rebins in a uniform flow, so their
+    destination bins collect ~1500 (CTA sort in shared memory) and ~6000 (beyond it)
+    far particles, over a random background.  Order bit-exact against the oracle's rule."""
+    wl = synth.workload("C2", n_particles=35_000)
+    wl.dims, wl.cell_size = (16, 16, 16), (1 / 16,) * 3
+    h, K = 1 / 16, 2
+    V = 1.25 * h / wl.dt                      # 1.25 cells per call, 2.5 per rebin interval
+    rng = np.random.default_rng(11)
+    parts = []
+    for n_c, cell in ((3000, (2, 5, 5)), (12000, (3, 9, 9))):
+        parts.append((np.asarray(cell, np.float64)[:, None] + rng.random((3, n_c))) * h)
+    parts.append(rng.random((3, 20000)) * 1.0)
+    x = np.minimum(np.concatenate(parts, axis=1), np.nextafter(1.0, 0.0)).astype(np.float32)
+    n = x.shape[1]
+    u = np.zeros((3, n), np.float32)
+    u[0] = V
+    d = np.full(n, 20e-6, np.float32)
+    w = np.ones(n, np.float32)
+    F = np.zeros((3, 16, 16, 16), np.float32)
+    F[0] = V
+    g = ScaleTrack(gpu_config(wl, capacity=n, rebin_interval=K))
+    o = oracle_sim(wl, "f32", K)
+    g.inject(x, u, d, w)
+    g.set_fluid_field(F)
+    for _ in range(K):
+        g.advance(wl.dt, 1)
+    P0 = g.get_particles()                     # flushed: home bins of the next rebin
+    for _ in range(K):
+        g.advance(wl.dt, 1)
+    after = g.get_particles()
+    nfar = _check_rebin_c15b(o, P0, after)
+    assert nfar == n and g.stats()["last_far"] == n, (nfar, g.stats()["last_far"])
+    _, cnt = np.unique(o.bin_key(after["x"]), return_counts=True)
+    assert cnt.max() > 4096, cnt.max()        # the longest tail is beyond the shared-memory sort
+    g.close()
+
+
 # ------------------------------------------------------------------ closed form through the GPU
 @pytest.mark.parametrize("drag", [0, 1])
 def test_c1_settling_terminal_velocity(drag):
