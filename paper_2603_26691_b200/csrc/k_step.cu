@@ -509,6 +509,9 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
 #include "k_fs.cuh"
 
 // ---------------------------------------------------------------- rebin preparation
+#ifndef ST_PREP_FAST
+#define ST_PREP_FAST 1   // k_rebin_prep ranks the 27 sources from per-axis counts (else 27 x 27 compares)
+#endif
 // Per destination bin d: sources s = d - delta over the 27 deltas (canonical,
 // deduplicated), in ascending s; base[j][s] = running sum; new_cnt[d] = total.
 // The slot-major layout makes consecutive threads touch consecutive words.
@@ -566,15 +569,72 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
     if ((threadIdx.x & 31) == __ffs(m) - 1 && sum) atomicAdd(movers, (unsigned long long)sum);
   }
   // stable order = ascending source bin: base of source q = sum of the counts of
-  // the sources with a smaller bin (keys are distinct), all in registers
+  // the sources with a smaller bin (keys are distinct)
   uint32_t total = 0;
+  bool fast = ST_PREP_FAST && SH == 3;
 #pragma unroll
-  for (int q = 0; q < 27; ++q) {
-    uint32_t base = 0;
+  for (int a = 0; a < 3; ++a) fast = fast && (g.bc[a] != ST_BC_PERIODIC || g.n[a] >= 3);
+  if (fast) {
+    // 8^3 chunks, three distinct source coordinates per axis: bin order is lexicographic
+    // in (kz, ky, kx, lz, ly, lx) (chunk coordinates k = c >> 3 first, then the cell in the
+    // chunk l = c & 7), so the rank of source (jx, jy, jz) among the 27 follows from
+    // per-axis counts: lt = options with a smaller k, eq = options with the same k,
+    // w = options with the same k and a smaller l (option i = source coordinate c + 1 - i,
+    // the j = (oz+1)*9 + (oy+1)*3 + (ox+1) convention with s = d - o).  Absent sources
+    // (walls, other ranks) have count 0 and any rank.
+    int lt[3][3], eq[3][3], wl[3][3];
+    const int cd[3] = {dx, dy, dz};
 #pragma unroll
-    for (int p = 0; p < 27; ++p) base += (key[p] < key[q]) ? (uint32_t)cnt[p] : 0u;
-    if (key[q] != 0x7fffffff) cnt_base[(int64_t)q * nbins + key[q]] = (int)base;
-    total += (uint32_t)cnt[q];
+    for (int a = 0; a < 3; ++a) {
+      int k[3], l[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        int sc = cd[a] + 1 - i;
+        if (g.bc[a] == ST_BC_PERIODIC) sc = sc < 0 ? sc + g.n[a] : (sc >= g.n[a] ? sc - g.n[a] : sc);
+        k[i] = sc >> 3;
+        l[i] = sc & 7;
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        lt[a][i] = 0;
+        eq[a][i] = 1;
+        wl[a][i] = 0;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+          if (o == i) continue;
+          lt[a][i] += k[o] < k[i];
+          eq[a][i] += k[o] == k[i];
+          wl[a][i] += (k[o] == k[i]) && (l[o] < l[i]);
+        }
+      }
+    }
+    int pos[27];
+    uint32_t sorted[27];
+#pragma unroll
+    for (int j = 0; j < 27; ++j) {
+      const int jx = j % 3, jy = (j / 3) % 3, jz = j / 9;
+      pos[j] = lt[2][jz] * 9 + eq[2][jz] * (lt[1][jy] * 3 + eq[1][jy] * lt[0][jx]) +
+               wl[2][jz] * eq[1][jy] * eq[0][jx] + wl[1][jy] * eq[0][jx] + wl[0][jx];
+      sorted[pos[j]] = (uint32_t)cnt[j];
+    }
+#pragma unroll
+    for (int p = 0; p < 27; ++p) {
+      const uint32_t c = sorted[p];
+      sorted[p] = total;
+      total += c;
+    }
+#pragma unroll
+    for (int q = 0; q < 27; ++q)
+      if (key[q] != 0x7fffffff) cnt_base[(int64_t)q * nbins + key[q]] = (int)sorted[pos[q]];
+  } else {
+#pragma unroll
+    for (int q = 0; q < 27; ++q) {
+      uint32_t base = 0;
+#pragma unroll
+      for (int p = 0; p < 27; ++p) base += (key[p] < key[q]) ? (uint32_t)cnt[p] : 0u;
+      if (key[q] != 0x7fffffff) cnt_base[(int64_t)q * nbins + key[q]] = (int)base;
+      total += (uint32_t)cnt[q];
+    }
   }
   // far particles of this destination (C-15b) take the slots after its 27 runs
   if (far_cnt && d < nbins) total += (uint32_t)far_cnt[d];
