@@ -47,7 +47,7 @@ def parse():
                     help="slab: z-slabs with migration (north star); sharded: every GPU holds the whole "
                          "domain, particles stay, sources all-reduced (PAPER Fig. 1c, SURVEY f2)")
     ap.add_argument("--particles", type=float, default=None, help="particles per GPU (default: the workload's)")
-    ap.add_argument("--rebin-interval", type=int, default=2,
+    ap.add_argument("--rebin-interval", type=int, default=4,
                     help="K: rebin (fused neighbour scatter) every K-th step; particles that moved more than one "
                          "cell in between go to their bin's far tail (C-15b, DESIGN.md section 9)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -585,6 +585,9 @@ def run_ours(args):
                "h2d_bytes_per_step": int(Fh[0].numel() * 4), "d2h_bytes_per_step": int(Sh.numel() * 4),
                "steps": k_e2e, "ms_per_step": ems / k_e2e, "clocks": eclocks,
                "device_ms_per_step_after": d0.elapsed_time(d1) / k_e2e}
+        # the store's cost per step drifts as the particles evolve: compare
+        # the e2e steps with the device-resident steps timed just before and just after them
+        e2e["vs_device_around"] = (ems / k_e2e) / (0.5 * (ms / args.steps + e2e["device_ms_per_step_after"])) - 1.0
         try:   # where the e2e time goes: the library's CUDA-event ring (st_trace) of these calls
             tr = [st.trace(k0 + k) for k in range(k_e2e)]
             stp = [(t[2], t[3]) for t in tr]

@@ -517,9 +517,13 @@ __global__ void __launch_bounds__(256, (SCATTER && ADVANCE) ? 3 : 4) k_step(Step
 // The slot-major layout makes consecutive threads touch consecutive words.
 // Destinations d >= nbins are the virtual bins of the neighbour planes (multi-GPU):
 // d = nbins + side * nvb + v.
+#ifndef ST_PREP_MINB
+#define ST_PREP_MINB 1
+#endif
 template <int SH>
-__global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cnt_base, uint32_t* __restrict__ new_cnt,
+__global__ void __launch_bounds__(128, ST_PREP_MINB) k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cnt_base, uint32_t* __restrict__ new_cnt,
                              const int* __restrict__ far_cnt, unsigned long long* __restrict__ movers) {
+  __shared__ uint32_t prep_rows[128 * 27];   // launched with 128 threads
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nbins + 2 * bg.nvb) return;
   int dx, dy, dz;
@@ -608,24 +612,26 @@ __global__ void k_rebin_prep(Geom g, BinGeom bg, int nbins, int* __restrict__ cn
         }
       }
     }
+    // counts scattered to their ranks in this thread's shared-memory row (stride 27
+    // words: conflict-free across the warp), scanned, gathered back
+    uint32_t* row = prep_rows + threadIdx.x * 27;
     int pos[27];
-    uint32_t sorted[27];
 #pragma unroll
     for (int j = 0; j < 27; ++j) {
       const int jx = j % 3, jy = (j / 3) % 3, jz = j / 9;
       pos[j] = lt[2][jz] * 9 + eq[2][jz] * (lt[1][jy] * 3 + eq[1][jy] * lt[0][jx]) +
                wl[2][jz] * eq[1][jy] * eq[0][jx] + wl[1][jy] * eq[0][jx] + wl[0][jx];
-      sorted[pos[j]] = (uint32_t)cnt[j];
+      row[pos[j]] = (uint32_t)cnt[j];
     }
 #pragma unroll
     for (int p = 0; p < 27; ++p) {
-      const uint32_t c = sorted[p];
-      sorted[p] = total;
+      const uint32_t c = row[p];
+      row[p] = total;
       total += c;
     }
 #pragma unroll
     for (int q = 0; q < 27; ++q)
-      if (key[q] != 0x7fffffff) cnt_base[(int64_t)q * nbins + key[q]] = (int)sorted[pos[q]];
+      if (key[q] != 0x7fffffff) cnt_base[(int64_t)q * nbins + key[q]] = (int)row[pos[q]];
   } else {
 #pragma unroll
     for (int q = 0; q < 27; ++q) {
