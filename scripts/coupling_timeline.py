@@ -39,7 +39,7 @@ def main():
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--particles", type=float, default=None)
     ap.add_argument("--steps", type=int, default=12)
-    ap.add_argument("--rebin-interval", type=int, default=2)
+    ap.add_argument("--rebin-interval", type=int, default=4)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     import torch
