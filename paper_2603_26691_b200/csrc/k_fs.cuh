@@ -78,28 +78,38 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
 
   const bool dyn = ST_DYN_ITEMS && a.item_ctr != nullptr;   // items as in k_ip
   int item = blockIdx.x * kFsWarps + wib;
-  int hb0 = 0, hb1 = 0, hrel = 0;
-  int64_t hp0 = 0;
-  auto header = [&](int it) {
+  // the next item's header in two phases, so that no load is consumed right after it is
+  // issued: its bins (after the first batch, once the counter's answer is in), then their
+  // offsets (after the second batch); consumed at the next item's start
+  int hb0 = 0, hb1 = 0;
+  int64_t hp0 = 0, hoff = 0;
+  auto header1 = [&](int it) {
     hb0 = a.item_bin0[it];
     hb1 = (it + 1 < n_items) ? a.item_bin0[it + 1] : nbins;
-    hp0 = a.off[hb0];
-    hrel = (lane <= hb1 - hb0) ? (int)(a.off[hb0 + lane] - hp0) : 0;
   };
-  if (item < n_items) header(item);
+  auto header2 = [&]() {
+    hp0 = a.off[hb0];
+    hoff = (lane <= hb1 - hb0) ? a.off[hb0 + lane] : hp0;
+  };
+  if (item < n_items) {
+    header1(item);
+    header2();
+  }
   while (item < n_items) {
     const int b0 = hb0, b1 = hb1;
-    const int nb = b1 - b0;
+    const int nb = b1 - b0;                       // <= 8, one chunk row along +x
     const int64_t p0 = hp0;
-    const int myrel = hrel;
+    const int myrel = (int)(hoff - hp0);
     const int np = __shfl_sync(kFull, myrel, nb);
     const int nbatch = (np + 63) >> 6;
     int tk = 0;
-    if (dyn && lane == 0) tk = atomicAdd(a.item_ctr, 1);
     int next = item + warps_total;
-    auto prefetch = [&]() {
+    auto prefetch1 = [&]() {
       if (dyn) next = warps_total + __shfl_sync(kFull, tk, 0);
-      if (next < n_items) header(next);
+      if (next < n_items) header1(next);
+    };
+    auto prefetch2 = [&]() {
+      if (next < n_items) header2();
     };
     int rx, ry, rz;
     cell_of_bin(g, a.bg, b0, rx, ry, rz);
@@ -111,6 +121,9 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
       for (int k = 0; k < kFsStages && k < nbatch; ++k) issue(k, p0 + 64 * k);
     }
     __syncwarp();
+    // the next item from the counter, issued after this item's copies (the proxy fence
+    // before them would otherwise wait for the atomic's round trip)
+    if (dyn && lane == 0) tk = atomicAdd(a.item_ctr, 1);
     if (lane <= nb) rel[lane] = myrel;
     for (int k = lane; k < kTable; k += 32) run[k] = 0;
     mbar_wait(ibar, iphase);
@@ -451,9 +464,11 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
         }
         __syncwarp();
       }
-      if (bi == 0) prefetch();
+      if (bi == 0) prefetch1();
+      if (bi == 1) prefetch2();
     }
-    if (nbatch == 0) prefetch();
+    if (nbatch == 0) prefetch1();
+    if (nbatch <= 1) prefetch2();
     __syncwarp();
     flush();
     __syncwarp();
