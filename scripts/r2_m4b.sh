@@ -1,0 +1,7 @@
+#!/bin/bash
+# 4-GPU box at HEAD: multi-rank GPU tests, then C5 weak scaling at N = 2 and 4 (K = 4).
+TAG=${1:-r2m4b}
+timeout 1500 python -m pytest tests/test_gpu_multirank.py -q -p no:cacheprovider > gpurun_out/${TAG}_pytest.log 2>&1
+echo "pytest multirank rc=$? $(tail -1 gpurun_out/${TAG}_pytest.log)"; grep -E "^FAILED" gpurun_out/${TAG}_pytest.log | head
+bash scripts/r2_mk.sh ${TAG}n2 2 "4"
+bash scripts/r2_mk.sh ${TAG}n4 4 "4"
