@@ -221,3 +221,50 @@ def test_far_tails_deterministic_order_fused():
         runs.append(B)
         g.close()
     assert all(np.array_equal(runs[0][k], runs[1][k]) for k in ("id", "x", "u"))
+
+
+def test_dense_bins_bench_interval_k4():
+    """The bench's default rebin interval (K = 4) at ~362 particles/cell: 10 free-running
+    calls (general rebin at call 4, the fused rebin + advance at call 9) against the
+    fp32 oracle (x within 1e-5 of L, the same particles), then the fused launch's order
+    bit-exact given the GPU's own positions (C-15 / C-15b, far tails included)."""
+    wl = _dense_workload()
+    g, o, F = _setup(wl, 4)
+    for _ in range(10):
+        g.advance(wl.dt, 1)
+        o.advance(wl.dt, 1)
+    st = g.stats()
+    assert st["fused_rebins"] >= 1, st
+    a, b = by_id(g.get_particles()), by_id(o.particles())
+    assert np.array_equal(a["id"], b["id"])
+    # C-11 (see test_dense_bins_free_running): a particle whose fp32 position lands within
+    # an ulp of a wall may be reflected on one side only; the flipped velocity then meets
+    # the drag of the next sub-step and shifts that axis' position by up to ~2 tau |u|
+    # (measured on this case: 1 particle of 5e6, 3e-4 m at the y wall, the same at K = 1, 2,
+    # 3 and 4).  Such offsets are allowed only on an axis whose wall the particle is near,
+    # and only for a handful of particles; every other coordinate within 1e-5 of L.
+    U = float(np.max(np.linalg.norm(F.reshape(3, -1), axis=0)))
+    L = np.array(wl.lengths)[:, None]
+    lo = np.array(wl.origin)[:, None]
+    dx = np.abs(a["x"].astype(np.float64) - b["x"]) / L
+    near = np.minimum(b["x"] - lo, lo + L - b["x"]) < 10 * 1.5 * U * wl.dt
+    bad = dx > 1e-5
+    assert not np.any(bad & ~near), float(np.max(np.where(near, 0.0, dx)))
+    assert int(bad.any(axis=0).sum()) <= max(2, int(1e-5 * a["x"].shape[1])), int(bad.any(axis=0).sum())
+    g.close()
+    # the order of one fused launch at this density: positions pinned by dt = 1e-9 calls
+    g, o, F = _setup(wl, 4)
+    tiny = 1e-9
+    for _ in range(3):
+        g.advance(wl.dt, 1)
+    g.advance(tiny, 1)              # call 4: general rebin of call-3 positions, nothing moved
+    A = g.get_particles()
+    for _ in range(3):
+        g.advance(wl.dt, 1)         # calls 5-7 in place
+    g.advance(tiny, 1)              # call 8 in place, counts the slots -> rebin due
+    g.advance(tiny, 1)              # call 9: FUSED rebin, moves nothing
+    B = g.get_particles()
+    want, nfar = _expected_order(o, A, B)
+    assert np.array_equal(B["id"], want)
+    assert g.stats()["last_far"] == nfar
+    g.close()
