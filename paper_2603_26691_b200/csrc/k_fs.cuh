@@ -20,9 +20,6 @@
 #ifndef ST_FS_WARPS
 #define ST_FS_WARPS 10   // A/B at C5 K = 3 (r2y): 10 warps 1 % faster than 8; 12 and 2-stage 16 slower
 #endif
-#ifndef ST_FS_EARLY_REFILL
-#define ST_FS_EARLY_REFILL 0   // 1: ids loaded with the floats, the stage refilled before the scatter
-#endif
 constexpr int kFsStages = ST_FS_STAGES;
 constexpr int kFsBoxI = 66;                                   // 64 ids + 2 of alignment slack
 constexpr int kFsStageBytes = (8 * kIpBoxF * 4 + kFsBoxI * 8 + 127) / 128 * 128;   // 2176 + 528 -> 2816
@@ -198,20 +195,6 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
             u[q][0] = m[3]; u[q][1] = m[4]; u[q][2] = m[5];
             dp[q] = m[6]; wp[q] = m[7];
           }
-      }
-      unsigned long long pid_e[2] = {0ull, 0ull};
-      if (ST_FS_EARLY_REFILL) {
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-          asm volatile("ld.shared.u64 %0, [%1];"
-                       : "=l"(pid_e[q])
-                       : "r"(stage0 + sk * kFsStageBytes + kFsOffId + 8u * (uint32_t)(((p0 + base) & 1) + 32 * q + lane)));
-        __syncwarp();
-        if (lane == 0 && bi + kFsStages < nbatch) {
-          if (ST_REFILL_FENCE) fence_proxy_async();
-          issue(sk, p0 + base + 64 * kFsStages);
-        }
-        __syncwarp();
       }
 
       // ---- rebin scatter (a8): destination of each particle from its current cell ----
@@ -441,11 +424,10 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         if (!wok[q]) continue;
-        unsigned long long pid = pid_e[q];
-        if (!ST_FS_EARLY_REFILL)
-          asm volatile("ld.shared.u64 %0, [%1];"
-                       : "=l"(pid)
-                       : "r"(stage0 + sk * kFsStageBytes + kFsOffId + 8u * (uint32_t)(((p0 + base) & 1) + 32 * q + lane)));
+        unsigned long long pid;
+        asm volatile("ld.shared.u64 %0, [%1];"
+                     : "=l"(pid)
+                     : "r"(stage0 + sk * kFsStageBytes + kFsOffId + 8u * (uint32_t)(((p0 + base) & 1) + 32 * q + lane)));
         const Store& o = (VP && vside[q] >= 0) ? a.sbuf[vside[q]] : a.B;
         const int64_t oc = (VP && vside[q] >= 0) ? a.scap : a.cap;
         const int64_t dd = dest[q];
@@ -456,14 +438,12 @@ __global__ void __launch_bounds__(32 * kFsWarps, kFsWarps > 8 ? 1 : 2) k_fs(cons
         reinterpret_cast<unsigned long long*>(o.id)[dd] = pid;
       }
       // the stage is consumed (ids read last): refill it with the batch kFsStages ahead
-      if (!ST_FS_EARLY_REFILL) {
-        __syncwarp();
-        if (lane == 0 && bi + kFsStages < nbatch) {
-          if (ST_REFILL_FENCE) fence_proxy_async();
-          issue(sk, p0 + base + 64 * kFsStages);
-        }
-        __syncwarp();
+      __syncwarp();
+      if (lane == 0 && bi + kFsStages < nbatch) {
+        fence_proxy_async();
+        issue(sk, p0 + base + 64 * kFsStages);
       }
+      __syncwarp();
       if (bi == 0) prefetch1();
       if (bi == 1) prefetch2();
     }

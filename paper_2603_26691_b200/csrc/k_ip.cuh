@@ -31,9 +31,6 @@ __device__ __forceinline__ float lg2_ftz(float x) {
   return r;
 }
 
-#ifndef ST_REFILL_FENCE
-#define ST_REFILL_FENCE 1      // fence.proxy.async before a stage refill (MEMBAR.ALL.CTA in SASS)
-#endif
 #ifndef ST_DYN_ITEMS
 #define ST_DYN_ITEMS 1   // step kernels take their items from a counter (k_ip, k_fs)
 #endif
@@ -268,7 +265,7 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
       }
       __syncwarp();
       if (lane == 0 && bi + kIpStages < nbatch) {
-        if (ST_REFILL_FENCE) fence_proxy_async();
+        fence_proxy_async();
         mbar_expect_tx(bar + sk, kIpTx);
         tma_rows(ws + sk * kIpStageBytes, &a.tm_f64, (int)((p0 + base + 64 * kIpStages) & ~3LL), bar + sk);
       }
