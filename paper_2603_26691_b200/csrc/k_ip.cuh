@@ -449,10 +449,12 @@ __global__ void __launch_bounds__(32 * kIpWarps, 2) k_ip(const __grid_constant__
     __syncwarp();
     flush();
     __syncwarp();
-    if (COUNT) {   // the item's bins are this warp's: plain stores, every entry
-      for (int k = lane; k < nb * kSlots; k += 32) {
-        const int l = k / kSlots, j = k - l * kSlots;
-        a.cnt_hist[(int64_t)j * nbins + b0 + l] = cnt_s[k];
+    if (COUNT) {   // the item's bins are this warp's: plain stores, every entry; lanes
+      // 8s..8s+7 write one slot row's 8 consecutive bins (one 32-B sector of the slot-major
+      // histogram) instead of 32 different rows
+      for (int k = lane; k < kSlots * kRowBins; k += 32) {
+        const int j = k >> 3, l = k & 7;
+        if (l < nb) a.cnt_hist[(int64_t)j * nbins + b0 + l] = cnt_s[l * kSlots + j];
       }
       __syncwarp();
     }
