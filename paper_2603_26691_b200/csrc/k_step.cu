@@ -539,10 +539,41 @@ __global__ void __launch_bounds__(128, ST_PREP_MINB) k_rebin_prep(Geom g, BinGeo
     return;
   }
   const int kz_lo = bg.kz0, kz_hi = bg.kz0 + bg.nkz;
+  bool fast = ST_PREP_FAST && SH == 3;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) fast = fast && (g.bc[a] != ST_BC_PERIODIC || g.n[a] >= 3);
+  // per axis a and option i (source coordinate c + 1 - i, the j convention below): chunk /
+  // in-chunk coordinate, presence, and its term of the bin index (8^3 chunks: bin =
+  // sum over axes of chunk stride * k + cell stride * l), so a source's key is two adds
+  int ka[3][3], la[3][3], pa[3][3];
+  bool oa[3][3];
+  if (fast) {
+    const int cd[3] = {dx, dy, dz};
+    const int cs[3] = {bg.cc3, bg.cc3 * g.NC[0], bg.cc3 * g.NC[0] * g.NC[1]};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        int sc = cd[a] + 1 - i;
+        if (g.bc[a] == ST_BC_PERIODIC) sc = sc < 0 ? sc + g.n[a] : (sc >= g.n[a] ? sc - g.n[a] : sc);
+        ka[a][i] = sc >> 3;
+        la[a][i] = sc & 7;
+        oa[a][i] = sc >= 0 && sc < g.n[a] && (a < 2 || (ka[a][i] >= kz_lo && ka[a][i] < kz_hi));
+        pa[a][i] = cs[a] * (a == 2 ? ka[a][i] - kz_lo : ka[a][i]) + (a == 0 ? 1 : (a == 1 ? 8 : 64)) * la[a][i];
+      }
+    }
+  }
   // the 27 candidate sources s = d - delta(j); key = bin (INT_MAX if absent)
   int key[27], cnt[27];
 #pragma unroll
   for (int j = 0; j < 27; ++j) {
+    if (fast) {
+      const int jx = j % 3, jy = (j / 3) % 3, jz = j / 9;
+      const bool ok = oa[0][jx] && oa[1][jy] && oa[2][jz];
+      key[j] = ok ? pa[0][jx] + pa[1][jy] + pa[2][jz] : 0x7fffffff;
+      cnt[j] = ok ? cnt_base[(int64_t)j * nbins + key[j]] : 0;
+      continue;
+    }
     const int ox = j % 3 - 1, oy = (j / 3) % 3 - 1, oz = j / 9 - 1;
     bool ok = true;
     const int sx = axis_step(dx, -ox, g.n[0], g.bc[0], ok);
@@ -575,9 +606,6 @@ __global__ void __launch_bounds__(128, ST_PREP_MINB) k_rebin_prep(Geom g, BinGeo
   // stable order = ascending source bin: base of source q = sum of the counts of
   // the sources with a smaller bin (keys are distinct)
   uint32_t total = 0;
-  bool fast = ST_PREP_FAST && SH == 3;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) fast = fast && (g.bc[a] != ST_BC_PERIODIC || g.n[a] >= 3);
   if (fast) {
     // 8^3 chunks, three distinct source coordinates per axis: bin order is lexicographic
     // in (kz, ky, kx, lz, ly, lx) (chunk coordinates k = c >> 3 first, then the cell in the
@@ -587,17 +615,10 @@ __global__ void __launch_bounds__(128, ST_PREP_MINB) k_rebin_prep(Geom g, BinGeo
     // the j = (oz+1)*9 + (oy+1)*3 + (ox+1) convention with s = d - o).  Absent sources
     // (walls, other ranks) have count 0 and any rank.
     int lt[3][3], eq[3][3], wl[3][3];
-    const int cd[3] = {dx, dy, dz};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      int k[3], l[3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        int sc = cd[a] + 1 - i;
-        if (g.bc[a] == ST_BC_PERIODIC) sc = sc < 0 ? sc + g.n[a] : (sc >= g.n[a] ? sc - g.n[a] : sc);
-        k[i] = sc >> 3;
-        l[i] = sc & 7;
-      }
+      const int* k = ka[a];
+      const int* l = la[a];
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         lt[a][i] = 0;
